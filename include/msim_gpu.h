@@ -1,0 +1,253 @@
+/*
+ * msim_gpu.h — C ABI of the B200-native MLS-MPM soft-body substep.
+ *
+ * This is the drop-in boundary for the hot path of the reference simulator
+ * ("msim", /root/reference/proj). The reference is a header-only C++ library
+ * whose soft-body path is entered through these C++ symbols; each entry
+ * point below replaces one of them (file:line relative to
+ * /root/reference/proj/include/msim/):
+ *
+ *   msim_gpu_create            SoftState{} + MpmGrid{} + Material{}        mpm.hpp:24-145
+ *                              (grid/step parameters, validate())          mpm.hpp:35-41, :103-106
+ *   msim_gpu_set_particles     SoftState::particles + init_buffers()       mpm.hpp:111-142
+ *   msim_gpu_set_bodies        World::bodies + BodyMirror shapes           coupling.hpp:54-104
+ *   msim_gpu_set_coupling      World::coupling (CouplingConfig)            coupling.hpp:20-26
+ *   msim_gpu_sync_bodies       sync_rigid_to_soft(World&)                  coupling.hpp:106-117
+ *   msim_gpu_soft_substep      soft_substep(st, particle_hook, grid_hook)  mpm.hpp:397-421
+ *                              with penalty_particle / penalty_grid hooks  coupling.hpp:151-214
+ *   msim_gpu_p2g               p2g(SoftState&)                             mpm.hpp:199-311
+ *   msim_gpu_grid_update       grid_update(SoftState&)                     mpm.hpp:315-342
+ *   msim_gpu_g2p               g2p_advect(SoftState&)                      mpm.hpp:346-379
+ *   msim_gpu_env_step          the rigid/soft part of env_step             coupling.hpp:248-293
+ *                              (integrate_free_body, sync, substeps,       rigid.hpp:52-66
+ *                               pending_wrenches staging)
+ *   msim_gpu_read_*            direct access to SoftState / MpmGrid /      mpm.hpp:76-79, :111-135
+ *                              World::wrenches fields                      coupling.hpp:69-70
+ *
+ * Conventions
+ *   - Plain C: POD structs, pointers + sizes, no exceptions cross the ABI.
+ *   - Return codes follow the reference CLI (tools/main.cpp:16):
+ *       MSIM_OK = 0, MSIM_ERR_INVALID = 2 (std::invalid_argument),
+ *       MSIM_ERR_DIVERGED = 3 (SimulationDiverged), MSIM_ERR_DEVICE = 4 (CUDA).
+ *     The message (with the first offending particle index where the
+ *     reference reports one) is available from msim_gpu_last_error().
+ *   - Host arrays are double precision, caller-owned, copied in/out.
+ *     Vectors are packed xyz; 3x3 matrices are row-major (M[r*3+c]).
+ *     On the device the state is fp32 structure-of-arrays.
+ *   - One context owns one device, one stream and a batch of n_env
+ *     independent environments ("worlds") sharing one grid description.
+ *     A context is not reentrant; distinct contexts may step concurrently.
+ */
+#ifndef MSIM_GPU_H
+#define MSIM_GPU_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MSIM_OK 0
+#define MSIM_ERR_INVALID 2
+#define MSIM_ERR_DIVERGED 3
+#define MSIM_ERR_DEVICE 4
+
+/* BoundaryKind, mpm.hpp:60 */
+#define MSIM_BOUNDARY_STICKY 0
+#define MSIM_BOUNDARY_SLIP 1
+
+/* CouplingMode, coupling.hpp:18 */
+#define MSIM_COUPLING_PARTICLE 0
+#define MSIM_COUPLING_GRID 1
+
+/* ShapeGeom variant order, sdf.hpp:65-83 */
+#define MSIM_SHAPE_PLANE 0
+#define MSIM_SHAPE_SPHERE 1
+#define MSIM_SHAPE_BOX 2
+#define MSIM_SHAPE_CAPSULE 3
+#define MSIM_SHAPE_VOLUME 4
+
+/* BodyMode, rigid.hpp:11. SCRIPTED is a harness extension: a kinematic body
+ * whose pose advances with its own constant twist every rigid step (the
+ * synthetic stand-in for a robot-driven link, rigid.hpp:142-151). */
+#define MSIM_BODY_DYNAMIC 0
+#define MSIM_BODY_KINEMATIC 1
+#define MSIM_BODY_SCRIPTED 2
+
+/* Constitutive model selector. HENCKY_VON_MISES is the reference's only
+ * model (mpm.hpp:150-181). */
+#define MSIM_MODEL_HENCKY_VON_MISES 0
+
+/* MpmGrid (mpm.hpp:65-107) + SoftState stepping parameters (mpm.hpp:115-120). */
+typedef struct msim_soft_desc {
+  double h;                        /* cell length */
+  int32_t dims[3];                 /* nodes per axis, >= 4 */
+  double origin[3];
+  uint8_t boundary[6];             /* x-, x+, y-, y+, z-, z+ */
+  uint8_t _pad[2];
+  double gravity[3];
+  double dt;
+  double cfl_factor;               /* 0.4 */
+  int32_t max_cfl_halvings;        /* 4 */
+  int32_t _pad2;
+  double lost_fraction_threshold;  /* 0.01 */
+} msim_soft_desc;
+
+/* Material (mpm.hpp:24-42). */
+typedef struct msim_material {
+  double density;
+  double youngs;
+  double poisson;
+  double yield_stress;
+  int32_t model;
+  int32_t _pad;
+} msim_material;
+
+/* Shape (sdf.hpp:87-110) with its geometry flattened.
+ *   plane:   params = normal xyz, offset
+ *   sphere:  params[0] = radius
+ *   box:     params = half extents xyz
+ *   capsule: params[0] = half_length (local z), params[1] = radius
+ *   volume:  vol_* fields; samples f32 x-fastest (sdf.hpp:20-30), copied. */
+typedef struct msim_shape {
+  int32_t type;
+  int32_t body;                    /* body index within its environment */
+  double local_q[4];               /* w x y z */
+  double local_t[3];
+  double friction;                 /* 0.5 */
+  double k_n;                      /* 1e3 */
+  double k_t;                      /* 10 */
+  double params[4];
+  int32_t vol_dims[3];
+  int32_t _pad;
+  double vol_origin[3];
+  double vol_voxel;
+  const float* vol_samples;
+} msim_shape;
+
+/* RigidBody (rigid.hpp:25-43). */
+typedef struct msim_body {
+  int32_t mode;
+  int32_t _pad;
+  double q[4];                     /* w x y z */
+  double t[3];
+  double v[3];
+  double w[3];
+  double mass;
+  double inertia[3];               /* body-frame principal */
+  double com_offset[3];            /* body frame */
+} msim_body;
+
+/* CouplingConfig (coupling.hpp:20-26). */
+typedef struct msim_coupling {
+  int32_t mode;
+  int32_t _pad;
+  double r_c_factor;               /* 0.5 */
+  double c_d;                      /* 10 */
+} msim_coupling;
+
+/* StepReport (coupling.hpp:41-50), rigid/soft fields; summed/maxed over
+ * environments for batched contexts (per-env values via msim_gpu_read_report). */
+typedef struct msim_step_report {
+  int32_t rigid_steps;
+  int32_t soft_substeps;
+  int32_t cfl_cycles;
+  int32_t _pad;
+  double max_penetration;
+  double max_force_balance_error;
+  int64_t lost_particles;
+} msim_step_report;
+
+typedef struct msim_gpu_ctx msim_gpu_ctx;
+
+/* ---- lifecycle ---------------------------------------------------------- */
+int msim_gpu_create(const msim_soft_desc* desc, const msim_material* materials, int n_materials,
+                    int n_env, int device, msim_gpu_ctx** out);
+void msim_gpu_destroy(msim_gpu_ctx* ctx);
+const char* msim_gpu_last_error(const msim_gpu_ctx* ctx);
+/* Error from a failed msim_gpu_create (no context exists yet). */
+const char* msim_gpu_create_error(void);
+int msim_gpu_version(void);
+
+/* ---- state setup -------------------------------------------------------- */
+/* All environments at once: env_offsets[n_env+1] partitions the n particles.
+ * x, v: n*3; F, C: n*9 (row-major); mass, vol0: n; material: n (may be NULL). */
+int msim_gpu_set_particles(msim_gpu_ctx* ctx, int64_t n, const int64_t* env_offsets,
+                           const double* x, const double* v, const double* F, const double* C,
+                           const double* mass, const double* vol0, const int32_t* material);
+/* Overwrite one environment's particles (count must match). */
+int msim_gpu_write_particles(msim_gpu_ctx* ctx, int env, int64_t n, const double* x,
+                             const double* v, const double* F, const double* C);
+/* Bodies + shapes of one environment; shape.body indexes into bodies. The
+ * body order is the contact order (coupling.hpp:75-90). Resets wrenches. */
+int msim_gpu_set_bodies(msim_gpu_ctx* ctx, int env, const msim_body* bodies, int n_bodies,
+                        const msim_shape* shapes, int n_shapes);
+int msim_gpu_set_coupling(msim_gpu_ctx* ctx, const msim_coupling* coupling);
+/* sync_rigid_to_soft: overwrite body state (pose/twist) of one env and zero
+ * its accumulating wrenches. */
+int msim_gpu_sync_bodies(msim_gpu_ctx* ctx, int env, const msim_body* bodies, int n_bodies);
+int msim_gpu_set_dt(msim_gpu_ctx* ctx, double dt);
+int msim_gpu_set_gravity(msim_gpu_ctx* ctx, const double* g3);
+int msim_gpu_set_lost_fraction_threshold(msim_gpu_ctx* ctx, double threshold);
+
+/* ---- stepping ----------------------------------------------------------- */
+/* n_substeps x soft_substep with the configured penalty hook, all envs.
+ * cycles_out (may be NULL) receives the per-env cycle count of the LAST substep. */
+int msim_gpu_soft_substep(msim_gpu_ctx* ctx, int n_substeps, int32_t* cycles_out);
+/* Hook-free phases for direct solver use (acceptance.cpp:81, test_mpm.cpp). */
+int msim_gpu_p2g(msim_gpu_ctx* ctx);
+int msim_gpu_grid_update(msim_gpu_ctx* ctx);
+int msim_gpu_g2p(msim_gpu_ctx* ctx);
+/* The soft/rigid part of env_step (coupling.hpp:248-293) for all envs:
+ * n_rigid x { integrate dynamic + scripted bodies with the staged wrenches,
+ * sync, n_soft substeps, stage wrenches }. Device-resident: no host round
+ * trip per rigid step. */
+int msim_gpu_env_step(msim_gpu_ctx* ctx, int n_rigid, int n_soft, msim_step_report* report);
+
+/* ---- readback ----------------------------------------------------------- */
+int64_t msim_gpu_particle_count(const msim_gpu_ctx* ctx, int env);
+int msim_gpu_read_particles(msim_gpu_ctx* ctx, int env, double* x, double* v, double* F,
+                            double* C, uint8_t* lost);
+/* Dense per-env grid channels (node_count doubles / node_count*3). velocity
+ * is written by grid_update; mass/momentum/force by p2g (+ grid hook). Any
+ * pointer may be NULL. Momentum/force are only kept separately in "split"
+ * mode (grid coupling or msim_gpu_set_split_channels(ctx,1)). */
+int msim_gpu_read_grid(msim_gpu_ctx* ctx, int env, double* mass, double* momentum, double* force,
+                       double* velocity);
+int msim_gpu_write_grid_velocity(msim_gpu_ctx* ctx, int env, const double* velocity);
+int msim_gpu_set_split_channels(msim_gpu_ctx* ctx, int split);
+/* Integer binning of the last p2g, in the reference layout (mpm.hpp:210-280):
+ * base[n*3] (lost = -10), cell_start[bins+1], cell_particles[n_alive],
+ * active_nodes[n_active] ascending. Capacities are checked; counts returned. */
+int msim_gpu_read_binning(msim_gpu_ctx* ctx, int env, int32_t* base, int32_t* cell_start,
+                          int64_t cell_start_cap, int32_t* cell_particles, int64_t cell_particles_cap,
+                          int64_t* n_alive, int64_t* active_nodes, int64_t active_cap,
+                          int64_t* n_active);
+int msim_gpu_read_wrenches(msim_gpu_ctx* ctx, int env, int pending, double* force,
+                           double* torque);
+int msim_gpu_read_bodies(msim_gpu_ctx* ctx, int env, msim_body* bodies, int n_bodies);
+int msim_gpu_read_report(msim_gpu_ctx* ctx, int env, msim_step_report* report);
+int64_t msim_gpu_lost_count(msim_gpu_ctx* ctx, int env);
+
+/* ---- test hooks (constitutive model on raw arrays, device code path) ---- */
+/* tau[n*9] = kirchhoff_stress(F), Fp[n*9] = von_mises_return_map(F) for material
+ * `mat`. Returns MSIM_ERR_INVALID if some det(F) <= 0. */
+int msim_gpu_constitutive(msim_gpu_ctx* ctx, int mat, int64_t n, const double* F, double* tau,
+                          double* Fp);
+
+/* ---- host-side reference utilities (no device work) --------------------- */
+/* seed_particles_box (seeding.hpp:13-35) with a caller-held mt19937_64 state.
+ * Returns the particle count; if x != NULL writes positions (n*3) and mass. */
+typedef struct msim_rng msim_rng;
+msim_rng* msim_rng_create(uint64_t seed);
+void msim_rng_destroy(msim_rng* rng);
+double msim_rng_uniform(msim_rng* rng, double lo, double hi);
+int64_t msim_seed_box_count(const double* box_min, const double* box_max, double particle_volume);
+int64_t msim_seed_box(msim_rng* rng, const double* box_min, const double* box_max,
+                      double density, double particle_volume, double* x, double* mass);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* MSIM_GPU_H */
