@@ -187,6 +187,8 @@ int msim_gpu_set_coupling(msim_gpu_ctx* ctx, const msim_coupling* coupling);
  * its accumulating wrenches. */
 int msim_gpu_sync_bodies(msim_gpu_ctx* ctx, int env, const msim_body* bodies, int n_bodies);
 int msim_gpu_set_dt(msim_gpu_ctx* ctx, double dt);
+/* World::rigid_gravity (coupling.hpp:60), used by msim_gpu_env_step. */
+int msim_gpu_set_rigid_gravity(msim_gpu_ctx* ctx, const double* g3);
 int msim_gpu_set_gravity(msim_gpu_ctx* ctx, const double* g3);
 int msim_gpu_set_lost_fraction_threshold(msim_gpu_ctx* ctx, double threshold);
 
@@ -216,6 +218,9 @@ int msim_gpu_read_grid(msim_gpu_ctx* ctx, int env, double* mass, double* momentu
                        double* velocity);
 int msim_gpu_write_grid_velocity(msim_gpu_ctx* ctx, int env, const double* velocity);
 int msim_gpu_set_split_channels(msim_gpu_ctx* ctx, int split);
+/* Record per-particle base cells during binning so msim_gpu_read_binning can
+ * rebuild the reference layout (inspection; costs 12 B/particle/cycle). */
+int msim_gpu_set_record_binning(msim_gpu_ctx* ctx, int on);
 /* Integer binning of the last p2g, in the reference layout (mpm.hpp:210-280):
  * base[n*3] (lost = -10), cell_start[bins+1], cell_particles[n_alive],
  * active_nodes[n_active] ascending. Capacities are checked; counts returned. */
@@ -242,6 +247,8 @@ typedef struct msim_rng msim_rng;
 msim_rng* msim_rng_create(uint64_t seed);
 void msim_rng_destroy(msim_rng* rng);
 double msim_rng_uniform(msim_rng* rng, double lo, double hi);
+/* n successive msim_rng_uniform(lo, hi) draws. */
+void msim_rng_fill_uniform(msim_rng* rng, int64_t n, double lo, double hi, double* out);
 int64_t msim_seed_box_count(const double* box_min, const double* box_max, double particle_volume);
 int64_t msim_seed_box(msim_rng* rng, const double* box_min, const double* box_max,
                       double density, double particle_volume, double* x, double* mass);

@@ -1,0 +1,218 @@
+"""ctypes mirror of include/msim_gpu.h and the loader for libmsim_gpu.so.
+
+The shared library is built in-tree (``make -C paper_2302_04659_b200``, or
+``__graft_entry__.build()``). There is no fallback: if the library is missing
+or fails to load, importing the package raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libmsim_gpu.so")
+
+MSIM_OK = 0
+MSIM_ERR_INVALID = 2
+MSIM_ERR_DIVERGED = 3
+MSIM_ERR_DEVICE = 4
+
+BOUNDARY_STICKY = 0
+BOUNDARY_SLIP = 1
+COUPLING_PARTICLE = 0
+COUPLING_GRID = 1
+SHAPE_PLANE, SHAPE_SPHERE, SHAPE_BOX, SHAPE_CAPSULE, SHAPE_VOLUME = range(5)
+BODY_DYNAMIC, BODY_KINEMATIC, BODY_SCRIPTED = range(3)
+
+
+class SoftDesc(C.Structure):
+    _fields_ = [
+        ("h", C.c_double),
+        ("dims", C.c_int32 * 3),
+        ("origin", C.c_double * 3),
+        ("boundary", C.c_uint8 * 6),
+        ("_pad", C.c_uint8 * 2),
+        ("gravity", C.c_double * 3),
+        ("dt", C.c_double),
+        ("cfl_factor", C.c_double),
+        ("max_cfl_halvings", C.c_int32),
+        ("_pad2", C.c_int32),
+        ("lost_fraction_threshold", C.c_double),
+    ]
+
+
+class Material(C.Structure):
+    _fields_ = [
+        ("density", C.c_double),
+        ("youngs", C.c_double),
+        ("poisson", C.c_double),
+        ("yield_stress", C.c_double),
+        ("model", C.c_int32),
+        ("_pad", C.c_int32),
+    ]
+
+
+class Shape(C.Structure):
+    _fields_ = [
+        ("type", C.c_int32),
+        ("body", C.c_int32),
+        ("local_q", C.c_double * 4),
+        ("local_t", C.c_double * 3),
+        ("friction", C.c_double),
+        ("k_n", C.c_double),
+        ("k_t", C.c_double),
+        ("params", C.c_double * 4),
+        ("vol_dims", C.c_int32 * 3),
+        ("_pad", C.c_int32),
+        ("vol_origin", C.c_double * 3),
+        ("vol_voxel", C.c_double),
+        ("vol_samples", C.POINTER(C.c_float)),
+    ]
+
+
+class Body(C.Structure):
+    _fields_ = [
+        ("mode", C.c_int32),
+        ("_pad", C.c_int32),
+        ("q", C.c_double * 4),
+        ("t", C.c_double * 3),
+        ("v", C.c_double * 3),
+        ("w", C.c_double * 3),
+        ("mass", C.c_double),
+        ("inertia", C.c_double * 3),
+        ("com_offset", C.c_double * 3),
+    ]
+
+
+class Coupling(C.Structure):
+    _fields_ = [
+        ("mode", C.c_int32),
+        ("_pad", C.c_int32),
+        ("r_c_factor", C.c_double),
+        ("c_d", C.c_double),
+    ]
+
+
+class StepReport(C.Structure):
+    _fields_ = [
+        ("rigid_steps", C.c_int32),
+        ("soft_substeps", C.c_int32),
+        ("cfl_cycles", C.c_int32),
+        ("_pad", C.c_int32),
+        ("max_penetration", C.c_double),
+        ("max_force_balance_error", C.c_double),
+        ("lost_particles", C.c_int64),
+    ]
+
+
+# Every symbol include/msim_gpu.h declares (checked by tests/test_abi.py).
+EXPORTED = [
+    "msim_gpu_create", "msim_gpu_destroy", "msim_gpu_last_error", "msim_gpu_create_error",
+    "msim_gpu_version", "msim_gpu_set_particles", "msim_gpu_write_particles",
+    "msim_gpu_set_bodies", "msim_gpu_set_coupling", "msim_gpu_sync_bodies", "msim_gpu_set_dt",
+    "msim_gpu_set_rigid_gravity", "msim_gpu_set_gravity", "msim_gpu_set_lost_fraction_threshold",
+    "msim_gpu_soft_substep", "msim_gpu_p2g", "msim_gpu_grid_update", "msim_gpu_g2p",
+    "msim_gpu_env_step", "msim_gpu_particle_count", "msim_gpu_read_particles",
+    "msim_gpu_read_grid", "msim_gpu_write_grid_velocity", "msim_gpu_set_split_channels",
+    "msim_gpu_set_record_binning", "msim_gpu_read_binning", "msim_gpu_read_wrenches",
+    "msim_gpu_read_bodies", "msim_gpu_read_report", "msim_gpu_lost_count",
+    "msim_gpu_constitutive", "msim_rng_create", "msim_rng_destroy", "msim_rng_uniform",
+    "msim_rng_fill_uniform",
+    "msim_seed_box_count", "msim_seed_box",
+]
+
+_dp = C.POINTER(C.c_double)
+_ip = C.POINTER(C.c_int32)
+_lp = C.POINTER(C.c_int64)
+_u8p = C.POINTER(C.c_uint8)
+_vp = C.c_void_p
+
+_SIGS = {
+    "msim_gpu_create": (C.c_int, [C.POINTER(SoftDesc), C.POINTER(Material), C.c_int, C.c_int, C.c_int, C.POINTER(_vp)]),
+    "msim_gpu_destroy": (None, [_vp]),
+    "msim_gpu_last_error": (C.c_char_p, [_vp]),
+    "msim_gpu_create_error": (C.c_char_p, []),
+    "msim_gpu_version": (C.c_int, []),
+    "msim_gpu_set_particles": (C.c_int, [_vp, C.c_int64, _lp, _dp, _dp, _dp, _dp, _dp, _dp, _ip]),
+    "msim_gpu_write_particles": (C.c_int, [_vp, C.c_int, C.c_int64, _dp, _dp, _dp, _dp]),
+    "msim_gpu_set_bodies": (C.c_int, [_vp, C.c_int, C.POINTER(Body), C.c_int, C.POINTER(Shape), C.c_int]),
+    "msim_gpu_set_coupling": (C.c_int, [_vp, C.POINTER(Coupling)]),
+    "msim_gpu_sync_bodies": (C.c_int, [_vp, C.c_int, C.POINTER(Body), C.c_int]),
+    "msim_gpu_set_dt": (C.c_int, [_vp, C.c_double]),
+    "msim_gpu_set_rigid_gravity": (C.c_int, [_vp, _dp]),
+    "msim_gpu_set_gravity": (C.c_int, [_vp, _dp]),
+    "msim_gpu_set_lost_fraction_threshold": (C.c_int, [_vp, C.c_double]),
+    "msim_gpu_soft_substep": (C.c_int, [_vp, C.c_int, _ip]),
+    "msim_gpu_p2g": (C.c_int, [_vp]),
+    "msim_gpu_grid_update": (C.c_int, [_vp]),
+    "msim_gpu_g2p": (C.c_int, [_vp]),
+    "msim_gpu_env_step": (C.c_int, [_vp, C.c_int, C.c_int, C.POINTER(StepReport)]),
+    "msim_gpu_particle_count": (C.c_int64, [_vp, C.c_int]),
+    "msim_gpu_read_particles": (C.c_int, [_vp, C.c_int, _dp, _dp, _dp, _dp, _u8p]),
+    "msim_gpu_read_grid": (C.c_int, [_vp, C.c_int, _dp, _dp, _dp, _dp]),
+    "msim_gpu_write_grid_velocity": (C.c_int, [_vp, C.c_int, _dp]),
+    "msim_gpu_set_split_channels": (C.c_int, [_vp, C.c_int]),
+    "msim_gpu_set_record_binning": (C.c_int, [_vp, C.c_int]),
+    "msim_gpu_read_binning": (C.c_int, [_vp, C.c_int, _ip, _ip, C.c_int64, _ip, C.c_int64, _lp, _lp, C.c_int64, _lp]),
+    "msim_gpu_read_wrenches": (C.c_int, [_vp, C.c_int, C.c_int, _dp, _dp]),
+    "msim_gpu_read_bodies": (C.c_int, [_vp, C.c_int, C.POINTER(Body), C.c_int]),
+    "msim_gpu_read_report": (C.c_int, [_vp, C.c_int, C.POINTER(StepReport)]),
+    "msim_gpu_lost_count": (C.c_int64, [_vp, C.c_int]),
+    "msim_gpu_constitutive": (C.c_int, [_vp, C.c_int, C.c_int64, _dp, _dp, _dp]),
+    "msim_rng_create": (_vp, [C.c_uint64]),
+    "msim_rng_destroy": (None, [_vp]),
+    "msim_rng_uniform": (C.c_double, [_vp, C.c_double, C.c_double]),
+    "msim_rng_fill_uniform": (None, [_vp, C.c_int64, C.c_double, C.c_double, _dp]),
+    "msim_seed_box_count": (C.c_int64, [_dp, _dp, C.c_double]),
+    "msim_seed_box": (C.c_int64, [_vp, _dp, _dp, C.c_double, C.c_double, _dp, _dp]),
+}
+
+_lib = None
+
+
+def load(path: str = LIB_PATH) -> C.CDLL:
+    """Load libmsim_gpu.so (raises if it is missing: there is no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise ImportError(
+            f"{path} not found: build the CUDA library first (python -c 'import __graft_entry__ as g; g.build()')"
+        )
+    lib = C.CDLL(path)
+    for name, (res, args) in _SIGS.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = lib
+    return lib
+
+
+def dptr(a: np.ndarray | None):
+    if a is None:
+        return None
+    assert a.dtype == np.float64 and a.flags.c_contiguous
+    return a.ctypes.data_as(_dp)
+
+
+def iptr(a: np.ndarray | None):
+    if a is None:
+        return None
+    assert a.dtype == np.int32 and a.flags.c_contiguous
+    return a.ctypes.data_as(_ip)
+
+
+def lptr(a: np.ndarray | None):
+    if a is None:
+        return None
+    assert a.dtype == np.int64 and a.flags.c_contiguous
+    return a.ctypes.data_as(_lp)
+
+
+def u8ptr(a: np.ndarray | None):
+    if a is None:
+        return None
+    assert a.dtype == np.uint8 and a.flags.c_contiguous
+    return a.ctypes.data_as(_u8p)

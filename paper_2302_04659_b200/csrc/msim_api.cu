@@ -1,0 +1,1069 @@
+// C-ABI host implementation (include/msim_gpu.h): context, device memory,
+// uploads/readbacks and the stepping loops that drive msim_kernels.cu.
+//
+// Stepping mirrors soft_substep (mpm.hpp:397-421) and the rigid/soft part of
+// env_step (coupling.hpp:248-293). The CFL cycle count of each substep is
+// decided on the device (k_plan); the host reads the batch maximum through
+// pinned mapped memory once per substep and enqueues that many cycles.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <climits>
+#include <cmath>
+#include <cstring>
+#include <random>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "msim_internal.h"
+
+using namespace msim_impl;
+using msim_dev::MatParams;
+using msim_dev::ShapeDev;
+
+namespace {
+
+thread_local std::string g_create_error;
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  ~DevBuf() { release(); }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+  }
+  cudaError_t ensure(size_t b) {
+    if (b <= bytes && p) return cudaSuccess;
+    release();
+    if (b == 0) b = 16;
+    cudaError_t e = cudaMalloc(&p, b);
+    if (e == cudaSuccess) bytes = b;
+    return e;
+  }
+  template <class T>
+  T* as() const {
+    return static_cast<T*>(p);
+  }
+};
+
+struct CudaError {
+  cudaError_t e;
+  const char* what;
+};
+
+#define CK(expr)                                            \
+  do {                                                      \
+    cudaError_t _e = (expr);                                \
+    if (_e != cudaSuccess) throw CudaError{_e, #expr};      \
+  } while (0)
+
+}  // namespace
+
+struct msim_gpu_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  msim_soft_desc desc{};
+  std::vector<msim_material> mats_h;
+  int n_env = 0;
+  double rigid_gravity[3] = {0, 0, -9.81};
+  msim_coupling coupling{MSIM_COUPLING_PARTICLE, 0, 0.5, 10.0};
+  int split_req = 0;
+  int record_binning = 0;
+  std::string err;
+
+  // geometry derived from desc
+  long long nodes_per_env = 0;
+  int bdims[3] = {0, 0, 0};
+  int blocks_per_env = 0;
+  int n_keys = 0;
+
+  // particles
+  long long n = 0;
+  std::vector<long long> env_off_h;
+  DevBuf env_off_d, env_of_d;
+  DevBuf pool_f[2], meta_b[2], pid_b[2];
+  Particles buf[2]{};
+  int cur = 0;
+  std::vector<double> mean_mass_h;
+  DevBuf mean_mass_d;
+  bool vmax_valid = false;
+
+  // bodies / shapes
+  std::vector<std::vector<msim_body>> bodies_h;
+  std::vector<std::vector<msim_shape>> shapes_h;
+  std::vector<std::vector<std::vector<float>>> vol_h;
+  int n_bodies = 0, n_shapes = 0;
+  bool bodies_on_device = false;
+  DevBuf bodies_d, shapes_host_d, shapes_d, shape_off_d, body_off_d, vol_pool_d, wrench_d, pending_d;
+
+  // per env
+  DevBuf mats_d, cycles_d, dt_cycle_d, applied_d, react_d, max_pen_d, vmax_d, lost_d, err_code_d,
+      err_pid_d, balance_d, cyc_sum_d;
+
+  // binning + grid
+  DevBuf key_d, rank_d, bucket_count_d, bucket_start_d, active_buckets_d, n_active_d, perm_d,
+      base_dbg_d;
+  DevBuf gPM_d, gF_d, gV_d, nb_flag_d, nb_scan_d, nb_list_d, n_nb_d, scan_tmp_d;
+  std::vector<char> env_grid_dirty;
+
+  // host-mapped control words
+  int* h_ctl = nullptr;  // [0] max cycles, [1] any error
+  int* d_ctl = nullptr;
+
+  double time = 0.0;
+};
+
+namespace {
+
+bool split_mode(const msim_gpu_ctx* c) {
+  return c->split_req || c->coupling.mode == MSIM_COUPLING_GRID;
+}
+
+MatParams mat_params(const msim_material& m) {
+  double mu = m.youngs / (2.0 * (1.0 + m.poisson));
+  double lambda = m.youngs * m.poisson / ((1.0 + m.poisson) * (1.0 - 2.0 * m.poisson));
+  MatParams p;
+  p.two_mu = (float)(2.0 * mu);
+  p.lambda = (float)lambda;
+  p.yield_thr = (float)(std::sqrt(2.0 / 3.0) * m.yield_stress);
+  p.density = (float)m.density;
+  return p;
+}
+
+SimParams params(msim_gpu_ctx* c) {
+  SimParams P{};
+  const msim_soft_desc& d = c->desc;
+  P.h = d.h;
+  P.inv_h = 1.0 / d.h;
+  for (int a = 0; a < 3; ++a) {
+    P.origin[a] = d.origin[a];
+    P.dims[a] = d.dims[a];
+    P.bdims[a] = c->bdims[a];
+    P.gravity[a] = (float)d.gravity[a];
+  }
+  P.nodes_per_env = c->nodes_per_env;
+  P.blocks_per_env = c->blocks_per_env;
+  P.n_env = c->n_env;
+  P.boundary_slip = 0;
+  for (int f = 0; f < 6; ++f)
+    if (d.boundary[f] == MSIM_BOUNDARY_SLIP) P.boundary_slip |= 1u << f;
+  P.h_f = (float)d.h;
+  P.d_inv_f = (float)(4.0 / (d.h * d.h));
+  P.n = c->n;
+  P.n_keys = c->n_keys;
+  P.split = split_mode(c) ? 1 : 0;
+  P.grid_mode = c->coupling.mode == MSIM_COUPLING_GRID;
+  P.r_c_particle = (float)(c->coupling.r_c_factor * d.h);
+  P.r_c_grid = (float)std::max(c->coupling.r_c_factor * d.h, 0.65 * d.h);
+  P.c_d = (float)c->coupling.c_d;
+  P.cycle = 0;
+  P.manual = 0;
+  P.dt_manual = (float)d.dt;
+  P.cur = c->buf[c->cur];
+  P.nxt = c->buf[1 - c->cur];
+  P.mats = c->mats_d.as<MatParams>();
+  P.cycles = c->cycles_d.as<int>();
+  P.dt_cycle = c->dt_cycle_d.as<float>();
+  P.env_off = c->env_off_d.as<long long>();
+  P.shape_off = c->shape_off_d.as<int>();
+  P.body_off = c->body_off_d.as<int>();
+  P.shapes = c->shapes_d.as<ShapeDev>();
+  P.vol_pool = c->vol_pool_d.as<float>();
+  P.wrench = c->wrench_d.as<double>();
+  P.applied = c->applied_d.as<double>();
+  P.react = c->react_d.as<double>();
+  P.max_pen_bits = c->max_pen_d.as<unsigned>();
+  P.vmax_bits = c->vmax_d.as<unsigned>();
+  P.lost_count = c->lost_d.as<long long>();
+  P.err_code = c->err_code_d.as<int>();
+  P.err_pid = c->err_pid_d.as<int>();
+  P.mean_mass = c->mean_mass_d.as<double>();
+  P.key = c->key_d.as<int>();
+  P.rank = c->rank_d.as<int>();
+  P.bucket_count = c->bucket_count_d.as<int>();
+  P.bucket_start = c->bucket_start_d.as<int>();
+  P.active_buckets = c->active_buckets_d.as<int>();
+  P.n_active_buckets = c->n_active_d.as<int>();
+  P.perm = c->perm_d.as<int>();
+  P.base_dbg = c->record_binning ? c->base_dbg_d.as<int>() : nullptr;
+  P.gPM = c->gPM_d.as<float4>();
+  P.gF = c->gF_d.as<float4>();
+  P.gV = c->gV_d.as<float4>();
+  P.nb_flag = c->nb_flag_d.as<int>();
+  P.nb_scan = c->nb_scan_d.as<int>();
+  P.nb_list = c->nb_list_d.as<int>();
+  P.n_nb = c->n_nb_d.as<int>();
+  P.scan_tmp = c->scan_tmp_d.as<int>();
+  P.balance_max = c->balance_d.as<double>();
+  P.lost_threshold = d.lost_fraction_threshold;
+  return P;
+}
+
+template <class F>
+int guarded(msim_gpu_ctx* c, F&& f) {
+  try {
+    return f();
+  } catch (const CudaError& e) {
+    if (c) c->err = std::string("CUDA error ") + cudaGetErrorString(e.e) + " at " + e.what;
+    return MSIM_ERR_DEVICE;
+  } catch (const std::exception& e) {
+    if (c) c->err = e.what();
+    return MSIM_ERR_INVALID;
+  }
+}
+
+void set_device(msim_gpu_ctx* c) { CK(cudaSetDevice(c->device)); }
+
+int fail(msim_gpu_ctx* c, int code, const std::string& msg) {
+  c->err = msg;
+  return code;
+}
+
+void carve_particles(msim_gpu_ctx* c, int b, long long n) {
+  // 24 float fields: x3 v3 C9 G9 + mass + vol0 = 26
+  const size_t nf = 26;
+  CK(c->pool_f[b].ensure(sizeof(float) * nf * (size_t)std::max<long long>(n, 1)));
+  CK(c->meta_b[b].ensure(sizeof(uint32_t) * (size_t)std::max<long long>(n, 1)));
+  CK(c->pid_b[b].ensure(sizeof(int32_t) * (size_t)std::max<long long>(n, 1)));
+  float* f = c->pool_f[b].as<float>();
+  size_t stride = (size_t)std::max<long long>(n, 1);
+  Particles& q = c->buf[b];
+  int k = 0;
+  for (int a = 0; a < 3; ++a) q.x[a] = f + stride * k++;
+  for (int a = 0; a < 3; ++a) q.v[a] = f + stride * k++;
+  for (int a = 0; a < 9; ++a) q.C[a] = f + stride * k++;
+  for (int a = 0; a < 9; ++a) q.G[a] = f + stride * k++;
+  q.mass = f + stride * k++;
+  q.vol0 = f + stride * k++;
+  q.meta = c->meta_b[b].as<uint32_t>();
+  q.pid = c->pid_b[b].as<int32_t>();
+}
+
+void alloc_binning(msim_gpu_ctx* c) {
+  long long n = std::max<long long>(c->n, 1);
+  CK(c->key_d.ensure(sizeof(int) * n));
+  CK(c->rank_d.ensure(sizeof(int) * n));
+  CK(c->perm_d.ensure(sizeof(int) * n));
+  if (c->record_binning) {
+    CK(c->base_dbg_d.ensure(sizeof(int) * 3 * n));
+    CK(cudaMemsetAsync(c->base_dbg_d.p, 0xff, sizeof(int) * 3 * n, c->stream));
+  }
+}
+
+// Errors latched on the device: first env (lowest index) wins.
+int collect_errors(msim_gpu_ctx* c) {
+  std::vector<int> code(c->n_env), pid(c->n_env);
+  CK(cudaMemcpyAsync(code.data(), c->err_code_d.p, sizeof(int) * c->n_env, cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaMemcpyAsync(pid.data(), c->err_pid_d.p, sizeof(int) * c->n_env, cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  for (int e = 0; e < c->n_env; ++e) {
+    if (!code[e]) continue;
+    long long local = pid[e] == INT_MAX ? -1 : pid[e] - c->env_off_h[e];
+    std::string where = c->n_env > 1 ? " (env " + std::to_string(e) + ")" : "";
+    switch (code[e]) {
+      case kErrDetStress:
+        return fail(c, MSIM_ERR_INVALID, "kirchhoff_stress: det(F) must be > 0 (particle " + std::to_string(local) + ")" + where);
+      case kErrDetReturn:
+        return fail(c, MSIM_ERR_INVALID, "von_mises_return_map: det(F) must be > 0 (particle " + std::to_string(local) + ")" + where);
+      case kErrLost:
+        return fail(c, MSIM_ERR_DIVERGED, "lost particle fraction exceeds threshold" + where);
+      case kErrCfl:
+        return fail(c, MSIM_ERR_DIVERGED, "CFL violation persists after max substep halvings" + where);
+      case kErrNan:
+        return fail(c, MSIM_ERR_DIVERGED, "NaN/Inf in particle " + std::to_string(local) + where);
+      default:
+        return fail(c, MSIM_ERR_DIVERGED, "simulation diverged" + where);
+    }
+  }
+  return MSIM_OK;
+}
+
+void reset_errors(msim_gpu_ctx* c) {
+  CK(cudaMemsetAsync(c->err_code_d.p, 0, sizeof(int) * c->n_env, c->stream));
+  CK(cudaMemsetAsync(c->err_pid_d.p, 0x7f, sizeof(int) * c->n_env, c->stream));
+}
+
+// pull integrated body states back to the host copies
+void download_bodies(msim_gpu_ctx* c) {
+  if (!c->bodies_on_device || c->n_bodies == 0) return;
+  std::vector<BodyDev> tmp(c->n_bodies);
+  CK(cudaMemcpyAsync(tmp.data(), c->bodies_d.p, sizeof(BodyDev) * c->n_bodies, cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  int k = 0;
+  for (int e = 0; e < c->n_env; ++e)
+    for (auto& b : c->bodies_h[e]) {
+      const BodyDev& d = tmp[k++];
+      std::memcpy(b.q, d.q, sizeof b.q);
+      std::memcpy(b.t, d.t, sizeof b.t);
+      std::memcpy(b.v, d.v, sizeof b.v);
+      std::memcpy(b.w, d.w, sizeof b.w);
+    }
+}
+
+// Rebuild the concatenated body/shape tables of all envs on the device.
+void upload_bodies(msim_gpu_ctx* c) {
+  std::vector<int> boff(c->n_env + 1, 0), soff(c->n_env + 1, 0);
+  std::vector<BodyDev> bd;
+  std::vector<ShapeHost> sh;
+  std::vector<float> pool;
+  for (int e = 0; e < c->n_env; ++e) {
+    boff[e] = (int)bd.size();
+    soff[e] = (int)sh.size();
+    for (const msim_body& b : c->bodies_h[e]) {
+      BodyDev d{};
+      d.mode = b.mode;
+      std::memcpy(d.q, b.q, sizeof d.q);
+      std::memcpy(d.t, b.t, sizeof d.t);
+      std::memcpy(d.v, b.v, sizeof d.v);
+      std::memcpy(d.w, b.w, sizeof d.w);
+      d.mass = b.mass;
+      std::memcpy(d.inertia, b.inertia, sizeof d.inertia);
+      std::memcpy(d.com_off, b.com_offset, sizeof d.com_off);
+      bd.push_back(d);
+    }
+    for (size_t s = 0; s < c->shapes_h[e].size(); ++s) {
+      const msim_shape& in = c->shapes_h[e][s];
+      ShapeHost o{};
+      o.type = in.type;
+      o.body = in.body;
+      std::memcpy(o.lq, in.local_q, sizeof o.lq);
+      std::memcpy(o.lt, in.local_t, sizeof o.lt);
+      o.friction = in.friction;
+      o.k_n = in.k_n;
+      o.k_t = in.k_t;
+      std::memcpy(o.p, in.params, sizeof o.p);
+      if (in.type == MSIM_SHAPE_VOLUME) {
+        for (int k = 0; k < 3; ++k) {
+          o.vol_dims[k] = in.vol_dims[k];
+          o.vol_origin[k] = in.vol_origin[k];
+        }
+        o.vol_voxel = in.vol_voxel;
+        o.vol_off = (long long)pool.size();
+        const auto& smp = c->vol_h[e][s];
+        pool.insert(pool.end(), smp.begin(), smp.end());
+      }
+      sh.push_back(o);
+    }
+  }
+  boff[c->n_env] = (int)bd.size();
+  soff[c->n_env] = (int)sh.size();
+  c->n_bodies = (int)bd.size();
+  c->n_shapes = (int)sh.size();
+  cudaStream_t s = c->stream;
+  CK(c->bodies_d.ensure(sizeof(BodyDev) * std::max<size_t>(bd.size(), 1)));
+  CK(c->shapes_host_d.ensure(sizeof(ShapeHost) * std::max<size_t>(sh.size(), 1)));
+  CK(c->shapes_d.ensure(sizeof(ShapeDev) * std::max<size_t>(sh.size(), 1)));
+  CK(c->body_off_d.ensure(sizeof(int) * boff.size()));
+  CK(c->shape_off_d.ensure(sizeof(int) * soff.size()));
+  CK(c->vol_pool_d.ensure(sizeof(float) * std::max<size_t>(pool.size(), 1)));
+  CK(c->wrench_d.ensure(sizeof(double) * 6 * std::max<size_t>(bd.size(), 1)));
+  CK(c->pending_d.ensure(sizeof(double) * 6 * std::max<size_t>(bd.size(), 1)));
+  if (!bd.empty()) CK(cudaMemcpyAsync(c->bodies_d.p, bd.data(), sizeof(BodyDev) * bd.size(), cudaMemcpyHostToDevice, s));
+  if (!sh.empty()) CK(cudaMemcpyAsync(c->shapes_host_d.p, sh.data(), sizeof(ShapeHost) * sh.size(), cudaMemcpyHostToDevice, s));
+  if (!pool.empty()) CK(cudaMemcpyAsync(c->vol_pool_d.p, pool.data(), sizeof(float) * pool.size(), cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(c->body_off_d.p, boff.data(), sizeof(int) * boff.size(), cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(c->shape_off_d.p, soff.data(), sizeof(int) * soff.size(), cudaMemcpyHostToDevice, s));
+  CK(cudaMemsetAsync(c->wrench_d.p, 0, sizeof(double) * 6 * std::max<size_t>(bd.size(), 1), s));
+  CK(cudaMemsetAsync(c->pending_d.p, 0, sizeof(double) * 6 * std::max<size_t>(bd.size(), 1), s));
+  c->bodies_on_device = true;
+  SimParams P = params(c);
+  launch_rigid(P, c->bodies_d.as<BodyDev>(), c->shapes_host_d.as<ShapeHost>(), c->pending_d.as<double>(), 0,
+               0.0, c->rigid_gravity, -1, s);
+  CK(cudaGetLastError());
+  // keep host storage alive until the copies land
+  CK(cudaStreamSynchronize(s));
+}
+
+// One CFL cycle for every env with cycle < cycles[env] (or all, manual).
+void run_cycle(msim_gpu_ctx* c, int cycle, int manual, int stages) {
+  for (int e = 0; e < c->n_env && (stages & kStageClear); ++e)
+    if (c->env_grid_dirty[e]) {
+      SimParams P = params(c);
+      launch_clear_env_grid(P, e, c->stream);
+      c->env_grid_dirty[e] = 0;
+    }
+  SimParams P = params(c);
+  P.cycle = cycle;
+  P.manual = manual;
+  int first = stages & (kStageClear | kStageBin | kStageP2G);
+  if (first) launch_cycle(P, first, c->stream);
+  if (stages & kStageP2G) {
+    c->cur ^= 1;  // P2G wrote the particles, in bucket order, to the other buffer
+    P.cur = c->buf[c->cur];
+    P.nxt = c->buf[1 - c->cur];
+  }
+  int second = stages & (kStageGrid | kStageG2P | kStageEnd);
+  if (second) launch_cycle(P, second, c->stream);
+  CK(cudaGetLastError());
+}
+
+int substeps(msim_gpu_ctx* c, int n_sub, int32_t* cycles_out) {
+  if (c->n == 0) return MSIM_OK;
+  for (int s = 0; s < n_sub; ++s) {
+    SimParams P = params(c);
+    if (!c->vmax_valid) {
+      launch_vmax(P, c->stream);
+      c->vmax_valid = true;
+    }
+    c->h_ctl[0] = 0;
+    c->h_ctl[1] = 0;
+    launch_plan(P, c->desc.dt, c->desc.cfl_factor * c->desc.h, c->desc.max_cfl_halvings, c->d_ctl,
+                c->d_ctl + 1, c->cyc_sum_d.as<int>(), c->stream);
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(c->stream));
+    if (c->h_ctl[1]) return collect_errors(c);
+    const int maxc = c->h_ctl[0];
+    for (int cy = 0; cy < maxc; ++cy) run_cycle(c, cy, 0, kStageAll);
+    if (cycles_out && s == n_sub - 1)
+      CK(cudaMemcpyAsync(cycles_out, c->cycles_d.p, sizeof(int) * c->n_env, cudaMemcpyDeviceToHost, c->stream));
+  }
+  CK(cudaStreamSynchronize(c->stream));
+  return collect_errors(c);
+}
+
+bool valid_material(const msim_material& m, std::string& why) {
+  if (m.youngs <= 0.0) { why = "Material: E must be > 0"; return false; }
+  if (m.poisson <= 0.0 || m.poisson >= 0.5) { why = "Material: nu must be in (0, 0.5)"; return false; }
+  if (m.yield_stress <= 0.0) { why = "Material: yield stress must be > 0"; return false; }
+  if (m.density <= 0.0) { why = "Material: density must be > 0"; return false; }
+  if (m.model != MSIM_MODEL_HENCKY_VON_MISES) { why = "Material: unknown constitutive model"; return false; }
+  return true;
+}
+
+}  // namespace
+
+extern "C" {
+
+int msim_gpu_version(void) { return 1; }
+
+const char* msim_gpu_create_error(void) { return g_create_error.c_str(); }
+
+int msim_gpu_create(const msim_soft_desc* desc, const msim_material* materials, int n_materials,
+                    int n_env, int device, msim_gpu_ctx** out) {
+  *out = nullptr;
+  g_create_error.clear();
+  if (!desc || n_env < 1 || n_materials < 1 || n_materials > 256) {
+    g_create_error = "msim_gpu_create: invalid arguments";
+    return MSIM_ERR_INVALID;
+  }
+  if (std::min(desc->dims[0], std::min(desc->dims[1], desc->dims[2])) < 4) {
+    g_create_error = "MpmGrid: dims must be >= 4 per axis";
+    return MSIM_ERR_INVALID;
+  }
+  if (!(desc->h > 0.0)) {
+    g_create_error = "MpmGrid: cell length must be > 0";
+    return MSIM_ERR_INVALID;
+  }
+  for (int i = 0; i < n_materials; ++i) {
+    std::string why;
+    if (!valid_material(materials[i], why)) {
+      g_create_error = why;
+      return MSIM_ERR_INVALID;
+    }
+  }
+  auto* c = new msim_gpu_ctx();
+  int rc = guarded(c, [&]() -> int {
+    c->device = device;
+    set_device(c);
+    CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    c->desc = *desc;
+    c->mats_h.assign(materials, materials + n_materials);
+    c->n_env = n_env;
+    for (int a = 0; a < 3; ++a) c->bdims[a] = (desc->dims[a] + 3) / 4;
+    c->blocks_per_env = c->bdims[0] * c->bdims[1] * c->bdims[2];
+    c->nodes_per_env = (long long)desc->dims[0] * desc->dims[1] * desc->dims[2];
+    long long nk = (long long)n_env * c->blocks_per_env + 1;
+    if (nk > INT_MAX / 2) throw std::runtime_error("too many node blocks for one context");
+    c->n_keys = (int)nk;
+    c->env_off_h.assign(n_env + 1, 0);
+    c->bodies_h.assign(n_env, {});
+    c->shapes_h.assign(n_env, {});
+    c->vol_h.assign(n_env, {});
+    c->mean_mass_h.assign(n_env, 0.0);
+    c->env_grid_dirty.assign(n_env, 0);
+    std::vector<MatParams> mp;
+    for (auto& m : c->mats_h) mp.push_back(mat_params(m));
+    CK(c->mats_d.ensure(sizeof(MatParams) * mp.size()));
+    CK(cudaMemcpy(c->mats_d.p, mp.data(), sizeof(MatParams) * mp.size(), cudaMemcpyHostToDevice));
+    auto per_env = [&](DevBuf& b, size_t elem) {
+      CK(b.ensure(elem * n_env));
+      CK(cudaMemset(b.p, 0, elem * n_env));
+    };
+    per_env(c->cycles_d, sizeof(int));
+    per_env(c->dt_cycle_d, sizeof(float));
+    per_env(c->applied_d, 3 * sizeof(double));
+    per_env(c->react_d, 3 * sizeof(double));
+    per_env(c->max_pen_d, sizeof(unsigned));
+    per_env(c->vmax_d, sizeof(unsigned));
+    per_env(c->lost_d, sizeof(long long));
+    per_env(c->err_code_d, sizeof(int));
+    per_env(c->err_pid_d, sizeof(int));
+    per_env(c->balance_d, sizeof(double));
+    per_env(c->cyc_sum_d, sizeof(int));
+    per_env(c->mean_mass_d, sizeof(double));
+    CK(cudaMemset(c->err_pid_d.p, 0x7f, sizeof(int) * n_env));
+    CK(c->env_off_d.ensure(sizeof(long long) * (n_env + 1)));
+    CK(cudaMemset(c->env_off_d.p, 0, sizeof(long long) * (n_env + 1)));
+    // grid: float4 per node, three channels, zeroed once (then cleared lazily)
+    size_t nodes = (size_t)c->nodes_per_env * n_env;
+    CK(c->gPM_d.ensure(sizeof(float4) * nodes));
+    CK(c->gF_d.ensure(sizeof(float4) * nodes));
+    CK(c->gV_d.ensure(sizeof(float4) * nodes));
+    CK(cudaMemset(c->gPM_d.p, 0, sizeof(float4) * nodes));
+    CK(cudaMemset(c->gF_d.p, 0, sizeof(float4) * nodes));
+    CK(cudaMemset(c->gV_d.p, 0, sizeof(float4) * nodes));
+    int nblocks = c->n_keys - 1;
+    CK(c->nb_flag_d.ensure(sizeof(int) * nblocks));
+    CK(c->nb_scan_d.ensure(sizeof(int) * (nblocks + 1)));
+    CK(c->nb_list_d.ensure(sizeof(int) * nblocks));
+    CK(c->n_nb_d.ensure(sizeof(int)));
+    CK(cudaMemset(c->nb_flag_d.p, 0, sizeof(int) * nblocks));
+    CK(cudaMemset(c->n_nb_d.p, 0, sizeof(int)));
+    CK(c->bucket_count_d.ensure(sizeof(int) * c->n_keys));
+    CK(c->bucket_start_d.ensure(sizeof(int) * (c->n_keys + 1)));
+    CK(c->active_buckets_d.ensure(sizeof(int) * c->n_keys));
+    CK(c->n_active_d.ensure(sizeof(int)));
+    CK(cudaMemset(c->bucket_count_d.p, 0, sizeof(int) * c->n_keys));
+    CK(cudaMemset(c->n_active_d.p, 0, sizeof(int)));
+    CK(c->scan_tmp_d.ensure(sizeof(int) * scan_tmp_ints(std::max(c->n_keys, (int)std::min<long long>(c->nodes_per_env + 1, INT_MAX)))));
+    CK(cudaHostAlloc(&c->h_ctl, 4 * sizeof(int), cudaHostAllocMapped));
+    CK(cudaHostGetDevicePointer(&c->d_ctl, c->h_ctl, 0));
+    carve_particles(c, 0, 0);
+    carve_particles(c, 1, 0);
+    alloc_binning(c);
+    upload_bodies(c);
+    CK(cudaDeviceSynchronize());
+    return MSIM_OK;
+  });
+  if (rc != MSIM_OK) {
+    g_create_error = c->err;
+    msim_gpu_destroy(c);
+    return rc;
+  }
+  *out = c;
+  return MSIM_OK;
+}
+
+void msim_gpu_destroy(msim_gpu_ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  if (c->h_ctl) cudaFreeHost(c->h_ctl);
+  if (c->stream) cudaStreamDestroy(c->stream);
+  delete c;
+}
+
+const char* msim_gpu_last_error(const msim_gpu_ctx* c) { return c ? c->err.c_str() : ""; }
+
+int msim_gpu_set_particles(msim_gpu_ctx* c, int64_t n, const int64_t* env_offsets, const double* x,
+                           const double* v, const double* F, const double* C, const double* mass,
+                           const double* vol0, const int32_t* material) {
+  return guarded(c, [&]() -> int {
+    if (n < 0 || n >= INT_MAX / 2) return fail(c, MSIM_ERR_INVALID, "set_particles: particle count out of range");
+    if (!env_offsets || env_offsets[0] != 0 || env_offsets[c->n_env] != n)
+      return fail(c, MSIM_ERR_INVALID, "set_particles: env_offsets must start at 0 and end at n");
+    for (int e = 0; e < c->n_env; ++e)
+      if (env_offsets[e + 1] < env_offsets[e]) return fail(c, MSIM_ERR_INVALID, "set_particles: env_offsets not monotone");
+    if (n > 0 && (!x || !mass || !vol0)) return fail(c, MSIM_ERR_INVALID, "set_particles: x, mass, vol0 required");
+    if (material)
+      for (int64_t i = 0; i < n; ++i)
+        if (material[i] < 0 || material[i] >= (int)c->mats_h.size())
+          return fail(c, MSIM_ERR_INVALID, "set_particles: material index out of range");
+    set_device(c);
+    cudaStream_t s = c->stream;
+    c->n = n;
+    c->cur = 0;
+    carve_particles(c, 0, n);
+    carve_particles(c, 1, n);
+    alloc_binning(c);
+    c->env_off_h.assign(env_offsets, env_offsets + c->n_env + 1);
+    CK(cudaMemcpyAsync(c->env_off_d.p, c->env_off_h.data(), sizeof(long long) * (c->n_env + 1), cudaMemcpyHostToDevice, s));
+    std::vector<int> env_of(n);
+    for (int e = 0; e < c->n_env; ++e) {
+      double msum = 0.0;
+      for (long long i = env_offsets[e]; i < env_offsets[e + 1]; ++i) {
+        env_of[i] = e;
+        msum += mass[i];
+      }
+      long long ne = env_offsets[e + 1] - env_offsets[e];
+      c->mean_mass_h[e] = ne > 0 ? msum / (double)ne : 0.0;  // World::init (coupling.hpp:97-99)
+    }
+    CK(cudaMemcpyAsync(c->mean_mass_d.p, c->mean_mass_h.data(), sizeof(double) * c->n_env, cudaMemcpyHostToDevice, s));
+    if (n > 0) {
+      // stage doubles on the device in chunks, convert to fp32 SoA
+      const long long chunk = 1 << 20;
+      DevBuf st;
+      CK(st.ensure(sizeof(double) * chunk * 26 + sizeof(int) * chunk * 2));
+      for (long long o = 0; o < n; o += chunk) {
+        long long m = std::min(chunk, n - o);
+        double* dx = st.as<double>();
+        double* dv = dx + 3 * chunk;
+        double* dF = dv + 3 * chunk;
+        double* dC = dF + 9 * chunk;
+        double* dm = dC + 9 * chunk;
+        double* dV = dm + chunk;
+        int* dmat = reinterpret_cast<int*>(dV + chunk);
+        int* denv = dmat + chunk;
+        CK(cudaMemcpyAsync(dx, x + 3 * o, sizeof(double) * 3 * m, cudaMemcpyHostToDevice, s));
+        if (v) CK(cudaMemcpyAsync(dv, v + 3 * o, sizeof(double) * 3 * m, cudaMemcpyHostToDevice, s));
+        if (F) CK(cudaMemcpyAsync(dF, F + 9 * o, sizeof(double) * 9 * m, cudaMemcpyHostToDevice, s));
+        if (C) CK(cudaMemcpyAsync(dC, C + 9 * o, sizeof(double) * 9 * m, cudaMemcpyHostToDevice, s));
+        CK(cudaMemcpyAsync(dm, mass + o, sizeof(double) * m, cudaMemcpyHostToDevice, s));
+        CK(cudaMemcpyAsync(dV, vol0 + o, sizeof(double) * m, cudaMemcpyHostToDevice, s));
+        if (material) CK(cudaMemcpyAsync(dmat, material + o, sizeof(int) * m, cudaMemcpyHostToDevice, s));
+        CK(cudaMemcpyAsync(denv, env_of.data() + o, sizeof(int) * m, cudaMemcpyHostToDevice, s));
+        SimParams P = params(c);
+        launch_convert_in(P, m, dx, v ? dv : nullptr, F ? dF : nullptr, C ? dC : nullptr, dm, dV,
+                          material ? dmat : nullptr, denv, o, 1, s);
+        CK(cudaGetLastError());
+        CK(cudaStreamSynchronize(s));  // staging reused
+      }
+    }
+    // init_buffers (mpm.hpp:137-142): lost flags, counts, clean grid
+    CK(cudaMemsetAsync(c->lost_d.p, 0, sizeof(long long) * c->n_env, s));
+    for (int e = 0; e < c->n_env; ++e) c->env_grid_dirty[e] = 1;
+    c->vmax_valid = false;
+    reset_errors(c);
+    CK(cudaStreamSynchronize(s));
+    return MSIM_OK;
+  });
+}
+
+int msim_gpu_write_particles(msim_gpu_ctx* c, int env, int64_t n, const double* x, const double* v,
+                             const double* F, const double* C) {
+  return guarded(c, [&]() -> int {
+    if (env < 0 || env >= c->n_env) return fail(c, MSIM_ERR_INVALID, "write_particles: env out of range");
+    long long first = c->env_off_h[env], ne = c->env_off_h[env + 1] - first;
+    if (n != ne) return fail(c, MSIM_ERR_INVALID, "write_particles: count mismatch");
+    set_device(c);
+    cudaStream_t s = c->stream;
+    DevBuf st;
+    CK(st.ensure(sizeof(double) * std::max<long long>(ne, 1) * 24));
+    double* dx = st.as<double>();
+    double* dv = dx + 3 * ne;
+    double* dF = dv + 3 * ne;
+    double* dC = dF + 9 * ne;
+    if (x) CK(cudaMemcpyAsync(dx, x, sizeof(double) * 3 * ne, cudaMemcpyHostToDevice, s));
+    if (v) CK(cudaMemcpyAsync(dv, v, sizeof(double) * 3 * ne, cudaMemcpyHostToDevice, s));
+    if (F) CK(cudaMemcpyAsync(dF, F, sizeof(double) * 9 * ne, cudaMemcpyHostToDevice, s));
+    if (C) CK(cudaMemcpyAsync(dC, C, sizeof(double) * 9 * ne, cudaMemcpyHostToDevice, s));
+    SimParams P = params(c);
+    launch_overwrite(P, env, first, ne, x ? dx : nullptr, v ? dv : nullptr, F ? dF : nullptr,
+                     C ? dC : nullptr, s);
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(s));
+    c->vmax_valid = false;
+    return MSIM_OK;
+  });
+}
+
+int msim_gpu_set_bodies(msim_gpu_ctx* c, int env, const msim_body* bodies, int n_bodies,
+                        const msim_shape* shapes, int n_shapes) {
+  return guarded(c, [&]() -> int {
+    if (env < 0 || env >= c->n_env) return fail(c, MSIM_ERR_INVALID, "set_bodies: env out of range");
+    if (n_bodies < 0 || n_bodies > kMaxBodiesPerEnv)
+      return fail(c, MSIM_ERR_INVALID, "set_bodies: at most 32 contact bodies per environment");
+    for (int i = 0; i < n_bodies; ++i) {
+      const msim_body& b = bodies[i];
+      if (b.mode == MSIM_BODY_DYNAMIC &&
+          (b.mass <= 0.0 || std::min(b.inertia[0], std::min(b.inertia[1], b.inertia[2])) <= 0.0))
+        return fail(c, MSIM_ERR_INVALID, "RigidBody: dynamic body needs positive mass and inertia");
+    }
+    std::vector<std::vector<float>> vols;
+    for (int s = 0; s < n_shapes; ++s) {
+      const msim_shape& sh = shapes[s];
+      if (sh.body < 0 || sh.body >= n_bodies) return fail(c, MSIM_ERR_INVALID, "set_bodies: shape body index out of range");
+      if (sh.friction < 0.0) return fail(c, MSIM_ERR_INVALID, "Shape: friction must be >= 0");
+      if (sh.k_n <= 0.0 || sh.k_t <= 0.0) return fail(c, MSIM_ERR_INVALID, "Shape: stiffness must be > 0");
+      std::vector<float> smp;
+      if (sh.type == MSIM_SHAPE_VOLUME) {
+        if (std::min(sh.vol_dims[0], std::min(sh.vol_dims[1], sh.vol_dims[2])) < 2 || !sh.vol_samples)
+          return fail(c, MSIM_ERR_INVALID, "SdfVolume: dims must be >= 2 per axis");
+        size_t ns = (size_t)sh.vol_dims[0] * sh.vol_dims[1] * sh.vol_dims[2];
+        smp.assign(sh.vol_samples, sh.vol_samples + ns);
+        for (float f : smp)
+          if (!std::isfinite(f)) return fail(c, MSIM_ERR_INVALID, "SdfVolume: non-finite sample");
+      } else if (sh.type < 0 || sh.type > MSIM_SHAPE_VOLUME) {
+        return fail(c, MSIM_ERR_INVALID, "Shape: unknown type");
+      }
+      vols.push_back(std::move(smp));
+    }
+    set_device(c);
+    download_bodies(c);
+    c->bodies_h[env].assign(bodies, bodies + n_bodies);
+    c->shapes_h[env].assign(shapes, shapes + n_shapes);
+    c->vol_h[env] = std::move(vols);
+    upload_bodies(c);
+    return MSIM_OK;
+  });
+}
+
+int msim_gpu_set_coupling(msim_gpu_ctx* c, const msim_coupling* cp) {
+  if (cp->mode != MSIM_COUPLING_PARTICLE && cp->mode != MSIM_COUPLING_GRID)
+    return fail(c, MSIM_ERR_INVALID, "set_coupling: unknown mode");
+  c->coupling = *cp;
+  return MSIM_OK;
+}
+
+int msim_gpu_sync_bodies(msim_gpu_ctx* c, int env, const msim_body* bodies, int n_bodies) {
+  return guarded(c, [&]() -> int {
+    if (env < 0 || env >= c->n_env) return fail(c, MSIM_ERR_INVALID, "sync_bodies: env out of range");
+    if ((int)c->bodies_h[env].size() != n_bodies) return fail(c, MSIM_ERR_INVALID, "sync_bodies: body count mismatch");
+    set_device(c);
+    // body slots of this env start at the prefix of earlier envs' counts
+    int off = 0;
+    for (int e = 0; e < env; ++e) off += (int)c->bodies_h[e].size();
+    std::vector<BodyDev> bd(n_bodies);
+    if (n_bodies) {
+      CK(cudaMemcpyAsync(bd.data(), c->bodies_d.as<BodyDev>() + off, sizeof(BodyDev) * n_bodies, cudaMemcpyDeviceToHost, c->stream));
+      CK(cudaStreamSynchronize(c->stream));
+    }
+    for (int i = 0; i < n_bodies; ++i) {
+      std::memcpy(bd[i].q, bodies[i].q, sizeof bd[i].q);
+      std::memcpy(bd[i].t, bodies[i].t, sizeof bd[i].t);
+      std::memcpy(bd[i].v, bodies[i].v, sizeof bd[i].v);
+      std::memcpy(bd[i].w, bodies[i].w, sizeof bd[i].w);
+      c->bodies_h[env][i] = bodies[i];
+    }
+    if (n_bodies)
+      CK(cudaMemcpyAsync(c->bodies_d.as<BodyDev>() + off, bd.data(), sizeof(BodyDev) * n_bodies, cudaMemcpyHostToDevice, c->stream));
+    SimParams P = params(c);
+    launch_rigid(P, c->bodies_d.as<BodyDev>(), c->shapes_host_d.as<ShapeHost>(), c->pending_d.as<double>(), 0,
+                 0.0, c->rigid_gravity, env, c->stream);
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(c->stream));
+    return MSIM_OK;
+  });
+}
+
+int msim_gpu_set_dt(msim_gpu_ctx* c, double dt) {
+  c->desc.dt = dt;
+  return MSIM_OK;
+}
+int msim_gpu_set_gravity(msim_gpu_ctx* c, const double* g) {
+  for (int a = 0; a < 3; ++a) c->desc.gravity[a] = g[a];
+  return MSIM_OK;
+}
+int msim_gpu_set_rigid_gravity(msim_gpu_ctx* c, const double* g) {
+  for (int a = 0; a < 3; ++a) c->rigid_gravity[a] = g[a];
+  return MSIM_OK;
+}
+int msim_gpu_set_lost_fraction_threshold(msim_gpu_ctx* c, double t) {
+  c->desc.lost_fraction_threshold = t;
+  return MSIM_OK;
+}
+int msim_gpu_set_split_channels(msim_gpu_ctx* c, int split) {
+  c->split_req = split ? 1 : 0;
+  return MSIM_OK;
+}
+int msim_gpu_set_record_binning(msim_gpu_ctx* c, int on) {
+  return guarded(c, [&]() -> int {
+    set_device(c);
+    c->record_binning = on ? 1 : 0;
+    alloc_binning(c);
+    return MSIM_OK;
+  });
+}
+
+int msim_gpu_soft_substep(msim_gpu_ctx* c, int n_substeps, int32_t* cycles_out) {
+  return guarded(c, [&]() -> int {
+    set_device(c);
+    reset_errors(c);
+    return substeps(c, n_substeps, cycles_out);
+  });
+}
+
+static int manual_phase(msim_gpu_ctx* c, int stages) {
+  return guarded(c, [&]() -> int {
+    set_device(c);
+    reset_errors(c);
+    if (c->n == 0) return MSIM_OK;
+    run_cycle(c, 0, 1, stages);
+    CK(cudaStreamSynchronize(c->stream));
+    c->vmax_valid = false;
+    return collect_errors(c);
+  });
+}
+
+int msim_gpu_p2g(msim_gpu_ctx* c) {
+  int saved = c->split_req;
+  c->split_req = 1;  // phase API keeps momentum and force apart like MpmGrid
+  int rc = manual_phase(c, kStageClear | kStageBin | kStageP2G | kStageEnd);
+  c->split_req = saved;
+  return rc;
+}
+int msim_gpu_grid_update(msim_gpu_ctx* c) {
+  int saved = c->split_req;
+  c->split_req = 1;
+  int rc = manual_phase(c, kStageGrid);
+  c->split_req = saved;
+  return rc;
+}
+int msim_gpu_g2p(msim_gpu_ctx* c) { return manual_phase(c, kStageG2P); }
+
+int msim_gpu_env_step(msim_gpu_ctx* c, int n_rigid, int n_soft, msim_step_report* report) {
+  return guarded(c, [&]() -> int {
+    if (n_rigid < 1 || n_soft < 1) return fail(c, MSIM_ERR_INVALID, "World: n_rigid and n_soft must be >= 1");
+    set_device(c);
+    cudaStream_t s = c->stream;
+    reset_errors(c);
+    CK(cudaMemsetAsync(c->max_pen_d.p, 0, sizeof(unsigned) * c->n_env, s));
+    CK(cudaMemsetAsync(c->balance_d.p, 0, sizeof(double) * c->n_env, s));
+    CK(cudaMemsetAsync(c->cyc_sum_d.p, 0, sizeof(int) * c->n_env, s));
+    const double dt_r = n_soft * c->desc.dt;
+    int rc = MSIM_OK;
+    int done_rigid = 0;
+    for (int r = 0; r < n_rigid && rc == MSIM_OK; ++r) {
+      SimParams P = params(c);
+      if (c->n_bodies > 0)
+        launch_rigid(P, c->bodies_d.as<BodyDev>(), c->shapes_host_d.as<ShapeHost>(), c->pending_d.as<double>(),
+                     1, dt_r, c->rigid_gravity, -1, s);
+      CK(cudaGetLastError());
+      rc = substeps(c, n_soft, nullptr);
+      if (c->n_bodies > 0) launch_stage_wrenches(P, c->pending_d.as<double>(), c->n_bodies, s);
+      ++done_rigid;
+    }
+    c->time += n_rigid * n_soft * c->desc.dt;
+    if (report) {
+      msim_step_report agg{};
+      agg.rigid_steps = done_rigid;
+      agg.soft_substeps = done_rigid * n_soft;
+      for (int e = 0; e < c->n_env; ++e) {
+        msim_step_report r{};
+        msim_gpu_read_report(c, e, &r);
+        agg.cfl_cycles = std::max(agg.cfl_cycles, r.cfl_cycles);
+        agg.max_penetration = std::max(agg.max_penetration, r.max_penetration);
+        agg.max_force_balance_error = std::max(agg.max_force_balance_error, r.max_force_balance_error);
+        agg.lost_particles += r.lost_particles;
+      }
+      *report = agg;
+    }
+    CK(cudaStreamSynchronize(s));
+    return rc;
+  });
+}
+
+int64_t msim_gpu_particle_count(const msim_gpu_ctx* c, int env) {
+  if (env < 0) return c->n;
+  if (env >= c->n_env) return -1;
+  return c->env_off_h[env + 1] - c->env_off_h[env];
+}
+
+int msim_gpu_read_particles(msim_gpu_ctx* c, int env, double* x, double* v, double* F, double* C,
+                            uint8_t* lost) {
+  return guarded(c, [&]() -> int {
+    if (env < 0 || env >= c->n_env) return fail(c, MSIM_ERR_INVALID, "read_particles: env out of range");
+    set_device(c);
+    cudaStream_t s = c->stream;
+    long long first = c->env_off_h[env], ne = c->env_off_h[env + 1] - first;
+    if (ne == 0) return MSIM_OK;
+    DevBuf st;
+    CK(st.ensure(sizeof(double) * ne * 24 + ne));
+    double* dx = st.as<double>();
+    double* dv = dx + 3 * ne;
+    double* dF = dv + 3 * ne;
+    double* dC = dF + 9 * ne;
+    uint8_t* dl = reinterpret_cast<uint8_t*>(dC + 9 * ne);
+    SimParams P = params(c);
+    launch_convert_out(P, env, first, ne, x ? dx : nullptr, v ? dv : nullptr, F ? dF : nullptr,
+                       C ? dC : nullptr, lost ? dl : nullptr, s);
+    CK(cudaGetLastError());
+    if (x) CK(cudaMemcpyAsync(x, dx, sizeof(double) * 3 * ne, cudaMemcpyDeviceToHost, s));
+    if (v) CK(cudaMemcpyAsync(v, dv, sizeof(double) * 3 * ne, cudaMemcpyDeviceToHost, s));
+    if (F) CK(cudaMemcpyAsync(F, dF, sizeof(double) * 9 * ne, cudaMemcpyDeviceToHost, s));
+    if (C) CK(cudaMemcpyAsync(C, dC, sizeof(double) * 9 * ne, cudaMemcpyDeviceToHost, s));
+    if (lost) CK(cudaMemcpyAsync(lost, dl, ne, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    return MSIM_OK;
+  });
+}
+
+int msim_gpu_read_grid(msim_gpu_ctx* c, int env, double* mass, double* momentum, double* force,
+                       double* velocity) {
+  return guarded(c, [&]() -> int {
+    if (env < 0 || env >= c->n_env) return fail(c, MSIM_ERR_INVALID, "read_grid: env out of range");
+    set_device(c);
+    cudaStream_t s = c->stream;
+    long long nn = c->nodes_per_env;
+    DevBuf st;
+    CK(st.ensure(sizeof(double) * nn * 10));
+    double* dm = st.as<double>();
+    double* dp = dm + nn;
+    double* df = dp + 3 * nn;
+    double* dv = df + 3 * nn;
+    SimParams P = params(c);
+    launch_grid_out(P, env, mass ? dm : nullptr, momentum ? dp : nullptr, force ? df : nullptr,
+                    velocity ? dv : nullptr, s);
+    CK(cudaGetLastError());
+    if (mass) CK(cudaMemcpyAsync(mass, dm, sizeof(double) * nn, cudaMemcpyDeviceToHost, s));
+    if (momentum) CK(cudaMemcpyAsync(momentum, dp, sizeof(double) * 3 * nn, cudaMemcpyDeviceToHost, s));
+    if (force) CK(cudaMemcpyAsync(force, df, sizeof(double) * 3 * nn, cudaMemcpyDeviceToHost, s));
+    if (velocity) CK(cudaMemcpyAsync(velocity, dv, sizeof(double) * 3 * nn, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    return MSIM_OK;
+  });
+}
+
+int msim_gpu_write_grid_velocity(msim_gpu_ctx* c, int env, const double* velocity) {
+  return guarded(c, [&]() -> int {
+    if (env < 0 || env >= c->n_env) return fail(c, MSIM_ERR_INVALID, "write_grid_velocity: env out of range");
+    set_device(c);
+    cudaStream_t s = c->stream;
+    long long nn = c->nodes_per_env;
+    DevBuf st;
+    CK(st.ensure(sizeof(double) * nn * 3));
+    CK(cudaMemcpyAsync(st.p, velocity, sizeof(double) * 3 * nn, cudaMemcpyHostToDevice, s));
+    SimParams P = params(c);
+    launch_grid_vel_in(P, env, st.as<double>(), s);
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(s));
+    c->env_grid_dirty[env] = 1;  // the next clear must wipe the whole env grid
+    return MSIM_OK;
+  });
+}
+
+int msim_gpu_read_binning(msim_gpu_ctx* c, int env, int32_t* base, int32_t* cell_start,
+                          int64_t cell_start_cap, int32_t* cell_particles, int64_t cell_particles_cap,
+                          int64_t* n_alive, int64_t* active_nodes, int64_t active_cap,
+                          int64_t* n_active) {
+  return guarded(c, [&]() -> int {
+    if (env < 0 || env >= c->n_env) return fail(c, MSIM_ERR_INVALID, "read_binning: env out of range");
+    if (!c->record_binning) return fail(c, MSIM_ERR_INVALID, "read_binning: enable msim_gpu_set_record_binning first");
+    set_device(c);
+    cudaStream_t s = c->stream;
+    long long first = c->env_off_h[env], ne = c->env_off_h[env + 1] - first;
+    const int nbins = (c->desc.dims[0] - 2) * (c->desc.dims[1] - 2) * (c->desc.dims[2] - 2);
+    const long long nn = c->nodes_per_env;
+    DevBuf cc, cs, cp, nf, ns, nl, nlc, an, tmp;
+    CK(cc.ensure(sizeof(int) * (nbins + 1)));
+    CK(cs.ensure(sizeof(int) * (nbins + 1)));
+    CK(cp.ensure(sizeof(int) * std::max<long long>(ne, 1)));
+    CK(nf.ensure(sizeof(int) * nn));
+    CK(ns.ensure(sizeof(int) * (nn + 1)));
+    CK(nl.ensure(sizeof(int) * nn));
+    CK(nlc.ensure(sizeof(int)));
+    CK(an.ensure(sizeof(long long) * nn));
+    CK(tmp.ensure(sizeof(int) * scan_tmp_ints((int)std::max<long long>(nbins + 1, nn + 1))));
+    SimParams P = params(c);
+    const int* b = c->base_dbg_d.as<int>() + 3 * first;
+    launch_binning_out(P, env, first, ne, b, cc.as<int>(), cs.as<int>(), cp.as<int>(), nf.as<int>(),
+                       ns.as<int>(), nl.as<int>(), nlc.as<int>(), an.as<long long>(), tmp.as<int>(), s);
+    CK(cudaGetLastError());
+    int total = 0, nact = 0;
+    CK(cudaMemcpyAsync(&total, cs.as<int>() + nbins, sizeof(int), cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(&nact, nlc.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    *n_alive = total;
+    *n_active = nact;
+    if (base) CK(cudaMemcpyAsync(base, b, sizeof(int) * 3 * ne, cudaMemcpyDeviceToHost, s));
+    if (cell_start) {
+      if (cell_start_cap < nbins + 1) return fail(c, MSIM_ERR_INVALID, "read_binning: cell_start capacity");
+      CK(cudaMemcpyAsync(cell_start, cs.p, sizeof(int) * (nbins + 1), cudaMemcpyDeviceToHost, s));
+    }
+    if (cell_particles) {
+      if (cell_particles_cap < total) return fail(c, MSIM_ERR_INVALID, "read_binning: cell_particles capacity");
+      CK(cudaMemcpyAsync(cell_particles, cp.p, sizeof(int) * total, cudaMemcpyDeviceToHost, s));
+    }
+    if (active_nodes) {
+      if (active_cap < nact) return fail(c, MSIM_ERR_INVALID, "read_binning: active_nodes capacity");
+      CK(cudaMemcpyAsync(active_nodes, an.p, sizeof(long long) * nact, cudaMemcpyDeviceToHost, s));
+    }
+    CK(cudaStreamSynchronize(s));
+    return MSIM_OK;
+  });
+}
+
+int msim_gpu_read_wrenches(msim_gpu_ctx* c, int env, int pending, double* force, double* torque) {
+  return guarded(c, [&]() -> int {
+    if (env < 0 || env >= c->n_env) return fail(c, MSIM_ERR_INVALID, "read_wrenches: env out of range");
+    set_device(c);
+    int off = 0;
+    for (int e = 0; e < env; ++e) off += (int)c->bodies_h[e].size();
+    int nb = (int)c->bodies_h[env].size();
+    if (nb == 0) return MSIM_OK;
+    std::vector<double> w(6 * nb);
+    const double* src = (pending ? c->pending_d.as<double>() : c->wrench_d.as<double>()) + 6 * off;
+    CK(cudaMemcpyAsync(w.data(), src, sizeof(double) * 6 * nb, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    for (int i = 0; i < nb; ++i)
+      for (int k = 0; k < 3; ++k) {
+        if (force) force[3 * i + k] = w[6 * i + k];
+        if (torque) torque[3 * i + k] = w[6 * i + 3 + k];
+      }
+    return MSIM_OK;
+  });
+}
+
+int msim_gpu_read_bodies(msim_gpu_ctx* c, int env, msim_body* out, int n_bodies) {
+  return guarded(c, [&]() -> int {
+    if (env < 0 || env >= c->n_env) return fail(c, MSIM_ERR_INVALID, "read_bodies: env out of range");
+    set_device(c);
+    download_bodies(c);
+    int nb = std::min<int>(n_bodies, (int)c->bodies_h[env].size());
+    for (int i = 0; i < nb; ++i) out[i] = c->bodies_h[env][i];
+    return MSIM_OK;
+  });
+}
+
+int msim_gpu_read_report(msim_gpu_ctx* c, int env, msim_step_report* r) {
+  return guarded(c, [&]() -> int {
+    if (env < 0 || env >= c->n_env) return fail(c, MSIM_ERR_INVALID, "read_report: env out of range");
+    set_device(c);
+    unsigned pen = 0;
+    double bal = 0.0;
+    long long lost = 0;
+    int cyc = 0;
+    cudaStream_t s = c->stream;
+    CK(cudaMemcpyAsync(&pen, c->max_pen_d.as<unsigned>() + env, sizeof pen, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(&bal, c->balance_d.as<double>() + env, sizeof bal, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(&lost, c->lost_d.as<long long>() + env, sizeof lost, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(&cyc, c->cyc_sum_d.as<int>() + env, sizeof cyc, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    float penf;
+    std::memcpy(&penf, &pen, sizeof penf);
+    r->max_penetration = penf;
+    r->max_force_balance_error = bal;
+    r->lost_particles = lost;
+    r->cfl_cycles = cyc;
+    return MSIM_OK;
+  });
+}
+
+int64_t msim_gpu_lost_count(msim_gpu_ctx* c, int env) {
+  long long lost = -1;
+  if (env < 0 || env >= c->n_env) return -1;
+  if (cudaSetDevice(c->device) != cudaSuccess) return -1;
+  if (cudaMemcpy(&lost, c->lost_d.as<long long>() + env, sizeof lost, cudaMemcpyDeviceToHost) != cudaSuccess)
+    return -1;
+  return lost;
+}
+
+int msim_gpu_constitutive(msim_gpu_ctx* c, int mat, int64_t n, const double* F, double* tau, double* Fp) {
+  return guarded(c, [&]() -> int {
+    if (mat < 0 || mat >= (int)c->mats_h.size()) return fail(c, MSIM_ERR_INVALID, "constitutive: material out of range");
+    set_device(c);
+    cudaStream_t s = c->stream;
+    DevBuf st;
+    CK(st.ensure(sizeof(double) * std::max<int64_t>(n, 1) * 27 + 16));
+    double* dF = st.as<double>();
+    double* dt = dF + 9 * n;
+    double* dp = dt + 9 * n;
+    int* bad = reinterpret_cast<int*>(dp + 9 * n);
+    CK(cudaMemsetAsync(bad, 0, sizeof(int), s));
+    CK(cudaMemcpyAsync(dF, F, sizeof(double) * 9 * n, cudaMemcpyHostToDevice, s));
+    launch_constitutive(mat_params(c->mats_h[mat]), n, dF, tau ? dt : nullptr, Fp ? dp : nullptr, bad, s);
+    CK(cudaGetLastError());
+    int hbad = 0;
+    CK(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, s));
+    if (tau) CK(cudaMemcpyAsync(tau, dt, sizeof(double) * 9 * n, cudaMemcpyDeviceToHost, s));
+    if (Fp) CK(cudaMemcpyAsync(Fp, dp, sizeof(double) * 9 * n, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (hbad) return fail(c, MSIM_ERR_INVALID, "kirchhoff_stress: det(F) must be > 0");
+    return MSIM_OK;
+  });
+}
+
+}  // extern "C"

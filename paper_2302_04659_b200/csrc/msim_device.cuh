@@ -1,0 +1,318 @@
+// Device-side building blocks of the B200 MLS-MPM substep: fp32 3-vector /
+// 3x3 math, the constitutive model on the displacement gradient, SDF
+// primitives and the penalty law. Reference semantics are cited per function
+// (paths relative to /root/reference/proj/include/msim/).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace msim_dev {
+
+// ---------------------------------------------------------------------------
+// Small fp32 vector / matrix helpers (row-major 3x3 in registers).
+
+struct f3 {
+  float x, y, z;
+};
+__host__ __device__ __forceinline__ f3 mk3(float x, float y, float z) { return f3{x, y, z}; }
+__host__ __device__ __forceinline__ f3 operator+(f3 a, f3 b) { return {a.x + b.x, a.y + b.y, a.z + b.z}; }
+__host__ __device__ __forceinline__ f3 operator-(f3 a, f3 b) { return {a.x - b.x, a.y - b.y, a.z - b.z}; }
+__host__ __device__ __forceinline__ f3 operator*(float s, f3 a) { return {s * a.x, s * a.y, s * a.z}; }
+__host__ __device__ __forceinline__ float dot(f3 a, f3 b) { return a.x * b.x + a.y * b.y + a.z * b.z; }
+__host__ __device__ __forceinline__ f3 cross(f3 a, f3 b) {
+  return {a.y * b.z - a.z * b.y, a.z * b.x - a.x * b.z, a.x * b.y - a.y * b.x};
+}
+__host__ __device__ __forceinline__ float norm(f3 a) { return sqrtf(dot(a, a)); }
+__host__ __device__ __forceinline__ float comp(f3 a, int i) { return i == 0 ? a.x : (i == 1 ? a.y : a.z); }
+
+// y = M x, M row-major float[9]
+__host__ __device__ __forceinline__ f3 matvec(const float* M, f3 x) {
+  return {M[0] * x.x + M[1] * x.y + M[2] * x.z, M[3] * x.x + M[4] * x.y + M[5] * x.z,
+          M[6] * x.x + M[7] * x.y + M[8] * x.z};
+}
+__host__ __device__ __forceinline__ f3 matTvec(const float* M, f3 x) {
+  return {M[0] * x.x + M[3] * x.y + M[6] * x.z, M[1] * x.x + M[4] * x.y + M[7] * x.z,
+          M[2] * x.x + M[5] * x.y + M[8] * x.z};
+}
+
+// ---------------------------------------------------------------------------
+// Symmetric 3x3 eigen-decomposition by cyclic Jacobi, fp32.
+// A = {a00, a11, a22, a01, a02, a12}; on return d = eigenvalues and V
+// (row-major, columns = eigenvectors) with A = V diag(d) V^T.
+// The solver runs on E = F F^T - I, whose entries are the (small) strains,
+// so eigenvalues carry fp32 precision RELATIVE to the strain rather than
+// relative to 1 (the cancellation that makes fp32 log(sigma) lossy).
+__device__ __forceinline__ void jacobi_rotate(float& app, float& aqq, float& apq, float& arp,
+                                              float& arq, float* V, int p, int q) {
+  if (fabsf(apq) < 1e-30f) return;
+  float theta = (aqq - app) / (2.0f * apq);
+  float t = copysignf(1.0f, theta) / (fabsf(theta) + sqrtf(theta * theta + 1.0f));
+  float c = rsqrtf(t * t + 1.0f);
+  float s = t * c;
+  app -= t * apq;
+  aqq += t * apq;
+  apq = 0.0f;
+  float rp = arp, rq = arq;
+  arp = c * rp - s * rq;
+  arq = s * rp + c * rq;
+#pragma unroll
+  for (int r = 0; r < 3; ++r) {
+    float vp = V[r * 3 + p], vq = V[r * 3 + q];
+    V[r * 3 + p] = c * vp - s * vq;
+    V[r * 3 + q] = s * vp + c * vq;
+  }
+}
+
+__device__ __forceinline__ void sym_eigen3(float a00, float a11, float a22, float a01, float a02,
+                                           float a12, float* d, float* V) {
+#pragma unroll
+  for (int i = 0; i < 9; ++i) V[i] = (i % 4 == 0) ? 1.0f : 0.0f;
+  // Scale-aware stopping: rotations below ~1e-9 of the diagonal scale are
+  // skipped; 5 sweeps reach fp32 convergence (quadratic) for any input.
+#pragma unroll 1
+  for (int sweep = 0; sweep < 6; ++sweep) {
+    float off = fabsf(a01) + fabsf(a02) + fabsf(a12);
+    float scale = fabsf(a00) + fabsf(a11) + fabsf(a22) + off;
+    if (off <= 1e-9f * scale || off == 0.0f) break;
+    jacobi_rotate(a00, a11, a01, a02, a12, V, 0, 1);  // (p,q)=(0,1), r=2: a_rp=a02, a_rq=a12
+    jacobi_rotate(a00, a22, a02, a01, a12, V, 0, 2);  // (0,2), r=1: a_rp=a01, a_rq=a12 (=a21)
+    jacobi_rotate(a11, a22, a12, a01, a02, V, 1, 2);  // (1,2), r=0: a_rp=a10, a_rq=a20
+  }
+  d[0] = a00;
+  d[1] = a11;
+  d[2] = a22;
+}
+
+// ---------------------------------------------------------------------------
+// Constitutive model on the displacement gradient G = F - I (stored state).
+
+struct MatParams {
+  float two_mu;       // 2 mu
+  float lambda;
+  float yield_thr;    // sqrt(2/3) * yield_stress
+  float density;
+};
+
+// det(I + G) without forming I + G (exact expansion).
+__device__ __forceinline__ float det_I_plus(const float* G) {
+  float tr = G[0] + G[4] + G[8];
+  float m2 = (G[0] * G[4] - G[1] * G[3]) + (G[0] * G[8] - G[2] * G[6]) + (G[4] * G[8] - G[5] * G[7]);
+  float dg = G[0] * (G[4] * G[8] - G[5] * G[7]) - G[1] * (G[3] * G[8] - G[5] * G[6]) +
+             G[2] * (G[3] * G[7] - G[4] * G[6]);
+  return 1.0f + tr + m2 + dg;
+}
+
+// Left principal frame of F = I + G: U (columns) and Hencky strains
+// eps_i = log(sigma_i) = 0.5*log1p(e_i), e = eig(F F^T - I).
+__device__ __forceinline__ void hencky_frame(const float* G, float* U, float* eps) {
+  // E = G + G^T + G G^T
+  float e00 = 2.0f * G[0] + (G[0] * G[0] + G[1] * G[1] + G[2] * G[2]);
+  float e11 = 2.0f * G[4] + (G[3] * G[3] + G[4] * G[4] + G[5] * G[5]);
+  float e22 = 2.0f * G[8] + (G[6] * G[6] + G[7] * G[7] + G[8] * G[8]);
+  float e01 = G[1] + G[3] + (G[0] * G[3] + G[1] * G[4] + G[2] * G[5]);
+  float e02 = G[2] + G[6] + (G[0] * G[6] + G[1] * G[7] + G[2] * G[8]);
+  float e12 = G[5] + G[7] + (G[3] * G[6] + G[4] * G[7] + G[5] * G[8]);
+  float d[3];
+  sym_eigen3(e00, e11, e22, e01, e02, e12, d, U);
+#pragma unroll
+  for (int i = 0; i < 3; ++i) eps[i] = 0.5f * log1pf(fmaxf(d[i], -0.99999994f));
+}
+
+// S = U diag(s) U^T  (symmetric, row-major out)
+__device__ __forceinline__ void sym_from_frame(const float* U, const float* s, float* S) {
+#pragma unroll
+  for (int r = 0; r < 3; ++r)
+#pragma unroll
+    for (int c = r; c < 3; ++c) {
+      float v = U[r * 3 + 0] * s[0] * U[c * 3 + 0] + U[r * 3 + 1] * s[1] * U[c * 3 + 1] +
+                U[r * 3 + 2] * s[2] * U[c * 3 + 2];
+      S[r * 3 + c] = v;
+      S[c * 3 + r] = v;
+    }
+}
+
+// Kirchhoff stress tau = U diag(2 mu eps + lambda tr eps) U^T (mpm.hpp:152-161).
+__device__ __forceinline__ void kirchhoff_from_frame(const float* U, const float* eps,
+                                                     const MatParams& m, float* tau) {
+  float tr = eps[0] + eps[1] + eps[2];
+  float p[3] = {m.two_mu * eps[0] + m.lambda * tr, m.two_mu * eps[1] + m.lambda * tr,
+                m.two_mu * eps[2] + m.lambda * tr};
+  sym_from_frame(U, p, tau);
+}
+
+// Von Mises radial return (mpm.hpp:166-181) applied to the displacement
+// gradient in place. Returns true if the state yielded. eps is updated to
+// the projected strains (the principal frame U is unchanged), so the caller
+// can form the next Kirchhoff stress without another decomposition.
+__device__ __forceinline__ bool von_mises_project(float* G, const float* U, float* eps,
+                                                  const MatParams& m) {
+  float mean = (eps[0] + eps[1] + eps[2]) * (1.0f / 3.0f);
+  float dev[3] = {eps[0] - mean, eps[1] - mean, eps[2] - mean};
+  float dev_norm = sqrtf(dev[0] * dev[0] + dev[1] * dev[1] + dev[2] * dev[2]);
+  float sdn = m.two_mu * dev_norm;
+  if (sdn <= m.yield_thr) return false;
+  float k = m.yield_thr / sdn;
+  float sm1[3];
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    float e_new = mean + dev[i] * k;
+    sm1[i] = expm1f(e_new - eps[i]);  // sigma'/sigma - 1
+    eps[i] = e_new;
+  }
+  // F' = U diag(s) U^T F  =>  G' = (S - I)(I + G) + G
+  float Sm[9];
+  sym_from_frame(U, sm1, Sm);
+  float Gn[9];
+#pragma unroll
+  for (int r = 0; r < 3; ++r)
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+      Gn[r * 3 + c] = G[r * 3 + c] + Sm[r * 3 + c] + Sm[r * 3 + 0] * G[0 * 3 + c] +
+                      Sm[r * 3 + 1] * G[1 * 3 + c] + Sm[r * 3 + 2] * G[2 * 3 + c];
+#pragma unroll
+  for (int i = 0; i < 9; ++i) G[i] = Gn[i];
+  return true;
+}
+
+// ---------------------------------------------------------------------------
+// Quadratic B-spline weights (mpm.hpp:188-193), fx in [0.5, 1.5).
+__device__ __forceinline__ void bspline_w(float fx, float* w) {
+  float a = 1.5f - fx, b = fx - 1.0f, c = fx - 0.5f;
+  w[0] = 0.5f * a * a;
+  w[1] = 0.75f - b * b;
+  w[2] = 0.5f * c * c;
+}
+
+// ---------------------------------------------------------------------------
+// Colliders: one record per shape with its world<->local transform, body
+// twist and contact parameters, written by the rigid-step kernel.
+struct ShapeDev {
+  float Rinv[9];   // world -> shape-local rotation (R^T)
+  float tinv[3];   // world -> shape-local translation
+  float R[9];      // shape-local -> world rotation (for gradients)
+  float com[3];    // owning body's world COM
+  float vlin[3];   // body linear velocity
+  float vang[3];   // body angular velocity
+  float p[4];      // geometry parameters (see msim_shape)
+  float friction, k_n, k_t;
+  int type;
+  int body;        // body index within env (wrench slot)
+  int vol_dims[3];
+  float vol_origin[3];
+  float vol_voxel;
+  long long vol_off;  // offset into the volume sample pool
+};
+
+// Trilinear SDF volume lookup with clamping (sdf.hpp:46-62), software
+// interpolation (texture filtering would use 8-bit weights).
+__device__ __forceinline__ float vol_at(const float* s, const ShapeDev& sh, int i, int j, int k) {
+  return s[((long long)k * sh.vol_dims[1] + j) * sh.vol_dims[0] + i];
+}
+__device__ __forceinline__ float vol_interp(const float* pool, const ShapeDev& sh, f3 p) {
+  const float* s = pool + sh.vol_off;
+  float inv = 1.0f / sh.vol_voxel;
+  f3 local = {(p.x - sh.vol_origin[0]) * inv, (p.y - sh.vol_origin[1]) * inv,
+              (p.z - sh.vol_origin[2]) * inv};
+  f3 cl = {fminf(fmaxf(local.x, 0.0f), sh.vol_dims[0] - 1.0f),
+           fminf(fmaxf(local.y, 0.0f), sh.vol_dims[1] - 1.0f),
+           fminf(fmaxf(local.z, 0.0f), sh.vol_dims[2] - 1.0f)};
+  float outside = sh.vol_voxel * norm(local - cl);
+  int i0 = min((int)cl.x, sh.vol_dims[0] - 2);
+  int j0 = min((int)cl.y, sh.vol_dims[1] - 2);
+  int k0 = min((int)cl.z, sh.vol_dims[2] - 2);
+  float fx = cl.x - i0, fy = cl.y - j0, fz = cl.z - k0;
+  float c00 = vol_at(s, sh, i0, j0, k0) * (1 - fx) + vol_at(s, sh, i0 + 1, j0, k0) * fx;
+  float c10 = vol_at(s, sh, i0, j0 + 1, k0) * (1 - fx) + vol_at(s, sh, i0 + 1, j0 + 1, k0) * fx;
+  float c01 = vol_at(s, sh, i0, j0, k0 + 1) * (1 - fx) + vol_at(s, sh, i0 + 1, j0, k0 + 1) * fx;
+  float c11 = vol_at(s, sh, i0, j0 + 1, k0 + 1) * (1 - fx) + vol_at(s, sh, i0 + 1, j0 + 1, k0 + 1) * fx;
+  float c0 = c00 * (1 - fy) + c10 * fy;
+  float c1 = c01 * (1 - fy) + c11 * fy;
+  return c0 * (1 - fz) + c1 * fz + outside;
+}
+
+// sdf_local (sdf.hpp:114-135)
+__device__ __forceinline__ float sdf_local(const ShapeDev& sh, const float* pool, f3 p) {
+  switch (sh.type) {
+    case 0:
+      return sh.p[0] * p.x + sh.p[1] * p.y + sh.p[2] * p.z - sh.p[3];
+    case 1:
+      return norm(p) - sh.p[0];
+    case 2: {
+      f3 q = {fabsf(p.x) - sh.p[0], fabsf(p.y) - sh.p[1], fabsf(p.z) - sh.p[2]};
+      f3 qp = {fmaxf(q.x, 0.0f), fmaxf(q.y, 0.0f), fmaxf(q.z, 0.0f)};
+      return norm(qp) + fminf(fmaxf(q.x, fmaxf(q.y, q.z)), 0.0f);
+    }
+    case 3: {
+      f3 q = {p.x, p.y, p.z - fminf(fmaxf(p.z, -sh.p[0]), sh.p[0])};
+      return norm(q) - sh.p[1];
+    }
+    default:
+      return vol_interp(pool, sh, p);
+  }
+}
+
+// sdf_gradient_local (sdf.hpp:139-179), tie-breaks toward +x.
+__device__ __forceinline__ f3 sdf_grad_local(const ShapeDev& sh, const float* pool, f3 p) {
+  const f3 tie = {1.0f, 0.0f, 0.0f};
+  switch (sh.type) {
+    case 0:
+      return {sh.p[0], sh.p[1], sh.p[2]};
+    case 1: {
+      float n = norm(p);
+      return n < 1e-12f ? tie : (1.0f / n) * p;
+    }
+    case 2: {
+      f3 q = {fabsf(p.x) - sh.p[0], fabsf(p.y) - sh.p[1], fabsf(p.z) - sh.p[2]};
+      f3 sg = {p.x < 0 ? -1.0f : 1.0f, p.y < 0 ? -1.0f : 1.0f, p.z < 0 ? -1.0f : 1.0f};
+      f3 qp = {fmaxf(q.x, 0.0f), fmaxf(q.y, 0.0f), fmaxf(q.z, 0.0f)};
+      float out = norm(qp);
+      if (out > 1e-12f) return (1.0f / out) * f3{sg.x * qp.x, sg.y * qp.y, sg.z * qp.z};
+      int ax = 0;
+      float qa = q.x;
+      if (q.y > qa) { ax = 1; qa = q.y; }
+      if (q.z > qa) { ax = 2; }
+      return ax == 0 ? f3{sg.x, 0, 0} : (ax == 1 ? f3{0, sg.y, 0} : f3{0, 0, sg.z});
+    }
+    case 3: {
+      f3 q = {p.x, p.y, p.z - fminf(fmaxf(p.z, -sh.p[0]), sh.p[0])};
+      float n = norm(q);
+      return n < 1e-12f ? tie : (1.0f / n) * q;
+    }
+    default: {
+      float h = 0.5f * sh.vol_voxel;
+      f3 g;
+      g.x = (vol_interp(pool, sh, p + f3{h, 0, 0}) - vol_interp(pool, sh, p - f3{h, 0, 0})) / (2 * h);
+      g.y = (vol_interp(pool, sh, p + f3{0, h, 0}) - vol_interp(pool, sh, p - f3{0, h, 0})) / (2 * h);
+      g.z = (vol_interp(pool, sh, p + f3{0, 0, h}) - vol_interp(pool, sh, p - f3{0, 0, h})) / (2 * h);
+      float n = norm(g);
+      return n < 1e-12f ? tie : (1.0f / n) * g;
+    }
+  }
+}
+
+// penalty_point_force (coupling.hpp:125-144). Returns false outside the band.
+__device__ __forceinline__ bool penalty_force(const ShapeDev& sh, const float* pool, f3 x, f3 v,
+                                              float r_c, float c_d, f3& f, float& pen) {
+  f3 local = matvec(sh.Rinv, x) + f3{sh.tinv[0], sh.tinv[1], sh.tinv[2]};
+  float phi = sdf_local(sh, pool, local);
+  if (!(phi < r_c)) return false;
+  f3 n = matvec(sh.R, sdf_grad_local(sh, pool, local));
+  float depth = r_c - phi;
+  f = (sh.k_n * depth) * n;
+  f3 com = {sh.com[0], sh.com[1], sh.com[2]};
+  f3 vb = f3{sh.vlin[0], sh.vlin[1], sh.vlin[2]} + cross(f3{sh.vang[0], sh.vang[1], sh.vang[2]}, x - com);
+  f3 vrel = v - vb;
+  float vn = dot(vrel, n);
+  f = f + (-c_d * fminf(0.0f, vn)) * n;
+  f3 vt = vrel - vn * n;
+  float vtn = norm(vt);
+  if (vtn > 1e-12f) {
+    float cap = fminf(sh.friction * sh.k_n * depth, sh.k_t * vtn);
+    f = f - (cap / vtn) * vt;
+  }
+  pen = fmaxf(0.0f, -phi);
+  return true;
+}
+
+}  // namespace msim_dev

@@ -1,0 +1,178 @@
+// Internal device-state layout shared by the kernels (msim_kernels.cu) and
+// the C-ABI host implementation (msim_api.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/msim_gpu.h"
+#include "msim_device.cuh"
+
+namespace msim_impl {
+
+constexpr int kMaxBodiesPerEnv = 32;  // wrench slots reduced in shared memory
+
+// Internal error codes latched per environment (first one wins); mapped to
+// MSIM_ERR_INVALID / MSIM_ERR_DIVERGED with the reference's messages.
+enum : int {
+  kErrDetStress = 20,     // kirchhoff_stress: det(F) must be > 0        (mpm.hpp:153-154)
+  kErrDetReturn = 21,     // von_mises_return_map: det(F) must be > 0    (mpm.hpp:167-168)
+  kErrLost = 30,          // lost particle fraction exceeds threshold    (mpm.hpp:246-249)
+  kErrCfl = 31,           // CFL violation persists after max halvings   (mpm.hpp:404-405)
+  kErrNan = 32,           // NaN/Inf in particle <i>                     (mpm.hpp:374-378)
+};
+constexpr int kLostBit = 31;
+constexpr uint32_t kEnvMask = 0x7FFFFFu;  // meta = lost<<31 | env<<8 | material
+
+// Particle state, fp32 structure-of-arrays (one buffer of a double-buffered
+// pair; the P2G pass writes particles into bucket order of the next buffer).
+struct Particles {
+  float* x[3];
+  float* v[3];
+  float* C[9];
+  float* G[9];  // displacement gradient F - I
+  float* mass;
+  float* vol0;
+  uint32_t* meta;
+  int32_t* pid;  // original (upload-order) index within the context
+};
+
+struct BodyDev {
+  int mode;
+  int _pad;
+  double q[4];
+  double t[3];
+  double v[3];
+  double w[3];
+  double mass;
+  double inertia[3];
+  double com_off[3];
+};
+
+struct ShapeHost {  // shape description kept on device in double for the rigid kernel
+  int type;
+  int body;
+  double lq[4];
+  double lt[3];
+  double friction, k_n, k_t;
+  double p[4];
+  int vol_dims[3];
+  double vol_origin[3];
+  double vol_voxel;
+  long long vol_off;
+};
+
+// Everything a kernel needs, passed by value.
+struct SimParams {
+  // grid
+  double h, inv_h;
+  double origin[3];
+  int dims[3];
+  int bdims[3];              // node blocks (4^3 nodes) per axis
+  long long nodes_per_env;
+  int blocks_per_env;
+  int n_env;
+  unsigned boundary_slip;    // bit f set => face f is slip
+  float gravity[3];
+  float h_f, d_inv_f;        // h, 4/h^2
+  long long n;               // particles in context
+  int n_keys;                // n_env*blocks_per_env + 1 (lost bucket last)
+  int split;                 // keep momentum and force separately
+  int grid_mode;             // coupling mode grid
+  float r_c_particle, r_c_grid, c_d;
+  int cycle;                 // current CFL cycle index
+  int manual;                // phase API: all envs run, dt from dt_manual
+  float dt_manual;
+
+  Particles cur, nxt;
+  const msim_dev::MatParams* mats;
+
+  // per env
+  const int* cycles;
+  const float* dt_cycle;
+  const long long* env_off;      // n_env+1
+  const int* shape_off;          // n_env+1
+  const int* body_off;           // n_env+1
+  msim_dev::ShapeDev* shapes;
+  const float* vol_pool;
+  double* wrench;                // per body: force xyz, torque xyz (accumulating)
+  double* applied;               // per env: sum of applied penalty force (this cycle), xyz
+  double* react;                 // per env: sum of reactions (this cycle), xyz
+  unsigned* max_pen_bits;        // per env, float bits
+  unsigned* vmax_bits;           // per env, float bits
+  long long* lost_count;         // per env
+  int* err_code;                 // per env
+  int* err_pid;                  // per env: first offending particle (min pid)
+  const double* mean_mass;       // per env (grid-mode scaling)
+
+  // binning
+  int* key;
+  int* rank;
+  int* bucket_count;             // n_keys
+  int* bucket_start;             // n_keys + 1
+  int* active_buckets;           // list
+  int* n_active_buckets;
+  int* perm;
+  int* base_dbg;                 // optional: base per pid (3 ints), -10 if lost
+
+  // grid (float4 per node)
+  float4* gPM;                   // momentum (or momentum + dt*force) xyz, mass w
+  float4* gF;                    // force xyz (split mode)
+  float4* gV;                    // velocity xyz
+  int* nb_flag;                  // node-block touched flags (n_env*blocks_per_env)
+  int* nb_scan;
+  int* nb_list;
+  int* n_nb;
+
+  int* scan_tmp;
+  double* balance_max;           // per env: max force-balance error this step
+  double lost_threshold;
+};
+
+// kernel launchers (msim_kernels.cu)
+void launch_convert_in(const SimParams& P, long long n, const double* x, const double* v,
+                       const double* F, const double* C, const double* mass, const double* vol0,
+                       const int32_t* mat, const int* env_of, long long first_pid, int write_all,
+                       cudaStream_t s);
+void launch_overwrite(const SimParams& P, int env, long long first_pid, long long n,
+                      const double* x, const double* v, const double* F, const double* C,
+                      cudaStream_t s);
+void launch_convert_out(const SimParams& P, int env, long long first_pid, long long n, double* x,
+                        double* v, double* F, double* C, uint8_t* lost, cudaStream_t s);
+void launch_vmax(const SimParams& P, cudaStream_t s);
+void launch_plan(const SimParams& P, double dt, double cfl_h, int max_halvings, int* max_cycles,
+                 int* any_err, int* cyc_sum, cudaStream_t s);
+void launch_cycle(const SimParams& P, int stage_mask, cudaStream_t s);
+void launch_rigid(const SimParams& P, BodyDev* bodies, const ShapeHost* shapes, double* pending,
+                  int integrate, double dt_r, const double* rigid_gravity3, int only_env,
+                  cudaStream_t s);
+void launch_stage_wrenches(const SimParams& P, double* pending, int n_bodies, cudaStream_t s);
+void launch_constitutive(const msim_dev::MatParams m, long long n, const double* F, double* tau,
+                         double* Fp, int* bad, cudaStream_t s);
+void launch_grid_out(const SimParams& P, int env, double* mass, double* mom, double* force,
+                     double* vel, cudaStream_t s);
+void launch_grid_vel_in(const SimParams& P, int env, const double* vel, cudaStream_t s);
+void launch_clear_env_grid(const SimParams& P, int env, cudaStream_t s);
+void launch_binning_out(const SimParams& P, int env, long long first_pid, long long n_env_p,
+                        const int* base, int* cell_count, int* cell_start, int* cell_particles,
+                        int* node_flag, int* node_scan, int* node_list, int* n_list,
+                        long long* active_nodes, int* tmp, cudaStream_t s);
+void scan_exclusive(const int* in, int* out, int n, int* compact_list, int* n_compact, int* tmp,
+                    cudaStream_t s);
+size_t scan_tmp_ints(int n);
+
+// cycle stage bits for launch_cycle
+enum : int {
+  kStageClear = 1,
+  kStageBin = 2,
+  kStageP2G = 4,
+  kStageGrid = 8,
+  kStageG2P = 16,
+  kStageEnd = 32,
+  kStageAll = 63,
+};
+
+}  // namespace msim_impl

@@ -1,0 +1,231 @@
+"""Python mirror of the reference's soft-body API on top of the C ABI.
+
+``GpuWorld`` is a thin, stateless-in-Python handle over one ``msim_gpu_ctx``
+(include/msim_gpu.h): all state lives on the device. Method names follow the
+reference (mpm.hpp / coupling.hpp): ``soft_substep``, ``p2g``,
+``grid_update``, ``g2p_advect``, ``env_step``, ``sync_rigid_to_soft``.
+Errors are raised as the reference's exception types: ``SimulationDiverged``
+(MSIM_ERR_DIVERGED) and ``ValueError`` for std::invalid_argument.
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from . import abi
+from .scenes import Scene
+
+
+class SimulationDiverged(RuntimeError):
+    """mpm.hpp:18-20"""
+
+
+class DeviceError(RuntimeError):
+    pass
+
+
+def _check(lib, ctx, rc: int):
+    if rc == abi.MSIM_OK:
+        return
+    msg = lib.msim_gpu_last_error(ctx).decode() if ctx else lib.msim_gpu_create_error().decode()
+    if rc == abi.MSIM_ERR_DIVERGED:
+        raise SimulationDiverged(msg)
+    if rc == abi.MSIM_ERR_INVALID:
+        raise ValueError(msg)
+    raise DeviceError(msg)
+
+
+class GpuWorld:
+    """All environments of a Scene on one device."""
+
+    def __init__(self, scene: Scene, device: int = 0, split_channels: bool = False,
+                 record_binning: bool = False):
+        self.lib = lib = abi.load()
+        self.scene = scene
+        self.n_env = len(scene.envs)
+        mats = scene.material_array()
+        ctx = C.c_void_p()
+        desc = scene.desc()
+        _check(lib, None, lib.msim_gpu_create(C.byref(desc), mats, len(scene.materials), self.n_env, device,
+                                              C.byref(ctx)))
+        self.ctx = ctx
+        if split_channels:
+            self.set_split_channels(True)
+        if record_binning:
+            _check(lib, ctx, lib.msim_gpu_set_record_binning(ctx, 1))
+        self.counts = [e.n for e in scene.envs]
+        self.offsets = np.zeros(self.n_env + 1, dtype=np.int64)
+        self.offsets[1:] = np.cumsum(self.counts)
+        self.upload(scene)
+        cp = abi.Coupling()
+        cp.mode, cp.r_c_factor, cp.c_d = scene.coupling_mode, scene.r_c_factor, scene.c_d
+        _check(lib, ctx, lib.msim_gpu_set_coupling(ctx, C.byref(cp)))
+        g = np.asarray(scene.rigid_gravity, dtype=np.float64)
+        _check(lib, ctx, lib.msim_gpu_set_rigid_gravity(ctx, abi.dptr(g)))
+        for e, env in enumerate(scene.envs):
+            if env.bodies:
+                self.set_bodies(e, env.bodies, env.shapes)
+
+    # ---- setup -------------------------------------------------------------
+    def upload(self, scene: Scene):
+        n = scene.n_particles
+
+        def cat(attr, shape, default):
+            parts = []
+            for e in scene.envs:
+                a = getattr(e, attr)
+                if a is None:
+                    a = np.broadcast_to(default, (e.n,) + shape)
+                parts.append(np.asarray(a, dtype=np.float64).reshape((e.n,) + shape))
+            return np.ascontiguousarray(np.concatenate(parts) if parts else np.zeros((0,) + shape))
+
+        x = cat("x", (3,), np.zeros(3))
+        v = cat("v", (3,), np.zeros(3))
+        F = cat("F", (3, 3), np.eye(3))
+        Cm = cat("C", (3, 3), np.zeros((3, 3)))
+        m = np.ascontiguousarray(np.concatenate([e.mass for e in scene.envs]).astype(np.float64))
+        v0 = np.ascontiguousarray(np.concatenate([e.vol0 for e in scene.envs]).astype(np.float64))
+        mat = np.ascontiguousarray(np.concatenate(
+            [e.material if e.material is not None else np.zeros(e.n, np.int32) for e in scene.envs]
+        ).astype(np.int32))
+        _check(self.lib, self.ctx, self.lib.msim_gpu_set_particles(
+            self.ctx, n, abi.lptr(self.offsets), abi.dptr(x), abi.dptr(v), abi.dptr(F), abi.dptr(Cm),
+            abi.dptr(m), abi.dptr(v0), abi.iptr(mat)))
+
+    def set_bodies(self, env: int, bodies, shapes):
+        B = (abi.Body * max(len(bodies), 1))(*[b.to_c() for b in bodies])
+        S = (abi.Shape * max(len(shapes), 1))(*[s.to_c() for s in shapes])
+        _check(self.lib, self.ctx, self.lib.msim_gpu_set_bodies(self.ctx, env, B, len(bodies), S, len(shapes)))
+
+    def sync_rigid_to_soft(self, env: int, bodies):
+        """sync_rigid_to_soft (coupling.hpp:106-117) with new body states."""
+        B = (abi.Body * max(len(bodies), 1))(*[b.to_c() for b in bodies])
+        _check(self.lib, self.ctx, self.lib.msim_gpu_sync_bodies(self.ctx, env, B, len(bodies)))
+
+    def set_dt(self, dt: float):
+        _check(self.lib, self.ctx, self.lib.msim_gpu_set_dt(self.ctx, dt))
+
+    def set_gravity(self, g):
+        g = np.asarray(g, dtype=np.float64)
+        _check(self.lib, self.ctx, self.lib.msim_gpu_set_gravity(self.ctx, abi.dptr(g)))
+
+    def set_lost_fraction_threshold(self, t: float):
+        _check(self.lib, self.ctx, self.lib.msim_gpu_set_lost_fraction_threshold(self.ctx, t))
+
+    def set_split_channels(self, on: bool):
+        _check(self.lib, self.ctx, self.lib.msim_gpu_set_split_channels(self.ctx, 1 if on else 0))
+
+    def write_particles(self, env: int, x=None, v=None, F=None, Cm=None):
+        n = self.counts[env]
+        f = lambda a, s: None if a is None else np.ascontiguousarray(np.asarray(a, np.float64).reshape((n,) + s))
+        x, v, F, Cm = f(x, (3,)), f(v, (3,)), f(F, (3, 3)), f(Cm, (3, 3))
+        _check(self.lib, self.ctx, self.lib.msim_gpu_write_particles(
+            self.ctx, env, n, abi.dptr(x), abi.dptr(v), abi.dptr(F), abi.dptr(Cm)))
+
+    # ---- stepping ----------------------------------------------------------
+    def soft_substep(self, n: int = 1):
+        cyc = np.zeros(self.n_env, dtype=np.int32)
+        _check(self.lib, self.ctx, self.lib.msim_gpu_soft_substep(self.ctx, n, abi.iptr(cyc)))
+        return cyc
+
+    def p2g(self):
+        _check(self.lib, self.ctx, self.lib.msim_gpu_p2g(self.ctx))
+
+    def grid_update(self):
+        _check(self.lib, self.ctx, self.lib.msim_gpu_grid_update(self.ctx))
+
+    def g2p_advect(self):
+        _check(self.lib, self.ctx, self.lib.msim_gpu_g2p(self.ctx))
+
+    def env_step(self, n_rigid: int | None = None, n_soft: int | None = None) -> abi.StepReport:
+        rep = abi.StepReport()
+        nr = self.scene.n_rigid if n_rigid is None else n_rigid
+        ns = self.scene.n_soft if n_soft is None else n_soft
+        _check(self.lib, self.ctx, self.lib.msim_gpu_env_step(self.ctx, nr, ns, C.byref(rep)))
+        return rep
+
+    # ---- readback ----------------------------------------------------------
+    def particles(self, env: int = 0):
+        n = self.counts[env]
+        x = np.zeros((n, 3))
+        v = np.zeros((n, 3))
+        F = np.zeros((n, 3, 3))
+        Cm = np.zeros((n, 3, 3))
+        lost = np.zeros(n, dtype=np.uint8)
+        _check(self.lib, self.ctx, self.lib.msim_gpu_read_particles(
+            self.ctx, env, abi.dptr(x), abi.dptr(v), abi.dptr(F), abi.dptr(Cm), abi.u8ptr(lost)))
+        return dict(x=x, v=v, F=F, C=Cm, lost=lost)
+
+    def grid(self, env: int = 0):
+        nn = int(np.prod(self.scene.dims))
+        m = np.zeros(nn)
+        p = np.zeros((nn, 3))
+        f = np.zeros((nn, 3))
+        vel = np.zeros((nn, 3))
+        _check(self.lib, self.ctx, self.lib.msim_gpu_read_grid(
+            self.ctx, env, abi.dptr(m), abi.dptr(p), abi.dptr(f), abi.dptr(vel)))
+        return dict(mass=m, momentum=p, force=f, velocity=vel)
+
+    def write_grid_velocity(self, env: int, vel: np.ndarray):
+        vel = np.ascontiguousarray(np.asarray(vel, dtype=np.float64).reshape(-1, 3))
+        _check(self.lib, self.ctx, self.lib.msim_gpu_write_grid_velocity(self.ctx, env, abi.dptr(vel)))
+
+    def binning(self, env: int = 0):
+        n = self.counts[env]
+        d = self.scene.dims
+        nbins = (d[0] - 2) * (d[1] - 2) * (d[2] - 2)
+        nn = d[0] * d[1] * d[2]
+        base = np.zeros((n, 3), dtype=np.int32)
+        cs = np.zeros(nbins + 1, dtype=np.int32)
+        cp = np.zeros(max(n, 1), dtype=np.int32)
+        act = np.zeros(nn, dtype=np.int64)
+        n_alive = C.c_int64()
+        n_act = C.c_int64()
+        _check(self.lib, self.ctx, self.lib.msim_gpu_read_binning(
+            self.ctx, env, abi.iptr(base), abi.iptr(cs), cs.size, abi.iptr(cp), cp.size, C.byref(n_alive),
+            abi.lptr(act), act.size, C.byref(n_act)))
+        return dict(base=base, cell_start=cs, cell_particles=cp[: n_alive.value], active_nodes=act[: n_act.value])
+
+    def wrenches(self, env: int = 0, pending: bool = False):
+        nb = len(self.scene.envs[env].bodies)
+        f = np.zeros((max(nb, 1), 3))
+        t = np.zeros((max(nb, 1), 3))
+        _check(self.lib, self.ctx, self.lib.msim_gpu_read_wrenches(self.ctx, env, 1 if pending else 0,
+                                                                    abi.dptr(f), abi.dptr(t)))
+        return f[:nb], t[:nb]
+
+    def bodies(self, env: int = 0):
+        nb = len(self.scene.envs[env].bodies)
+        B = (abi.Body * max(nb, 1))()
+        _check(self.lib, self.ctx, self.lib.msim_gpu_read_bodies(self.ctx, env, B, nb))
+        return [B[i] for i in range(nb)]
+
+    def report(self, env: int = 0) -> abi.StepReport:
+        r = abi.StepReport()
+        _check(self.lib, self.ctx, self.lib.msim_gpu_read_report(self.ctx, env, C.byref(r)))
+        return r
+
+    def lost_count(self, env: int = 0) -> int:
+        return int(self.lib.msim_gpu_lost_count(self.ctx, env))
+
+    def constitutive(self, F: np.ndarray, mat: int = 0):
+        """(kirchhoff_stress(F), von_mises_return_map(F)) on the device code path."""
+        F = np.ascontiguousarray(np.asarray(F, dtype=np.float64).reshape(-1, 3, 3))
+        n = F.shape[0]
+        tau = np.zeros_like(F)
+        Fp = np.zeros_like(F)
+        _check(self.lib, self.ctx, self.lib.msim_gpu_constitutive(self.ctx, mat, n, abi.dptr(F), abi.dptr(tau),
+                                                                  abi.dptr(Fp)))
+        return tau, Fp
+
+    def close(self):
+        if getattr(self, "ctx", None):
+            self.lib.msim_gpu_destroy(self.ctx)
+            self.ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
