@@ -234,6 +234,22 @@ int msim_gpu_read_bodies(msim_gpu_ctx* ctx, int env, msim_body* bodies, int n_bo
 int msim_gpu_read_report(msim_gpu_ctx* ctx, int env, msim_step_report* report);
 int64_t msim_gpu_lost_count(msim_gpu_ctx* ctx, int env);
 
+/* ---- batched host<->device exchange (one copy for all envs) ------------ */
+int msim_gpu_body_count(const msim_gpu_ctx* ctx, int env); /* env < 0: all envs */
+/* Overwrite the state of every body of every env (concatenated in env order)
+ * and sync mirrors (sync_rigid_to_soft for all envs). */
+int msim_gpu_sync_all_bodies(msim_gpu_ctx* ctx, const msim_body* bodies, int n_total);
+/* force xyz, torque xyz per body, all envs concatenated (n_total*6 doubles). */
+int msim_gpu_read_all_wrenches(msim_gpu_ctx* ctx, int pending, double* wrench6);
+
+/* ---- instrumentation ---------------------------------------------------- */
+void* msim_gpu_stream(msim_gpu_ctx* ctx);          /* the context's cudaStream_t */
+int64_t msim_gpu_launches(const msim_gpu_ctx* ctx);  /* kernels launched so far */
+int msim_gpu_set_kernel_timing(msim_gpu_ctx* ctx, int on);  /* CUDA events per kernel; resets */
+int msim_gpu_kernel_count(void);
+int msim_gpu_kernel_stats(msim_gpu_ctx* ctx, int id, const char** name, int64_t* launches,
+                          double* total_ms);
+
 /* ---- test hooks (constitutive model on raw arrays, device code path) ---- */
 /* tau[n*9] = kirchhoff_stress(F), Fp[n*9] = von_mises_return_map(F) for material
  * `mat`. Returns MSIM_ERR_INVALID if some det(F) <= 0. */

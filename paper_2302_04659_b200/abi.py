@@ -119,7 +119,9 @@ EXPORTED = [
     "msim_gpu_set_record_binning", "msim_gpu_read_binning", "msim_gpu_read_wrenches",
     "msim_gpu_read_bodies", "msim_gpu_read_report", "msim_gpu_lost_count",
     "msim_gpu_constitutive", "msim_rng_create", "msim_rng_destroy", "msim_rng_uniform",
-    "msim_rng_fill_uniform",
+    "msim_rng_fill_uniform", "msim_gpu_body_count", "msim_gpu_sync_all_bodies",
+    "msim_gpu_read_all_wrenches", "msim_gpu_stream", "msim_gpu_launches", "msim_gpu_set_kernel_timing",
+    "msim_gpu_kernel_count", "msim_gpu_kernel_stats",
     "msim_seed_box_count", "msim_seed_box",
 ]
 
@@ -166,6 +168,14 @@ _SIGS = {
     "msim_rng_uniform": (C.c_double, [_vp, C.c_double, C.c_double]),
     "msim_rng_fill_uniform": (None, [_vp, C.c_int64, C.c_double, C.c_double, _dp]),
     "msim_seed_box_count": (C.c_int64, [_dp, _dp, C.c_double]),
+    "msim_gpu_body_count": (C.c_int, [_vp, C.c_int]),
+    "msim_gpu_sync_all_bodies": (C.c_int, [_vp, C.POINTER(Body), C.c_int]),
+    "msim_gpu_read_all_wrenches": (C.c_int, [_vp, C.c_int, _dp]),
+    "msim_gpu_stream": (_vp, [_vp]),
+    "msim_gpu_launches": (C.c_int64, [_vp]),
+    "msim_gpu_set_kernel_timing": (C.c_int, [_vp, C.c_int]),
+    "msim_gpu_kernel_count": (C.c_int, []),
+    "msim_gpu_kernel_stats": (C.c_int, [_vp, C.c_int, C.POINTER(C.c_char_p), _lp, _dp]),
     "msim_seed_box": (C.c_int64, [_vp, _dp, _dp, C.c_double, C.c_double, _dp, _dp]),
 }
 

@@ -114,6 +114,7 @@ struct msim_gpu_ctx {
   int* d_ctl = nullptr;
 
   double time = 0.0;
+  KernelTimer timer;
 };
 
 namespace {
@@ -135,6 +136,7 @@ MatParams mat_params(const msim_material& m) {
 
 SimParams params(msim_gpu_ctx* c) {
   SimParams P{};
+  P.timer = &c->timer;
   const msim_soft_desc& d = c->desc;
   P.h = d.h;
   P.inv_h = 1.0 / d.h;
@@ -414,6 +416,7 @@ int substeps(msim_gpu_ctx* c, int n_sub, int32_t* cycles_out) {
                 c->d_ctl + 1, c->cyc_sum_d.as<int>(), c->stream);
     CK(cudaGetLastError());
     CK(cudaStreamSynchronize(c->stream));
+    c->timer.flush();
     if (c->h_ctl[1]) return collect_errors(c);
     const int maxc = c->h_ctl[0];
     for (int cy = 0; cy < maxc; ++cy) run_cycle(c, cy, 0, kStageAll);
@@ -421,6 +424,7 @@ int substeps(msim_gpu_ctx* c, int n_sub, int32_t* cycles_out) {
       CK(cudaMemcpyAsync(cycles_out, c->cycles_d.p, sizeof(int) * c->n_env, cudaMemcpyDeviceToHost, c->stream));
   }
   CK(cudaStreamSynchronize(c->stream));
+  c->timer.flush();
   return collect_errors(c);
 }
 
@@ -1062,6 +1066,68 @@ int msim_gpu_constitutive(msim_gpu_ctx* c, int mat, int64_t n, const double* F, 
     if (Fp) CK(cudaMemcpyAsync(Fp, dp, sizeof(double) * 9 * n, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
     if (hbad) return fail(c, MSIM_ERR_INVALID, "kirchhoff_stress: det(F) must be > 0");
+    return MSIM_OK;
+  });
+}
+
+
+void* msim_gpu_stream(msim_gpu_ctx* c) { return c ? (void*)c->stream : nullptr; }
+
+int64_t msim_gpu_launches(const msim_gpu_ctx* c) { return c ? c->timer.launches : -1; }
+
+int msim_gpu_set_kernel_timing(msim_gpu_ctx* c, int on) {
+  return guarded(c, [&]() -> int {
+    set_device(c);
+    CK(cudaStreamSynchronize(c->stream));
+    c->timer.reset();
+    c->timer.enabled = on != 0;
+    return MSIM_OK;
+  });
+}
+
+int msim_gpu_kernel_count(void) { return kKernelIds; }
+
+int msim_gpu_kernel_stats(msim_gpu_ctx* c, int id, const char** name, int64_t* launches, double* total_ms) {
+  if (id < 0 || id >= kKernelIds) return MSIM_ERR_INVALID;
+  if (cudaSetDevice(c->device) != cudaSuccess || cudaStreamSynchronize(c->stream) != cudaSuccess)
+    return MSIM_ERR_DEVICE;
+  c->timer.flush();
+  if (name) *name = kernel_name(id);
+  if (launches) *launches = c->timer.count[id];
+  if (total_ms) *total_ms = c->timer.total_ms[id];
+  return MSIM_OK;
+}
+
+int msim_gpu_body_count(const msim_gpu_ctx* c, int env) {
+  if (env < 0) return c->n_bodies;
+  if (env >= c->n_env) return -1;
+  return (int)c->bodies_h[env].size();
+}
+
+int msim_gpu_sync_all_bodies(msim_gpu_ctx* c, const msim_body* bodies, int n_total) {
+  return guarded(c, [&]() -> int {
+    if (n_total != c->n_bodies) return fail(c, MSIM_ERR_INVALID, "sync_all_bodies: body count mismatch");
+    if (n_total == 0) return MSIM_OK;
+    set_device(c);
+    static_assert(sizeof(msim_body) == sizeof(BodyDev), "body layouts differ");
+    // msim_body and BodyDev share one layout; mass/inertia/com are taken from
+    // the caller like sync_rigid_to_soft copies whole bodies.
+    CK(cudaMemcpyAsync(c->bodies_d.p, bodies, sizeof(msim_body) * n_total, cudaMemcpyHostToDevice, c->stream));
+    SimParams P = params(c);
+    launch_rigid(P, c->bodies_d.as<BodyDev>(), c->shapes_host_d.as<ShapeHost>(), c->pending_d.as<double>(), 0,
+                 0.0, c->rigid_gravity, -1, c->stream);
+    CK(cudaGetLastError());
+    return MSIM_OK;
+  });
+}
+
+int msim_gpu_read_all_wrenches(msim_gpu_ctx* c, int pending, double* wrench6) {
+  return guarded(c, [&]() -> int {
+    if (c->n_bodies == 0) return MSIM_OK;
+    set_device(c);
+    const void* src = pending ? c->pending_d.p : c->wrench_d.p;
+    CK(cudaMemcpyAsync(wrench6, src, sizeof(double) * 6 * c->n_bodies, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
     return MSIM_OK;
   });
 }

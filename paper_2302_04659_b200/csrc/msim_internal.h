@@ -65,8 +65,71 @@ struct ShapeHost {  // shape description kept on device in double for the rigid 
   long long vol_off;
 };
 
+// Per-kernel CUDA-event timing on the context stream (bench / profiling) and
+// the count of kernel launches. Host-only; SimParams carries a pointer.
+enum KernelId : int {
+  kKPlan = 0, kKVmax, kKClear, kKBin, kKBucketScan, kKScatter, kKP2G, kKBlockScan, kKGrid, kKG2P,
+  kKEnd, kKRigid, kKStage, kKernelIds
+};
+inline const char* kernel_name(int id) {
+  static const char* names[kKernelIds] = {"k_plan", "k_vmax", "k_clear", "k_bin", "bucket_scan", "k_scatter",
+                                          "k_p2g", "block_scan", "k_grid", "k_g2p", "k_cycle_end",
+                                          "k_rigid", "k_stage"};
+  return id >= 0 && id < kKernelIds ? names[id] : "?";
+}
+struct KernelTimer {
+  bool enabled = false;
+  long long launches = 0;
+  std::vector<cudaEvent_t> pool;
+  size_t used = 0;
+  struct Rec { int id; cudaEvent_t a, b; };
+  std::vector<Rec> recs;
+  double total_ms[kKernelIds] = {};
+  long long count[kKernelIds] = {};
+  cudaEvent_t ev() {
+    if (used == pool.size()) {
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      pool.push_back(e);
+    }
+    return pool[used++];
+  }
+  cudaEvent_t begin(cudaStream_t s, int nlaunch) {
+    launches += nlaunch;
+    if (!enabled) return nullptr;
+    cudaEvent_t a = ev();
+    cudaEventRecord(a, s);
+    return a;
+  }
+  void end(int id, cudaEvent_t a, cudaStream_t s) {
+    if (!enabled || !a) return;
+    cudaEvent_t b = ev();
+    cudaEventRecord(b, s);
+    recs.push_back({id, a, b});
+  }
+  void flush() {  // call after the stream is synchronized
+    for (const Rec& r : recs) {
+      float ms = 0.f;
+      if (cudaEventElapsedTime(&ms, r.a, r.b) == cudaSuccess) {
+        total_ms[r.id] += ms;
+        count[r.id] += 1;
+      }
+    }
+    recs.clear();
+    used = 0;
+  }
+  void reset() {
+    flush();
+    for (int i = 0; i < kKernelIds; ++i) { total_ms[i] = 0; count[i] = 0; }
+  }
+  ~KernelTimer() {
+    for (cudaEvent_t e : pool) cudaEventDestroy(e);
+  }
+};
+
 // Everything a kernel needs, passed by value.
 struct SimParams {
+  KernelTimer* timer;            // host-side instrumentation (never dereferenced on device)
   // grid
   double h, inv_h;
   double origin[3];

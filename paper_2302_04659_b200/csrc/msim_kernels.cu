@@ -1072,6 +1072,20 @@ __global__ void k_list_to_ll(const int* list, const int* n, long long* out) {
 
 inline unsigned nblk(long long n, int t = 256) { return (unsigned)((n + t - 1) / t); }
 
+// Wraps the launches of one logical kernel with optional CUDA events.
+struct Timed {
+  KernelTimer* t;
+  int id;
+  cudaStream_t s;
+  cudaEvent_t a;
+  Timed(const SimParams& P, int id_, cudaStream_t s_, int nlaunch = 1) : t(P.timer), id(id_), s(s_), a(nullptr) {
+    if (t) a = t->begin(s, nlaunch);
+  }
+  ~Timed() {
+    if (t) t->end(id, a, s);
+  }
+};
+
 }  // namespace
 
 // ---------------------------------------------------------------------------
@@ -1110,10 +1124,12 @@ void launch_convert_out(const SimParams& P, int, long long first_pid, long long 
 }
 void launch_vmax(const SimParams& P, cudaStream_t s) {
   cudaMemsetAsync(P.vmax_bits, 0, sizeof(unsigned) * P.n_env, s);
+  Timed tm(P, kKVmax, s);
   if (P.n > 0) k_vmax<<<nblk(P.n), 256, 0, s>>>(P);
 }
 void launch_plan(const SimParams& P, double dt, double cfl_h, int max_halvings, int* max_cycles,
                  int* any_err, int* cyc_sum, cudaStream_t s) {
+  Timed tm(P, kKPlan, s);
   k_plan<<<nblk(P.n_env), 256, 0, s>>>(P, dt, cfl_h, max_halvings, max_cycles, any_err, cyc_sum);
 }
 
@@ -1127,33 +1143,58 @@ void launch_cycle(const SimParams& P, int stages, cudaStream_t s) {
   }
   const unsigned persist = (unsigned)sm_count * 8;
   const int n_blocks = P.n_keys - 1;
-  if (stages & kStageClear) k_clear<<<persist, 256, 0, s>>>(P);
+  if (stages & kStageClear) {
+    Timed tm(P, kKClear, s);
+    k_clear<<<persist, 256, 0, s>>>(P);
+  }
   if (stages & kStageBin) {
-    k_bin<<<nblk(std::max<long long>(std::max<long long>(P.n, P.n_env), 1)), 256, 0, s>>>(P);
-    scan_exclusive(P.bucket_count, P.bucket_start, P.n_keys, P.active_buckets, P.n_active_buckets,
-                   P.scan_tmp, s);
-    if (P.n > 0) k_scatter<<<nblk(P.n), 256, 0, s>>>(P);
+    {
+      Timed tm(P, kKBin, s);
+      k_bin<<<nblk(std::max<long long>(std::max<long long>(P.n, P.n_env), 1)), 256, 0, s>>>(P);
+    }
+    {
+      Timed tm(P, kKBucketScan, s, 3);
+      scan_exclusive(P.bucket_count, P.bucket_start, P.n_keys, P.active_buckets, P.n_active_buckets,
+                     P.scan_tmp, s);
+    }
+    if (P.n > 0) {
+      Timed tm(P, kKScatter, s);
+      k_scatter<<<nblk(P.n), 256, 0, s>>>(P);
+    }
   }
   if (stages & kStageP2G) {
-    if (P.split)
-      k_p2g<1><<<persist, kThreads, 0, s>>>(P);
-    else
-      k_p2g<0><<<persist, kThreads, 0, s>>>(P);
+    {
+      Timed tm(P, kKP2G, s);
+      if (P.split)
+        k_p2g<1><<<persist, kThreads, 0, s>>>(P);
+      else
+        k_p2g<0><<<persist, kThreads, 0, s>>>(P);
+    }
+    Timed tm(P, kKBlockScan, s, 3);
     scan_exclusive(P.nb_flag, P.nb_scan, n_blocks, P.nb_list, P.n_nb, P.scan_tmp, s);
   }
-  if (stages & kStageGrid) k_grid<<<persist, 256, 0, s>>>(P);
-  if (stages & kStageG2P) {
-    if (P.n > 0) k_g2p<<<nblk(P.n), 256, 0, s>>>(P);
+  if (stages & kStageGrid) {
+    Timed tm(P, kKGrid, s);
+    k_grid<<<persist, 256, 0, s>>>(P);
   }
-  if (stages & kStageEnd) k_cycle_end<<<nblk(P.n_env), 256, 0, s>>>(P, P.balance_max, P.lost_threshold);
+  if ((stages & kStageG2P) && P.n > 0) {
+    Timed tm(P, kKG2P, s);
+    k_g2p<<<nblk(P.n), 256, 0, s>>>(P);
+  }
+  if (stages & kStageEnd) {
+    Timed tm(P, kKEnd, s);
+    k_cycle_end<<<nblk(P.n_env), 256, 0, s>>>(P, P.balance_max, P.lost_threshold);
+  }
 }
 
 void launch_rigid(const SimParams& P, BodyDev* bodies, const ShapeHost* shapes, double* pending,
                   int integrate, double dt_r, const double* g, int only_env, cudaStream_t s) {
+  Timed tm(P, kKRigid, s);
   k_rigid<<<nblk(P.n_env), 256, 0, s>>>(P, bodies, shapes, pending, integrate, dt_r, g[0], g[1], g[2],
                                         only_env);
 }
 void launch_stage_wrenches(const SimParams& P, double* pending, int n_bodies, cudaStream_t s) {
+  Timed tm(P, kKStage, s);
   if (n_bodies > 0) k_stage<<<nblk(6LL * n_bodies), 256, 0, s>>>(P.wrench, pending, n_bodies);
 }
 void launch_constitutive(const MatParams m, long long n, const double* F, double* tau, double* Fp,

@@ -72,6 +72,8 @@ class GpuWorld:
         n = scene.n_particles
 
         def cat(attr, shape, default):
+            if all(getattr(e, attr) is None for e in scene.envs):
+                return None  # the C ABI defaults it (v = 0, F = I, C = 0)
             parts = []
             for e in scene.envs:
                 a = getattr(e, attr)
