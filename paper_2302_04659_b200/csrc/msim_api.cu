@@ -100,8 +100,9 @@ struct msim_gpu_ctx {
   DevBuf bodies_d, shapes_host_d, shapes_d, shape_off_d, body_off_d, vol_pool_d, wrench_d, pending_d;
 
   // per env
-  DevBuf mats_d, cycles_d, dt_cycle_d, applied_d, react_d, max_pen_d, vmax_d, lost_d, err_code_d,
-      err_pid_d, balance_d, cyc_sum_d;
+  DevBuf mats_d, run_d, applied_d, react_d, max_pen_d, vmax_d, lost_d, err_code_d, err_pid_d, balance_d;
+  bool perm_valid = false;   // bucket keys/perm describe the stored positions
+  bool grid_clean = true;    // P2G accumulators are zero (fused stepping consumes them)
 
   // binning + grid
   DevBuf key_d, rank_d, bucket_count_d, bucket_start_d, active_buckets_d, n_active_d, perm_d,
@@ -161,14 +162,22 @@ SimParams params(msim_gpu_ctx* c) {
   P.r_c_particle = (float)(c->coupling.r_c_factor * d.h);
   P.r_c_grid = (float)std::max(c->coupling.r_c_factor * d.h, 0.65 * d.h);
   P.c_d = (float)c->coupling.c_d;
-  P.cycle = 0;
-  P.manual = 0;
-  P.dt_manual = (float)d.dt;
+  P.dt_full = d.dt;
+  P.cfl_h = d.cfl_factor * d.h;
+  P.max_halvings = d.max_cfl_halvings;
+  P.n_soft = 1;
+  P.integrate_rigid = 0;
+  P.clear_on_read = 1;
+  for (int a = 0; a < 3; ++a) P.rigid_g[a] = c->rigid_gravity[a];
+  P.dt_r = d.dt;
+  P.run = c->run_d.as<EnvRun>();
+  P.bodies = c->bodies_d.as<BodyDev>();
+  P.shape_src = c->shapes_host_d.as<ShapeHost>();
+  P.pending = c->pending_d.as<double>();
+  P.n_running = nullptr;
   P.cur = c->buf[c->cur];
   P.nxt = c->buf[1 - c->cur];
   P.mats = c->mats_d.as<MatParams>();
-  P.cycles = c->cycles_d.as<int>();
-  P.dt_cycle = c->dt_cycle_d.as<float>();
   P.env_off = c->env_off_d.as<long long>();
   P.shape_off = c->shape_off_d.as<int>();
   P.body_off = c->body_off_d.as<int>();
@@ -372,59 +381,80 @@ void upload_bodies(msim_gpu_ctx* c) {
   CK(cudaMemsetAsync(c->pending_d.p, 0, sizeof(double) * 6 * std::max<size_t>(bd.size(), 1), s));
   c->bodies_on_device = true;
   SimParams P = params(c);
-  launch_rigid(P, c->bodies_d.as<BodyDev>(), c->shapes_host_d.as<ShapeHost>(), c->pending_d.as<double>(), 0,
-               0.0, c->rigid_gravity, -1, s);
+  launch_rigid(P, 0, -1, s);
   CK(cudaGetLastError());
   // keep host storage alive until the copies land
   CK(cudaStreamSynchronize(s));
 }
 
-// One CFL cycle for every env with cycle < cycles[env] (or all, manual).
-void run_cycle(msim_gpu_ctx* c, int cycle, int manual, int stages) {
-  for (int e = 0; e < c->n_env && (stages & kStageClear); ++e)
-    if (c->env_grid_dirty[e]) {
-      SimParams P = params(c);
-      launch_clear_env_grid(P, e, c->stream);
-      c->env_grid_dirty[e] = 0;
-    }
+// Make the stored state ready for a P2G: bucket keys of the stored positions,
+// clean P2G accumulators, a valid max speed for the CFL plan.
+void prepare(msim_gpu_ctx* c, bool need_vmax) {
+  cudaStream_t s = c->stream;
   SimParams P = params(c);
-  P.cycle = cycle;
-  P.manual = manual;
-  int first = stages & (kStageClear | kStageBin | kStageP2G);
-  if (first) launch_cycle(P, first, c->stream);
-  if (stages & kStageP2G) {
-    c->cur ^= 1;  // P2G wrote the particles, in bucket order, to the other buffer
-    P.cur = c->buf[c->cur];
-    P.nxt = c->buf[1 - c->cur];
+  if (!c->perm_valid) {
+    launch_rebin(P, s);
+    c->perm_valid = true;
   }
-  int second = stages & (kStageGrid | kStageG2P | kStageEnd);
-  if (second) launch_cycle(P, second, c->stream);
+  if (!c->grid_clean) {
+    launch_clear(P, s);
+    for (int e = 0; e < c->n_env; ++e)
+      if (c->env_grid_dirty[e]) launch_clear_env_grid(P, e, s);
+    c->grid_clean = true;
+  }
+  for (int e = 0; e < c->n_env; ++e) c->env_grid_dirty[e] = 0;
+  if (need_vmax && !c->vmax_valid) {
+    launch_vmax(P, s);
+    c->vmax_valid = true;
+  }
   CK(cudaGetLastError());
 }
 
-int substeps(msim_gpu_ctx* c, int n_sub, int32_t* cycles_out) {
-  if (c->n == 0) return MSIM_OK;
-  for (int s = 0; s < n_sub; ++s) {
-    SimParams P = params(c);
-    if (!c->vmax_valid) {
-      launch_vmax(P, c->stream);
-      c->vmax_valid = true;
+// After a particle launch the other buffer holds the particles (bucket order).
+void swap_buffers(msim_gpu_ctx* c) { c->cur ^= 1; }
+
+// n_sub soft substeps of every env (soft_substep, mpm.hpp:397-421), or the
+// rigid/soft part of env_step when integrate_rigid (coupling.hpp:248-293).
+// Launch sequence: call_begin -> P2G -> grid, then one fused launch per cycle.
+// The host syncs once at the end (more only when some env halved its step).
+int step_call(msim_gpu_ctx* c, int n_sub, bool integrate_rigid, int n_soft, int32_t* cycles_out) {
+  cudaStream_t s = c->stream;
+  if (c->n == 0 || n_sub <= 0) return MSIM_OK;
+  prepare(c, true);
+  auto P = [&]() {
+    SimParams q = params(c);
+    q.integrate_rigid = integrate_rigid ? 1 : 0;
+    q.n_soft = n_soft;
+    q.dt_r = n_soft * c->desc.dt;
+    q.clear_on_read = 1;
+    return q;
+  };
+  launch_call_begin(P(), n_sub, kActP2G, s);
+  launch_iteration(P(), false, true, s);
+  swap_buffers(c);
+  int planned = n_sub;  // one launch per substep when no env halves its step
+  int launched = 0;
+  std::vector<EnvRun> run(c->n_env);
+  for (int guard = 0; guard < 64; ++guard) {
+    for (; launched < planned; ++launched) {
+      launch_iteration(P(), true, true, s);
+      swap_buffers(c);
     }
-    c->h_ctl[0] = 0;
-    c->h_ctl[1] = 0;
-    launch_plan(P, c->desc.dt, c->desc.cfl_factor * c->desc.h, c->desc.max_cfl_halvings, c->d_ctl,
-                c->d_ctl + 1, c->cyc_sum_d.as<int>(), c->stream);
     CK(cudaGetLastError());
-    CK(cudaStreamSynchronize(c->stream));
+    CK(cudaMemcpyAsync(run.data(), c->run_d.p, sizeof(EnvRun) * c->n_env, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
     c->timer.flush();
-    if (c->h_ctl[1]) return collect_errors(c);
-    const int maxc = c->h_ctl[0];
-    for (int cy = 0; cy < maxc; ++cy) run_cycle(c, cy, 0, kStageAll);
-    if (cycles_out && s == n_sub - 1)
-      CK(cudaMemcpyAsync(cycles_out, c->cycles_d.p, sizeof(int) * c->n_env, cudaMemcpyDeviceToHost, c->stream));
+    int more = 0;
+    for (const EnvRun& r : run)
+      if (r.substeps_left > 0) more = std::max(more, (r.cycles - r.cycle) + (r.substeps_left - 1));
+    if (more == 0) break;
+    planned += more;
   }
-  CK(cudaStreamSynchronize(c->stream));
-  c->timer.flush();
+  c->vmax_valid = true;   // the last G2P accumulated it
+  c->grid_clean = true;   // every P2G was consumed by a grid update
+  c->perm_valid = true;
+  if (cycles_out)
+    for (int e = 0; e < c->n_env; ++e) cycles_out[e] = run[e].cycles;
   return collect_errors(c);
 }
 
@@ -472,11 +502,13 @@ int msim_gpu_create(const msim_soft_desc* desc, const msim_material* materials, 
   int rc = guarded(c, [&]() -> int {
     c->device = device;
     set_device(c);
+    configure_kernels();
     CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
     c->desc = *desc;
     c->mats_h.assign(materials, materials + n_materials);
     c->n_env = n_env;
-    for (int a = 0; a < 3; ++a) c->bdims[a] = (desc->dims[a] + 3) / 4;
+    const int kb[3] = {kBX, kBY, kBZ};
+    for (int a = 0; a < 3; ++a) c->bdims[a] = (desc->dims[a] + kb[a] - 1) / kb[a];
     c->blocks_per_env = c->bdims[0] * c->bdims[1] * c->bdims[2];
     c->nodes_per_env = (long long)desc->dims[0] * desc->dims[1] * desc->dims[2];
     long long nk = (long long)n_env * c->blocks_per_env + 1;
@@ -496,8 +528,7 @@ int msim_gpu_create(const msim_soft_desc* desc, const msim_material* materials, 
       CK(b.ensure(elem * n_env));
       CK(cudaMemset(b.p, 0, elem * n_env));
     };
-    per_env(c->cycles_d, sizeof(int));
-    per_env(c->dt_cycle_d, sizeof(float));
+    per_env(c->run_d, sizeof(EnvRun));
     per_env(c->applied_d, 3 * sizeof(double));
     per_env(c->react_d, 3 * sizeof(double));
     per_env(c->max_pen_d, sizeof(unsigned));
@@ -506,7 +537,6 @@ int msim_gpu_create(const msim_soft_desc* desc, const msim_material* materials, 
     per_env(c->err_code_d, sizeof(int));
     per_env(c->err_pid_d, sizeof(int));
     per_env(c->balance_d, sizeof(double));
-    per_env(c->cyc_sum_d, sizeof(int));
     per_env(c->mean_mass_d, sizeof(double));
     CK(cudaMemset(c->err_pid_d.p, 0x7f, sizeof(int) * n_env));
     CK(c->env_off_d.ensure(sizeof(long long) * (n_env + 1)));
@@ -621,7 +651,7 @@ int msim_gpu_set_particles(msim_gpu_ctx* c, int64_t n, const int64_t* env_offset
         CK(cudaMemcpyAsync(denv, env_of.data() + o, sizeof(int) * m, cudaMemcpyHostToDevice, s));
         SimParams P = params(c);
         launch_convert_in(P, m, dx, v ? dv : nullptr, F ? dF : nullptr, C ? dC : nullptr, dm, dV,
-                          material ? dmat : nullptr, denv, o, 1, s);
+                          material ? dmat : nullptr, denv, o, s);
         CK(cudaGetLastError());
         CK(cudaStreamSynchronize(s));  // staging reused
       }
@@ -629,7 +659,9 @@ int msim_gpu_set_particles(msim_gpu_ctx* c, int64_t n, const int64_t* env_offset
     // init_buffers (mpm.hpp:137-142): lost flags, counts, clean grid
     CK(cudaMemsetAsync(c->lost_d.p, 0, sizeof(long long) * c->n_env, s));
     for (int e = 0; e < c->n_env; ++e) c->env_grid_dirty[e] = 1;
+    c->grid_clean = false;
     c->vmax_valid = false;
+    c->perm_valid = false;
     reset_errors(c);
     CK(cudaStreamSynchronize(s));
     return MSIM_OK;
@@ -655,11 +687,11 @@ int msim_gpu_write_particles(msim_gpu_ctx* c, int env, int64_t n, const double* 
     if (F) CK(cudaMemcpyAsync(dF, F, sizeof(double) * 9 * ne, cudaMemcpyHostToDevice, s));
     if (C) CK(cudaMemcpyAsync(dC, C, sizeof(double) * 9 * ne, cudaMemcpyHostToDevice, s));
     SimParams P = params(c);
-    launch_overwrite(P, env, first, ne, x ? dx : nullptr, v ? dv : nullptr, F ? dF : nullptr,
-                     C ? dC : nullptr, s);
+    launch_overwrite(P, first, ne, x ? dx : nullptr, v ? dv : nullptr, F ? dF : nullptr, C ? dC : nullptr, s);
     CK(cudaGetLastError());
     CK(cudaStreamSynchronize(s));
     c->vmax_valid = false;
+    c->perm_valid = false;
     return MSIM_OK;
   });
 }
@@ -735,8 +767,7 @@ int msim_gpu_sync_bodies(msim_gpu_ctx* c, int env, const msim_body* bodies, int 
     if (n_bodies)
       CK(cudaMemcpyAsync(c->bodies_d.as<BodyDev>() + off, bd.data(), sizeof(BodyDev) * n_bodies, cudaMemcpyHostToDevice, c->stream));
     SimParams P = params(c);
-    launch_rigid(P, c->bodies_d.as<BodyDev>(), c->shapes_host_d.as<ShapeHost>(), c->pending_d.as<double>(), 0,
-                 0.0, c->rigid_gravity, env, c->stream);
+    launch_rigid(P, 0, env, c->stream);
     CK(cudaGetLastError());
     CK(cudaStreamSynchronize(c->stream));
     return MSIM_OK;
@@ -776,37 +807,52 @@ int msim_gpu_soft_substep(msim_gpu_ctx* c, int n_substeps, int32_t* cycles_out) 
   return guarded(c, [&]() -> int {
     set_device(c);
     reset_errors(c);
-    return substeps(c, n_substeps, cycles_out);
+    return step_call(c, n_substeps, false, 1, cycles_out);
   });
 }
 
-static int manual_phase(msim_gpu_ctx* c, int stages) {
+// Phase API (p2g / grid_update / g2p_advect as separate calls): one launch
+// per phase with every env active, dt_c = dt, momentum and force kept apart.
+static int manual_phase(msim_gpu_ctx* c, int which) {
   return guarded(c, [&]() -> int {
     set_device(c);
     reset_errors(c);
     if (c->n == 0) return MSIM_OK;
-    run_cycle(c, 0, 1, stages);
-    CK(cudaStreamSynchronize(c->stream));
-    c->vmax_valid = false;
+    cudaStream_t s = c->stream;
+    if (which == 0) {  // p2g
+      prepare(c, false);
+      SimParams P = params(c);
+      launch_set_action(P, kActP2G, (float)c->desc.dt, s);
+      P.clear_on_read = 0;
+      launch_particles(P, s);
+      launch_iteration_end(P, s);
+      swap_buffers(c);
+      c->grid_clean = false;
+      c->perm_valid = true;
+    } else if (which == 1) {  // grid_update
+      SimParams P = params(c);
+      launch_set_action(P, kActP2G, (float)c->desc.dt, s);
+      P.clear_on_read = 0;
+      launch_grid(P, s);
+    } else {  // g2p_advect
+      if (!c->perm_valid) launch_rebin(params(c), s), c->perm_valid = true;
+      SimParams P = params(c);
+      launch_set_action(P, kActG2P, (float)c->desc.dt, s);
+      launch_particles(P, s);
+      swap_buffers(c);
+      c->vmax_valid = true;
+      c->perm_valid = true;
+    }
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(s));
+    c->timer.flush();
     return collect_errors(c);
   });
 }
 
-int msim_gpu_p2g(msim_gpu_ctx* c) {
-  int saved = c->split_req;
-  c->split_req = 1;  // phase API keeps momentum and force apart like MpmGrid
-  int rc = manual_phase(c, kStageClear | kStageBin | kStageP2G | kStageEnd);
-  c->split_req = saved;
-  return rc;
-}
-int msim_gpu_grid_update(msim_gpu_ctx* c) {
-  int saved = c->split_req;
-  c->split_req = 1;
-  int rc = manual_phase(c, kStageGrid);
-  c->split_req = saved;
-  return rc;
-}
-int msim_gpu_g2p(msim_gpu_ctx* c) { return manual_phase(c, kStageG2P); }
+int msim_gpu_p2g(msim_gpu_ctx* c) { return manual_phase(c, 0); }
+int msim_gpu_grid_update(msim_gpu_ctx* c) { return manual_phase(c, 1); }
+int msim_gpu_g2p(msim_gpu_ctx* c) { return manual_phase(c, 2); }
 
 int msim_gpu_env_step(msim_gpu_ctx* c, int n_rigid, int n_soft, msim_step_report* report) {
   return guarded(c, [&]() -> int {
@@ -816,25 +862,12 @@ int msim_gpu_env_step(msim_gpu_ctx* c, int n_rigid, int n_soft, msim_step_report
     reset_errors(c);
     CK(cudaMemsetAsync(c->max_pen_d.p, 0, sizeof(unsigned) * c->n_env, s));
     CK(cudaMemsetAsync(c->balance_d.p, 0, sizeof(double) * c->n_env, s));
-    CK(cudaMemsetAsync(c->cyc_sum_d.p, 0, sizeof(int) * c->n_env, s));
-    const double dt_r = n_soft * c->desc.dt;
-    int rc = MSIM_OK;
-    int done_rigid = 0;
-    for (int r = 0; r < n_rigid && rc == MSIM_OK; ++r) {
-      SimParams P = params(c);
-      if (c->n_bodies > 0)
-        launch_rigid(P, c->bodies_d.as<BodyDev>(), c->shapes_host_d.as<ShapeHost>(), c->pending_d.as<double>(),
-                     1, dt_r, c->rigid_gravity, -1, s);
-      CK(cudaGetLastError());
-      rc = substeps(c, n_soft, nullptr);
-      if (c->n_bodies > 0) launch_stage_wrenches(P, c->pending_d.as<double>(), c->n_bodies, s);
-      ++done_rigid;
-    }
+    const int rc = step_call(c, n_rigid * n_soft, c->n_bodies > 0, n_soft, nullptr);
     c->time += n_rigid * n_soft * c->desc.dt;
     if (report) {
       msim_step_report agg{};
-      agg.rigid_steps = done_rigid;
-      agg.soft_substeps = done_rigid * n_soft;
+      agg.rigid_steps = n_rigid;
+      agg.soft_substeps = n_rigid * n_soft;
       for (int e = 0; e < c->n_env; ++e) {
         msim_step_report r{};
         msim_gpu_read_report(c, e, &r);
@@ -845,7 +878,6 @@ int msim_gpu_env_step(msim_gpu_ctx* c, int n_rigid, int n_soft, msim_step_report
       }
       *report = agg;
     }
-    CK(cudaStreamSynchronize(s));
     return rc;
   });
 }
@@ -872,7 +904,7 @@ int msim_gpu_read_particles(msim_gpu_ctx* c, int env, double* x, double* v, doub
     double* dC = dF + 9 * ne;
     uint8_t* dl = reinterpret_cast<uint8_t*>(dC + 9 * ne);
     SimParams P = params(c);
-    launch_convert_out(P, env, first, ne, x ? dx : nullptr, v ? dv : nullptr, F ? dF : nullptr,
+    launch_convert_out(P, first, ne, x ? dx : nullptr, v ? dv : nullptr, F ? dF : nullptr,
                        C ? dC : nullptr, lost ? dl : nullptr, s);
     CK(cudaGetLastError());
     if (x) CK(cudaMemcpyAsync(x, dx, sizeof(double) * 3 * ne, cudaMemcpyDeviceToHost, s));
@@ -925,6 +957,7 @@ int msim_gpu_write_grid_velocity(msim_gpu_ctx* c, int env, const double* velocit
     CK(cudaGetLastError());
     CK(cudaStreamSynchronize(s));
     c->env_grid_dirty[env] = 1;  // the next clear must wipe the whole env grid
+    c->grid_clean = false;
     return MSIM_OK;
   });
 }
@@ -953,8 +986,8 @@ int msim_gpu_read_binning(msim_gpu_ctx* c, int env, int32_t* base, int32_t* cell
     CK(tmp.ensure(sizeof(int) * scan_tmp_ints((int)std::max<long long>(nbins + 1, nn + 1))));
     SimParams P = params(c);
     const int* b = c->base_dbg_d.as<int>() + 3 * first;
-    launch_binning_out(P, env, first, ne, b, cc.as<int>(), cs.as<int>(), cp.as<int>(), nf.as<int>(),
-                       ns.as<int>(), nl.as<int>(), nlc.as<int>(), an.as<long long>(), tmp.as<int>(), s);
+    launch_binning_out(P, ne, b, cc.as<int>(), cs.as<int>(), cp.as<int>(), nf.as<int>(), ns.as<int>(),
+                       nl.as<int>(), nlc.as<int>(), an.as<long long>(), tmp.as<int>(), s);
     CK(cudaGetLastError());
     int total = 0, nact = 0;
     CK(cudaMemcpyAsync(&total, cs.as<int>() + nbins, sizeof(int), cudaMemcpyDeviceToHost, s));
@@ -1024,14 +1057,16 @@ int msim_gpu_read_report(msim_gpu_ctx* c, int env, msim_step_report* r) {
     CK(cudaMemcpyAsync(&pen, c->max_pen_d.as<unsigned>() + env, sizeof pen, cudaMemcpyDeviceToHost, s));
     CK(cudaMemcpyAsync(&bal, c->balance_d.as<double>() + env, sizeof bal, cudaMemcpyDeviceToHost, s));
     CK(cudaMemcpyAsync(&lost, c->lost_d.as<long long>() + env, sizeof lost, cudaMemcpyDeviceToHost, s));
-    CK(cudaMemcpyAsync(&cyc, c->cyc_sum_d.as<int>() + env, sizeof cyc, cudaMemcpyDeviceToHost, s));
+    EnvRun run{};
+    CK(cudaMemcpyAsync(&run, c->run_d.as<EnvRun>() + env, sizeof run, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
     float penf;
     std::memcpy(&penf, &pen, sizeof penf);
     r->max_penetration = penf;
     r->max_force_balance_error = bal;
     r->lost_particles = lost;
-    r->cfl_cycles = cyc;
+    r->cfl_cycles = run.cyc_sum;
+    (void)cyc;
     return MSIM_OK;
   });
 }
@@ -1114,8 +1149,7 @@ int msim_gpu_sync_all_bodies(msim_gpu_ctx* c, const msim_body* bodies, int n_tot
     // the caller like sync_rigid_to_soft copies whole bodies.
     CK(cudaMemcpyAsync(c->bodies_d.p, bodies, sizeof(msim_body) * n_total, cudaMemcpyHostToDevice, c->stream));
     SimParams P = params(c);
-    launch_rigid(P, c->bodies_d.as<BodyDev>(), c->shapes_host_d.as<ShapeHost>(), c->pending_d.as<double>(), 0,
-                 0.0, c->rigid_gravity, -1, c->stream);
+    launch_rigid(P, 0, -1, c->stream);
     CK(cudaGetLastError());
     return MSIM_OK;
   });

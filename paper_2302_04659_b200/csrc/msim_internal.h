@@ -15,6 +15,34 @@ namespace msim_impl {
 
 constexpr int kMaxBodiesPerEnv = 32;  // wrench slots reduced in shared memory
 
+// Bucket = node block of kBX x kBY x kBZ base cells. Particles are grouped
+// by the bucket of their base cell; one CTA processes one bucket with a
+// G2P tile of (kB+2) nodes and a P2G tile of (kB+4) nodes per axis.
+constexpr int kBX = 4, kBY = 4, kBZ = 2;
+
+// Per-env action of one batched cycle launch.
+enum : int {
+  kActIdle = 0,     // env finished (or errored): particles are only carried along
+  kActP2G = 1,      // first P2G of a call (from stored v, C)
+  kActFused = 2,    // G2P of this cycle + P2G of the next cycle in one pass
+  kActG2P = 3,      // last G2P of a call (stores v, C)
+};
+
+// Device-side stepping state of one environment (independent worlds advance
+// their own substeps/cycles; CFL halving is decided per env, mpm.hpp:400-409).
+struct EnvRun {
+  int substeps_left;   // substeps of this call not yet completed (incl. current)
+  int cycle;           // cycle index within the current substep
+  int cycles;          // 2^halvings of the current substep
+  int soft_in_rigid;   // index of the current substep within its rigid step
+  int action;          // kAct* for the next launch
+  int next_new_sub;    // the P2G of this launch starts a new substep
+  int next_new_rigid;  // ... and a new rigid step
+  float dt_c;          // dt / cycles (current cycle)
+  int cyc_sum;         // report: cycles executed
+  int _pad[3];
+};
+
 // Internal error codes latched per environment (first one wins); mapped to
 // MSIM_ERR_INVALID / MSIM_ERR_DIVERGED with the reference's messages.
 enum : int {
@@ -146,16 +174,24 @@ struct SimParams {
   int split;                 // keep momentum and force separately
   int grid_mode;             // coupling mode grid
   float r_c_particle, r_c_grid, c_d;
-  int cycle;                 // current CFL cycle index
-  int manual;                // phase API: all envs run, dt from dt_manual
-  float dt_manual;
+  double dt_full;            // SoftState::dt
+  double cfl_h;              // cfl_factor * h
+  int max_halvings;
+  int n_soft;                // substeps per rigid step
+  int integrate_rigid;       // env_step: rigid step at rigid boundaries
+  int clear_on_read;         // grid update zeroes consumed P2G accumulators
+  double rigid_g[3];
+  double dt_r;               // n_soft * dt
+  EnvRun* run;
+  BodyDev* bodies;
+  const ShapeHost* shape_src;
+  double* pending;           // staged wrenches (pending_wrenches)
+  int* n_running;            // envs with substeps left after the last iteration
 
   Particles cur, nxt;
   const msim_dev::MatParams* mats;
 
   // per env
-  const int* cycles;
-  const float* dt_cycle;
   const long long* env_off;      // n_env+1
   const int* shape_off;          // n_env+1
   const int* body_off;           // n_env+1
@@ -195,47 +231,49 @@ struct SimParams {
   double lost_threshold;
 };
 
-// kernel launchers (msim_kernels.cu)
+// ---- utility kernels (msim_kernels.cu)
 void launch_convert_in(const SimParams& P, long long n, const double* x, const double* v,
                        const double* F, const double* C, const double* mass, const double* vol0,
-                       const int32_t* mat, const int* env_of, long long first_pid, int write_all,
-                       cudaStream_t s);
-void launch_overwrite(const SimParams& P, int env, long long first_pid, long long n,
-                      const double* x, const double* v, const double* F, const double* C,
-                      cudaStream_t s);
-void launch_convert_out(const SimParams& P, int env, long long first_pid, long long n, double* x,
-                        double* v, double* F, double* C, uint8_t* lost, cudaStream_t s);
+                       const int32_t* mat, const int* env_of, long long first_pid, cudaStream_t s);
+void launch_overwrite(const SimParams& P, long long first_pid, long long n, const double* x,
+                      const double* v, const double* F, const double* C, cudaStream_t s);
+void launch_convert_out(const SimParams& P, long long first_pid, long long n, double* x, double* v,
+                        double* F, double* C, uint8_t* lost, cudaStream_t s);
 void launch_vmax(const SimParams& P, cudaStream_t s);
-void launch_plan(const SimParams& P, double dt, double cfl_h, int max_halvings, int* max_cycles,
-                 int* any_err, int* cyc_sum, cudaStream_t s);
-void launch_cycle(const SimParams& P, int stage_mask, cudaStream_t s);
-void launch_rigid(const SimParams& P, BodyDev* bodies, const ShapeHost* shapes, double* pending,
-                  int integrate, double dt_r, const double* rigid_gravity3, int only_env,
-                  cudaStream_t s);
-void launch_stage_wrenches(const SimParams& P, double* pending, int n_bodies, cudaStream_t s);
+void launch_rigid(const SimParams& P, int integrate, int only_env, cudaStream_t s);
+void launch_stage_wrenches(const SimParams& P, int n_bodies, cudaStream_t s);
 void launch_constitutive(const msim_dev::MatParams m, long long n, const double* F, double* tau,
                          double* Fp, int* bad, cudaStream_t s);
 void launch_grid_out(const SimParams& P, int env, double* mass, double* mom, double* force,
                      double* vel, cudaStream_t s);
 void launch_grid_vel_in(const SimParams& P, int env, const double* vel, cudaStream_t s);
 void launch_clear_env_grid(const SimParams& P, int env, cudaStream_t s);
-void launch_binning_out(const SimParams& P, int env, long long first_pid, long long n_env_p,
-                        const int* base, int* cell_count, int* cell_start, int* cell_particles,
-                        int* node_flag, int* node_scan, int* node_list, int* n_list,
-                        long long* active_nodes, int* tmp, cudaStream_t s);
-void scan_exclusive(const int* in, int* out, int n, int* compact_list, int* n_compact, int* tmp,
+void launch_binning_out(const SimParams& P, long long n_env_p, const int* base, int* cell_count,
+                        int* cell_start, int* cell_particles, int* node_flag, int* node_scan,
+                        int* node_list, int* n_list, long long* active_nodes, int* tmp, cudaStream_t s);
+void scan_exclusive(int* in, int* out, int n, int* compact_list, int* n_compact, int* tmp,
                     cudaStream_t s);
 size_t scan_tmp_ints(int n);
 
-// cycle stage bits for launch_cycle
-enum : int {
-  kStageClear = 1,
-  kStageBin = 2,
-  kStageP2G = 4,
-  kStageGrid = 8,
-  kStageG2P = 16,
-  kStageEnd = 32,
-  kStageAll = 63,
-};
+// ---- hot path (msim_substep.cu)
+// Bucket keys of the stored positions (after uploads / external writes).
+void launch_rebin(const SimParams& P, cudaStream_t s);
+// Zero the grid nodes touched by the last P2G (manual phases) and reset flags.
+void launch_clear(const SimParams& P, cudaStream_t s);
+// Per-env actions for the phase API (all envs, dt_c = dt).
+void launch_set_action(const SimParams& P, int action, float dt, cudaStream_t s);
+// Start of a stepping call: substep counters, rigid step 0, CFL plan of substep 0.
+void launch_call_begin(const SimParams& P, int n_substeps, int first_action, cudaStream_t s);
+// One batched cycle: [iter_begin] -> particle kernel -> bucket scan -> perm ->
+// node-block scan -> [iter_end] -> grid update.
+void launch_iteration(const SimParams& P, bool bookkeeping, bool grid_update, cudaStream_t s);
+// The particle kernel + re-sort only (phase API).
+void launch_particles(const SimParams& P, cudaStream_t s);
+// Grid update only (phase API).
+void launch_grid(const SimParams& P, cudaStream_t s);
+// Per-env end-of-launch bookkeeping only (phase API p2g: lost check, balance).
+void launch_iteration_end(const SimParams& P, cudaStream_t s);
+// Dynamic shared memory opt-in for the particle kernel (call once per device).
+void configure_kernels();
 
 }  // namespace msim_impl

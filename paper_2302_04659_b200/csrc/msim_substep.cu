@@ -1,0 +1,935 @@
+// Hot path of the B200 MLS-MPM substep (sm_100a).
+//
+// The reference runs each CFL cycle as clear -> penalty hook -> p2g ->
+// grid hook -> grid_update -> g2p_advect (mpm.hpp:410-418). Here one
+// batched launch sequence per cycle does, for every environment at once:
+//
+//   k_particles  one CTA per bucket (node block of kBX x kBY x kBZ base
+//                cells). Gathers the bucket's particles (perm), runs G2P of
+//                this cycle against a shared-memory velocity tile
+//                (mpm.hpp:346-379) with the von Mises return map
+//                (mpm.hpp:166-181), and in the same pass the P2G of the next
+//                cycle: penalty hook (coupling.hpp:151-172), Kirchhoff stress
+//                from the SAME principal frame (mpm.hpp:152-161), and a
+//                warp-cooperative scatter of mass/momentum/force into a
+//                shared-memory node tile (cell-sorted, 3 particles x 9 stencil
+//                rows per warp, no per-particle atomics), flushed with
+//                vector REDs. Particles are written back in bucket order with
+//                their next bucket key (the per-cycle radix-style re-sort).
+//   scans        bucket offsets + active list, node-block list
+//   k_iter_end   per env: substep/cycle counters, CFL plan (mpm.hpp:400-409),
+//                lost-fraction check, force-balance diagnostic
+//   k_grid       per touched node block: p/m + dt (g + f/m), grid-mode penalty
+//                (coupling.hpp:186-214), boundary bands (mpm.hpp:315-342);
+//                consumes (zeroes) the P2G accumulators
+//
+// Because G2P(c) and P2G(c+1) share one pass, each particle-substep reads and
+// writes x, F-I, mass, V0, meta, pid once; v and C stay in registers except
+// at the first/last cycle of a call.
+#include <cuda_runtime.h>
+
+#include <cfloat>
+
+#include "msim_common.cuh"
+
+using namespace msim_dev;
+
+namespace msim_impl {
+namespace {
+
+constexpr int kT = 128;    // threads per CTA (particle kernel), 4 CTAs per SM
+constexpr int kCap = 256;  // particles staged per round
+constexpr int GX = kBX + 2, GY = kBY + 2, GZ = kBZ + 2, GN = GX * GY * GZ;  // G2P velocity tile
+constexpr int PX = kBX + 4, PY = kBY + 4, PZ = kBZ + 4, PN = PX * PY * PZ;  // P2G node tile (origin o-1)
+constexpr int CX = kBX + 2, CY = kBY + 2, CZ = kBZ + 2, CN = CX * CY * CZ;  // P2G base cells (origin o-1)
+constexpr int kNCH = 7;    // m, momentum, force
+constexpr int kPay = 32;   // staged P2G payload floats per particle (8 x float4)
+constexpr int kWs = kMaxBodiesPerEnv * 6 + 3;
+
+struct Smem {
+  float4 gtile[GN];
+  int itile[kNCH][PN];     // fixed-point node accumulators (native int shared atomics)
+  float pay[kCap][kPay];
+  int cnt[CN];
+  int off[CN];
+  int clist[CN];
+  int order[kCap];
+  double wsum[kWs];
+  int n_clist;
+  unsigned penmax;
+  unsigned maxb[3];
+  int scan_ws[8];
+  int scan_tot;
+};
+
+__device__ __forceinline__ int warp_incl_scan(int v) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    int t = __shfl_up_sync(0xffffffffu, v, o);
+    if (lane >= o) v += t;
+  }
+  return v;
+}
+
+// Exclusive scan of one int per thread over the block (kT threads).
+__device__ __forceinline__ int block_excl_scan(Smem& S, int v, int* total) {
+  constexpr int NW = kT / 32;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  int inc = warp_incl_scan(v);
+  if (lane == 31) S.scan_ws[wid] = inc;
+  __syncthreads();
+  if (wid == 0) {
+    int s = lane < NW ? S.scan_ws[lane] : 0;
+    int si = warp_incl_scan(s);
+    if (lane < NW) S.scan_ws[lane] = si - s;
+    if (lane == NW - 1) S.scan_tot = si;
+  }
+  __syncthreads();
+  int r = inc - v + S.scan_ws[wid];
+  *total = S.scan_tot;
+  __syncthreads();
+  return r;
+}
+
+__device__ __forceinline__ float wsel(float a, float b, float c, int i) { return i == 0 ? a : (i == 1 ? b : c); }
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Global-memory scatter of one particle (fallback when its stencil leaves the
+// bucket's P2G tile, e.g. a particle faster than the CFL bound assumed).
+__device__ void scatter_global(const SimParams& P, int env, const int* b, const float* w9, float m, f3 bp,
+                               const float* Ap, f3 bf, const float* Af) {
+  for (int dk = 0; dk < 3; ++dk)
+    for (int dj = 0; dj < 3; ++dj)
+      for (int di = 0; di < 3; ++di) {
+        float w = w9[di] * w9[3 + dj] * w9[6 + dk];
+        f3 pq = {bp.x + Ap[0] * di + Ap[1] * dj + Ap[2] * dk, bp.y + Ap[3] * di + Ap[4] * dj + Ap[5] * dk,
+                 bp.z + Ap[6] * di + Ap[7] * dj + Ap[8] * dk};
+        f3 fq = {bf.x + Af[0] * di + Af[1] * dj + Af[2] * dk, bf.y + Af[3] * di + Af[4] * dj + Af[5] * dk,
+                 bf.z + Af[6] * di + Af[7] * dj + Af[8] * dk};
+        const int gx = b[0] + di, gy = b[1] + dj, gz = b[2] + dk;
+        const long long gi = env * P.nodes_per_env + ((long long)gz * P.dims[1] + gy) * P.dims[0] + gx;
+        atomicAdd(&P.gPM[gi], make_float4(w * pq.x, w * pq.y, w * pq.z, w * m));
+        atomicAdd(&P.gF[gi], make_float4(w * fq.x, w * fq.y, w * fq.z, 0.0f));
+        P.nb_flag[env * P.blocks_per_env + ((gz / kBZ) * P.bdims[1] + gy / kBY) * P.bdims[0] + gx / kBX] = 1;
+      }
+}
+
+__global__ void __launch_bounds__(kT, 4) k_particles(SimParams P) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  Smem& S = *reinterpret_cast<Smem*>(smem_raw);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const unsigned FULL = 0xffffffffu;
+  const int nitems = *P.n_active_buckets;
+
+  for (int t = tid; t < kNCH * PN; t += kT) (&S.itile[0][0])[t] = 0;
+  for (int t = tid; t < CN; t += kT) S.cnt[t] = 0;
+
+  for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
+    const int key = P.active_buckets[item];
+    const int s = P.bucket_start[key], e = P.bucket_start[key + 1];
+    const bool lostb = key == P.n_keys - 1;
+    const int benv = lostb ? 0 : key / P.blocks_per_env;
+    const int act = lostb ? kActIdle : P.run[benv].action;
+    const bool do_g2p = act == kActFused || act == kActG2P;
+    const bool do_p2g = act == kActP2G || act == kActFused;
+    const int lb = key - benv * P.blocks_per_env;
+    const int ox = kBX * (lb % P.bdims[0]), oy = kBY * ((lb / P.bdims[0]) % P.bdims[1]),
+              oz = kBZ * (lb / (P.bdims[0] * P.bdims[1]));
+    const float dt = do_g2p ? P.run[benv].dt_c : 0.0f;
+    const int s0 = lostb ? 0 : P.shape_off[benv], s1 = lostb ? 0 : P.shape_off[benv + 1];
+    const bool penalty = do_p2g && !P.grid_mode && s1 > s0;
+
+    __syncthreads();  // smem reuse across items
+    if (do_g2p) {
+      for (int t = tid; t < GN; t += kT) {
+        const int lx = t % GX, ly = (t / GX) % GY, lz = t / (GX * GY);
+        const int gx = ox + lx, gy = oy + ly, gz = oz + lz;
+        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (gx < P.dims[0] && gy < P.dims[1] && gz < P.dims[2])
+          v = P.gV[benv * P.nodes_per_env + ((long long)gz * P.dims[1] + gy) * P.dims[0] + gx];
+        S.gtile[t] = v;
+      }
+    }
+    if (penalty)
+      for (int t = tid; t < kWs; t += kT) S.wsum[t] = 0.0;
+    if (tid == 0) S.penmax = 0u;
+    __syncthreads();
+
+    for (int r0 = s; r0 < e; r0 += kCap) {
+      const int rn = min(kCap, e - r0);
+      const int trips = (rn + kT - 1) / kT;
+      if (tid < 3) S.maxb[tid] = 0u;
+      float mx_m = 0.f, mx_p = 0.f, mx_f = 0.f;
+      // ---------------- per-particle phase (CTA-uniform trip count for warp collectives)
+      for (int trip = 0; trip < trips; ++trip) {
+        const int t = trip * kT + tid;
+        const bool valid = t < rn;
+        const int j = r0 + t;
+        const int i = valid ? P.perm[j] : 0;
+        unsigned meta = valid ? P.cur.meta[i] : (1u << kLostBit);
+        const int penv = (meta >> 8) & kEnvMask;
+        const bool was_lost = meta >> kLostBit;
+        const int pact = lostb ? (valid ? P.run[penv].action : kActIdle) : act;
+        f3 x = {0.f, 0.f, 0.f}, v = {0.f, 0.f, 0.f};
+        float G[9], Cm[9];
+        float m = 0.f, V0 = 0.f;
+        int pid = 0;
+        if (valid) {
+          x = load3(P.cur.x, i);
+#pragma unroll
+          for (int k = 0; k < 9; ++k) G[k] = P.cur.G[k][i];
+          m = P.cur.mass[i];
+          V0 = P.cur.vol0[i];
+          pid = P.cur.pid[i];
+        } else {
+#pragma unroll
+          for (int k = 0; k < 9; ++k) G[k] = 0.f;
+        }
+        const bool read_vc = valid && (lostb || !do_g2p);
+        if (read_vc) {
+          v = load3(P.cur.v, i);
+#pragma unroll
+          for (int k = 0; k < 9; ++k) Cm[k] = P.cur.C[k][i];
+        } else {
+#pragma unroll
+          for (int k = 0; k < 9; ++k) Cm[k] = 0.f;
+        }
+        bool write_vc = valid && (lostb || act != kActFused);
+        const bool live = valid && !lostb && !was_lost && act != kActIdle;
+        float speed = -1.0f;
+        float U[9], eps[3];
+        const MatParams mp = P.mats[meta & 0xFFu];
+
+        // ---------------- G2P of this cycle (mpm.hpp:346-379)
+        if (live && do_g2p) {
+          int b[3];
+          float fx[3];
+          base_of(P, x.x, x.y, x.z, b, fx);
+          const int lx = b[0] - ox, ly = b[1] - oy, lz = b[2] - oz;
+          float wx[3], wy[3], wz[3];
+          bspline_w(fx[0], wx);
+          bspline_w(fx[1], wy);
+          bspline_w(fx[2], wz);
+          f3 vs = {0.f, 0.f, 0.f}, Sx = {0.f, 0.f, 0.f}, Sy = {0.f, 0.f, 0.f}, Sz = {0.f, 0.f, 0.f};
+#pragma unroll
+          for (int dk = 0; dk < 3; ++dk)
+#pragma unroll
+            for (int dj = 0; dj < 3; ++dj) {
+              const int tb = ((lz + dk) * GY + (ly + dj)) * GX + lx;
+              const float4 v0 = S.gtile[tb], v1 = S.gtile[tb + 1], v2 = S.gtile[tb + 2];
+              const f3 a = {wx[0] * v0.x + wx[1] * v1.x + wx[2] * v2.x, wx[0] * v0.y + wx[1] * v1.y + wx[2] * v2.y,
+                            wx[0] * v0.z + wx[1] * v1.z + wx[2] * v2.z};
+              const f3 ax = {wx[1] * v1.x + 2.f * wx[2] * v2.x, wx[1] * v1.y + 2.f * wx[2] * v2.y,
+                             wx[1] * v1.z + 2.f * wx[2] * v2.z};
+              const float wr = wy[dj] * wz[dk];
+              vs = vs + wr * a;
+              Sx = Sx + wr * ax;
+              if (dj) Sy = Sy + (wr * dj) * a;
+              if (dk) Sz = Sz + (wr * dk) * a;
+            }
+          // C = (4/h) sum w v (off - fx)^T = (4/h)(S - v fx^T)  (partition of unity)
+          const float k4h = 4.0f / P.h_f;
+          Cm[0] = k4h * (Sx.x - vs.x * fx[0]); Cm[1] = k4h * (Sy.x - vs.x * fx[1]); Cm[2] = k4h * (Sz.x - vs.x * fx[2]);
+          Cm[3] = k4h * (Sx.y - vs.y * fx[0]); Cm[4] = k4h * (Sy.y - vs.y * fx[1]); Cm[5] = k4h * (Sz.y - vs.y * fx[2]);
+          Cm[6] = k4h * (Sx.z - vs.z * fx[0]); Cm[7] = k4h * (Sy.z - vs.z * fx[1]); Cm[8] = k4h * (Sz.z - vs.z * fx[2]);
+          v = vs;
+          x = x + dt * vs;
+          if (dt != 0.0f) {
+            float Gn[9];
+#pragma unroll
+            for (int r = 0; r < 3; ++r)
+#pragma unroll
+              for (int c = 0; c < 3; ++c)
+                Gn[r * 3 + c] = G[r * 3 + c] + dt * (Cm[r * 3 + c] + Cm[r * 3 + 0] * G[0 * 3 + c] +
+                                                     Cm[r * 3 + 1] * G[1 * 3 + c] + Cm[r * 3 + 2] * G[2 * 3 + c]);
+            if (!(det_I_plus(Gn) > 0.0f)) set_error(P, penv, kErrDetReturn, pid);
+            hencky_frame(Gn, U, eps);
+            von_mises_project(Gn, U, eps, mp);
+#pragma unroll
+            for (int k = 0; k < 9; ++k) G[k] = Gn[k];
+          } else if (do_p2g) {
+            hencky_frame(G, U, eps);
+          }
+          bool bad = false;
+#pragma unroll
+          for (int k = 0; k < 9; ++k) bad |= !isfinite(G[k]);
+          bad |= !isfinite(x.x) || !isfinite(x.y) || !isfinite(x.z) || !isfinite(v.x) || !isfinite(v.y) ||
+                 !isfinite(v.z);
+          if (bad) set_error(P, penv, kErrNan, pid);
+          speed = norm(v);
+          if (!(speed >= 0.0f)) speed = FLT_MAX;
+        } else if (live && do_p2g) {
+          if (!(det_I_plus(G) > 0.0f)) set_error(P, penv, kErrDetStress, pid);
+          hencky_frame(G, U, eps);
+        }
+
+        // ---------------- binning of the (new) position + P2G payload of the next cycle
+        int key_new = P.n_keys - 1;
+        bool staged = false;
+        int cell = 0;
+        int b2[3] = {-10, -10, -10};
+        float fx2[3] = {0.f, 0.f, 0.f};
+        f3 fext = {0.f, 0.f, 0.f};
+        const bool p2g_here = valid && !was_lost && (lostb ? (pact == kActP2G || pact == kActFused) : do_p2g);
+        if (valid && !was_lost) {
+          base_of(P, x.x, x.y, x.z, b2, fx2);
+          if (base_in_range(P, b2)) {
+            if (!lostb || pact == kActIdle || pact == kActG2P) key_new = bucket_of(P, penv, b2);
+          } else if (p2g_here) {
+            // leaves the domain now: reaction-only penalty, freeze, count (mpm.hpp:239-245)
+            if (!P.grid_mode && P.shape_off[penv + 1] > P.shape_off[penv]) penalty_reaction_only(P, penv, x, v);
+            meta |= 1u << kLostBit;
+            v = {0.f, 0.f, 0.f};
+            write_vc = true;
+            atomicAdd((unsigned long long*)&P.lost_count[penv], 1ull);
+            b2[0] = b2[1] = b2[2] = -10;
+          }
+        }
+        const bool now_lost = meta >> kLostBit;
+        const bool scatter_me = p2g_here && !lostb && !now_lost;
+        if (P.base_dbg && valid && (p2g_here || (lostb && was_lost && (pact == kActP2G || pact == kActFused)))) {
+          P.base_dbg[3 * pid + 0] = now_lost ? -10 : b2[0];
+          P.base_dbg[3 * pid + 1] = now_lost ? -10 : b2[1];
+          P.base_dbg[3 * pid + 2] = now_lost ? -10 : b2[2];
+        }
+
+        // penalty hook: warp-cooperative per shape (coupling.hpp:151-172)
+        if (penalty) {
+          for (int sidx = s0; sidx < s1; ++sidx) {
+            const ShapeDev& sh = P.shapes[sidx];
+            f3 f = {0.f, 0.f, 0.f};
+            float pen = 0.f;
+            const bool hit = scatter_me && penalty_force(sh, P.vol_pool, x, v, P.r_c_particle, P.c_d, f, pen);
+            if (!hit) f = {0.f, 0.f, 0.f};
+            fext = fext + f;
+            if (__any_sync(FULL, hit)) {
+              const f3 com = {sh.com[0], sh.com[1], sh.com[2]};
+              const f3 tq = hit ? cross(x - com, f3{-f.x, -f.y, -f.z}) : f3{0.f, 0.f, 0.f};
+              float r6[6] = {-f.x, -f.y, -f.z, tq.x, tq.y, tq.z};
+#pragma unroll
+              for (int k = 0; k < 6; ++k) r6[k] = warp_sum(r6[k]);
+              unsigned pb = hit ? __float_as_uint(pen) : 0u;
+#pragma unroll
+              for (int o = 16; o > 0; o >>= 1) pb = max(pb, __shfl_xor_sync(FULL, pb, o));
+              if (lane == 0) {
+                double* ws = S.wsum + 6 * min(sh.body, kMaxBodiesPerEnv - 1);
+#pragma unroll
+                for (int k = 0; k < 6; ++k) atomicAdd(ws + k, (double)r6[k]);
+#pragma unroll
+                for (int k = 0; k < 3; ++k) atomicAdd(S.wsum + 6 * kMaxBodiesPerEnv + k, -(double)r6[k]);
+                atomicMax(&S.penmax, pb);
+              }
+            }
+          }
+        }
+
+        if (scatter_me) {
+          float tau[9];
+          kirchhoff_from_frame(U, eps, mp, tau);
+          const float h = P.h_f;
+          const float hm = h * m;
+          const float hs = -h * P.d_inv_f * V0;  // h * stress scale -(4/h^2) V0
+          float w9[9];
+          bspline_w(fx2[0], w9);
+          bspline_w(fx2[1], w9 + 3);
+          bspline_w(fx2[2], w9 + 6);
+          const int lx = b2[0] - (ox - 1), ly = b2[1] - (oy - 1), lz = b2[2] - (oz - 1);
+          // Ap = h m C ; Af = h (-(4/h^2) V0) tau (symmetric)
+          const f3 bp = {m * v.x - hm * (Cm[0] * fx2[0] + Cm[1] * fx2[1] + Cm[2] * fx2[2]),
+                         m * v.y - hm * (Cm[3] * fx2[0] + Cm[4] * fx2[1] + Cm[5] * fx2[2]),
+                         m * v.z - hm * (Cm[6] * fx2[0] + Cm[7] * fx2[1] + Cm[8] * fx2[2])};
+          const f3 bf = {fext.x - hs * (tau[0] * fx2[0] + tau[1] * fx2[1] + tau[2] * fx2[2]),
+                         fext.y - hs * (tau[3] * fx2[0] + tau[4] * fx2[1] + tau[5] * fx2[2]),
+                         fext.z - hs * (tau[6] * fx2[0] + tau[7] * fx2[1] + tau[8] * fx2[2])};
+          if (lx >= 0 && ly >= 0 && lz >= 0 && lx < CX && ly < CY && lz < CZ) {
+            cell = (lz * CY + ly) * CX + lx;
+            float4* p4 = reinterpret_cast<float4*>(S.pay[t]);
+            p4[0] = make_float4(m, w9[0], w9[1], w9[2]);
+            p4[1] = make_float4(w9[3], w9[4], w9[5], w9[6]);
+            p4[2] = make_float4(w9[7], w9[8], bp.x, bp.y);
+            p4[3] = make_float4(bp.z, hm * Cm[0], hm * Cm[1], hm * Cm[2]);
+            p4[4] = make_float4(hm * Cm[3], hm * Cm[4], hm * Cm[5], hm * Cm[6]);
+            p4[5] = make_float4(hm * Cm[7], hm * Cm[8], bf.x, bf.y);
+            p4[6] = make_float4(bf.z, hs * tau[0], hs * tau[1], hs * tau[2]);
+            p4[7] = make_float4(hs * tau[4], hs * tau[5], hs * tau[8], 0.f);
+            staged = true;
+            // bounds of |b + A off| over off in {0,1,2}^3 for the fixed-point scales
+            mx_m = fmaxf(mx_m, m);
+            const float ap0 = fabsf(hm) * (fabsf(Cm[0]) + fabsf(Cm[1]) + fabsf(Cm[2]));
+            const float ap1 = fabsf(hm) * (fabsf(Cm[3]) + fabsf(Cm[4]) + fabsf(Cm[5]));
+            const float ap2 = fabsf(hm) * (fabsf(Cm[6]) + fabsf(Cm[7]) + fabsf(Cm[8]));
+            mx_p = fmaxf(mx_p, fmaxf(fabsf(bp.x) + 2.f * ap0, fmaxf(fabsf(bp.y) + 2.f * ap1, fabsf(bp.z) + 2.f * ap2)));
+            const float af0 = fabsf(hs) * (fabsf(tau[0]) + fabsf(tau[1]) + fabsf(tau[2]));
+            const float af1 = fabsf(hs) * (fabsf(tau[3]) + fabsf(tau[4]) + fabsf(tau[5]));
+            const float af2 = fabsf(hs) * (fabsf(tau[6]) + fabsf(tau[7]) + fabsf(tau[8]));
+            mx_f = fmaxf(mx_f, fmaxf(fabsf(bf.x) + 2.f * af0, fmaxf(fabsf(bf.y) + 2.f * af1, fabsf(bf.z) + 2.f * af2)));
+          } else {
+            float Ap[9], Af[9];
+#pragma unroll
+            for (int k = 0; k < 9; ++k) {
+              Ap[k] = hm * Cm[k];
+              Af[k] = hs * tau[k];
+            }
+            scatter_global(P, penv, b2, w9, m, bp, Ap, bf, Af);
+          }
+        }
+        int rank_in_cell = 0;
+        if (staged) rank_in_cell = atomicAdd(&S.cnt[cell], 1);
+        if (valid) S.order[t] = staged ? ((cell << 16) | rank_in_cell) : -1;
+
+        // ---------------- write back in bucket order (the re-sort)
+        if (valid) {
+          P.nxt.x[0][j] = x.x; P.nxt.x[1][j] = x.y; P.nxt.x[2][j] = x.z;
+#pragma unroll
+          for (int k = 0; k < 9; ++k) P.nxt.G[k][j] = G[k];
+          P.nxt.mass[j] = m;
+          P.nxt.vol0[j] = V0;
+          P.nxt.meta[j] = meta;
+          P.nxt.pid[j] = pid;
+          if (write_vc) {
+            P.nxt.v[0][j] = v.x; P.nxt.v[1][j] = v.y; P.nxt.v[2][j] = v.z;
+#pragma unroll
+            for (int k = 0; k < 9; ++k) P.nxt.C[k][j] = Cm[k];
+          }
+          if (now_lost) key_new = P.n_keys - 1;
+          P.key[j] = key_new;
+        }
+        {  // next bucket key: warp-aggregated count
+          const unsigned am = __ballot_sync(FULL, valid);
+          if (valid) {
+            const unsigned peers = __match_any_sync(am, key_new);
+            const int leader = __ffs(peers) - 1;
+            int basecnt = 0;
+            if (lane == leader) basecnt = atomicAdd(&P.bucket_count[key_new], __popc(peers));
+            basecnt = __shfl_sync(peers, basecnt, leader);
+            P.rank[j] = basecnt + __popc(peers & ((1u << lane) - 1u));
+          }
+        }
+        if (do_g2p) {  // per-env max speed (bucket env-uniform): warp max -> one atomic
+          float sp = speed;
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) sp = fmaxf(sp, __shfl_xor_sync(FULL, sp, o));
+          if (lane == 0 && sp >= 0.0f) float_bits_max(&P.vmax_bits[benv], sp);
+        }
+      }
+      if (!do_p2g) {
+        __syncthreads();
+        continue;
+      }
+      // fixed-point scales of this round: |node sum| <= rn * max bound < 2^30 / scale
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        mx_m = fmaxf(mx_m, __shfl_xor_sync(FULL, mx_m, o));
+        mx_p = fmaxf(mx_p, __shfl_xor_sync(FULL, mx_p, o));
+        mx_f = fmaxf(mx_f, __shfl_xor_sync(FULL, mx_f, o));
+      }
+      if (lane == 0) {
+        atomicMax(&S.maxb[0], __float_as_uint(mx_m));
+        atomicMax(&S.maxb[1], __float_as_uint(mx_p));
+        atomicMax(&S.maxb[2], __float_as_uint(mx_f));
+      }
+      __syncthreads();
+
+      // ---------------- cell offsets + non-empty cell list
+      {
+        int n0 = 0, n1 = 0;
+        const int c0 = 2 * tid, c1 = 2 * tid + 1;
+        if (c0 < CN) n0 = S.cnt[c0];
+        if (c1 < CN) n1 = S.cnt[c1];
+        int tot;
+        const int o = block_excl_scan(S, n0 + n1, &tot);
+        const int ne = block_excl_scan(S, (n0 > 0) + (n1 > 0), &tot);
+        if (c0 < CN) {
+          S.off[c0] = o;
+          if (n0 > 0) S.clist[ne] = c0;
+        }
+        if (c1 < CN) {
+          S.off[c1] = o + n0;
+          if (n1 > 0) S.clist[ne + (n0 > 0)] = c1;
+        }
+        if (tid == 0) S.n_clist = tot;
+        __syncthreads();
+        int codes[kCap / kT];
+#pragma unroll
+        for (int q = 0; q < kCap / kT; ++q) {
+          const int t = q * kT + tid;
+          codes[q] = t < rn ? S.order[t] : -1;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int q = 0; q < kCap / kT; ++q)
+          if (codes[q] >= 0) S.order[S.off[codes[q] >> 16] + (codes[q] & 0xFFFF)] = q * kT + tid;
+        __syncthreads();
+      }
+
+      // ---------------- warp-cooperative scatter: lane = (particle group g, stencil row (dj, dk))
+      {
+        const float bm = __uint_as_float(S.maxb[0]), bpm = __uint_as_float(S.maxb[1]), bfm = __uint_as_float(S.maxb[2]);
+        const float lim = 1073741824.0f / (float)rn;  // 2^30 / rn
+        const float sc_m = bm > 0.f ? lim / bm : 0.f;
+        const float sc_p = bpm > 0.f ? lim / bpm : 0.f;
+        const float sc_f = bfm > 0.f ? lim / bfm : 0.f;
+        const int grp = lane / 9, row = lane % 9, dj = row % 3, dk = row / 3;
+        const float fdj = (float)dj, fdk = (float)dk;
+        const int ncl = S.n_clist;
+        for (int ci = warp; ci < ncl; ci += kT / 32) {
+          const int c = S.clist[ci];
+          const int n = S.cnt[c], base = S.off[c];
+          float acc[3][kNCH];
+#pragma unroll
+          for (int a = 0; a < 3; ++a)
+#pragma unroll
+            for (int q = 0; q < kNCH; ++q) acc[a][q] = 0.f;
+          if (grp < 3) {
+            for (int k = grp; k < n; k += 3) {
+              const float4* p4 = reinterpret_cast<const float4*>(S.pay[S.order[base + k]]);
+              // [0]=(m,wx0,wx1,wx2) [1]=(wy0,wy1,wy2,wz0) [2]=(wz1,wz2,bp.x,bp.y) [3]=(bp.z,Ap00,Ap01,Ap02)
+              // [4]=(Ap10,Ap11,Ap12,Ap20) [5]=(Ap21,Ap22,bf.x,bf.y) [6]=(bf.z,Af00,Af01,Af02) [7]=(Af11,Af12,Af22,-)
+              const float4 q0 = p4[0], q1 = p4[1], q2 = p4[2], q3 = p4[3], q4 = p4[4], q5 = p4[5], q6 = p4[6],
+                           q7 = p4[7];
+              const float wy = wsel(q1.x, q1.y, q1.z, dj);
+              const float wz = wsel(q1.w, q2.x, q2.y, dk);
+              const float wyz = wy * wz;
+              const float rpx = q2.z + q3.z * fdj + q3.w * fdk;
+              const float rpy = q2.w + q4.y * fdj + q4.z * fdk;
+              const float rpz = q3.x + q5.x * fdj + q5.y * fdk;
+              const float cpx = q3.y, cpy = q4.x, cpz = q4.w;
+              // Af symmetric: row0 (Af00, Af01, Af02), row1 (Af01, Af11, Af12), row2 (Af02, Af12, Af22)
+              const float rfx = q5.z + q6.z * fdj + q6.w * fdk;
+              const float rfy = q5.w + q7.x * fdj + q7.y * fdk;
+              const float rfz = q6.x + q7.y * fdj + q7.z * fdk;
+              const float cfx = q6.y, cfy = q6.z, cfz = q6.w;
+              const float m = q0.x;
+              const float w0 = wyz * q0.y, w1 = wyz * q0.z, w2 = wyz * q0.w;
+              acc[0][3] += w0 * m; acc[1][3] += w1 * m; acc[2][3] += w2 * m;
+              acc[0][0] += w0 * rpx; acc[0][1] += w0 * rpy; acc[0][2] += w0 * rpz;
+              acc[1][0] += w1 * (rpx + cpx); acc[1][1] += w1 * (rpy + cpy); acc[1][2] += w1 * (rpz + cpz);
+              acc[2][0] += w2 * (rpx + 2.f * cpx); acc[2][1] += w2 * (rpy + 2.f * cpy); acc[2][2] += w2 * (rpz + 2.f * cpz);
+              acc[0][4] += w0 * rfx; acc[0][5] += w0 * rfy; acc[0][6] += w0 * rfz;
+              acc[1][4] += w1 * (rfx + cfx); acc[1][5] += w1 * (rfy + cfy); acc[1][6] += w1 * (rfz + cfz);
+              acc[2][4] += w2 * (rfx + 2.f * cfx); acc[2][5] += w2 * (rfy + 2.f * cfy); acc[2][6] += w2 * (rfz + 2.f * cfz);
+            }
+          }
+#pragma unroll
+          for (int a = 0; a < 3; ++a)
+#pragma unroll
+            for (int q = 0; q < kNCH; ++q) {
+              const float s1 = __shfl_down_sync(FULL, acc[a][q], 9);
+              const float s2 = __shfl_down_sync(FULL, acc[a][q], 18);
+              acc[a][q] += s1 + s2;
+            }
+          if (lane < 9) {
+            const int cx = c % CX, cy = (c / CX) % CY, cz = c / (CX * CY);
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+              const int nt = ((cz + dk) * PY + (cy + dj)) * PX + (cx + a);
+#pragma unroll
+              for (int q = 0; q < kNCH; ++q) {
+                const float sc = q == 3 ? sc_m : (q < 3 ? sc_p : sc_f);
+                atomicAdd(&S.itile[q][nt], __float2int_rn(acc[a][q] * sc));
+              }
+            }
+          }
+        }
+        __syncthreads();
+        // ---------------- flush the round's node tile (vector REDs) + touched node blocks
+        const float qm = sc_m > 0.f ? 1.0f / sc_m : 0.f, qp = sc_p > 0.f ? 1.0f / sc_p : 0.f,
+                    qf = sc_f > 0.f ? 1.0f / sc_f : 0.f;
+        for (int t = tid; t < PN; t += kT) {
+          const int im = S.itile[3][t];
+          if (im != 0) {
+            const int lx = t % PX, ly = (t / PX) % PY, lz = t / (PX * PY);
+            const int gx = ox - 1 + lx, gy = oy - 1 + ly, gz = oz - 1 + lz;
+            if (gx >= 0 && gy >= 0 && gz >= 0 && gx < P.dims[0] && gy < P.dims[1] && gz < P.dims[2]) {
+              const long long gi = benv * P.nodes_per_env + ((long long)gz * P.dims[1] + gy) * P.dims[0] + gx;
+              atomicAdd(&P.gPM[gi], make_float4(qp * (float)S.itile[0][t], qp * (float)S.itile[1][t],
+                                                qp * (float)S.itile[2][t], qm * (float)im));
+              atomicAdd(&P.gF[gi], make_float4(qf * (float)S.itile[4][t], qf * (float)S.itile[5][t],
+                                               qf * (float)S.itile[6][t], 0.0f));
+              P.nb_flag[benv * P.blocks_per_env + ((gz / kBZ) * P.bdims[1] + gy / kBY) * P.bdims[0] + gx / kBX] = 1;
+            }
+          }
+#pragma unroll
+          for (int q = 0; q < kNCH; ++q) S.itile[q][t] = 0;
+        }
+        for (int c = tid; c < CN; c += kT) S.cnt[c] = 0;
+        __syncthreads();
+      }
+    }
+
+    if (penalty) {
+      const int b0 = P.body_off[benv], nb = min(P.body_off[benv + 1] - b0, kMaxBodiesPerEnv);
+      for (int t = tid; t < nb * 6; t += kT) {
+        const double val = S.wsum[t];
+        if (val != 0.0) atomicAdd(P.wrench + 6 * b0 + t, val);
+      }
+      if (tid < 3) {
+        const double a = S.wsum[6 * kMaxBodiesPerEnv + tid];
+        if (a != 0.0) {
+          atomicAdd(P.applied + 3 * benv + tid, a);
+          double r = 0.0;
+          for (int bb = 0; bb < nb; ++bb) r += S.wsum[6 * bb + tid];
+          atomicAdd(P.react + 3 * benv + tid, r);
+        }
+      }
+      if (tid == 0 && S.penmax) atomicMax(&P.max_pen_bits[benv], S.penmax);
+    }
+  }
+}
+
+// Bucket keys of stored positions (after uploads): no loss flagging here, a
+// particle outside the domain is flagged by the next P2G (mpm.hpp:226-245).
+__global__ void __launch_bounds__(256) k_rebin(SimParams P) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const bool valid = i < P.n;
+  int key = P.n_keys - 1;
+  if (valid) {
+    const unsigned meta = P.cur.meta[i];
+    if (!(meta >> kLostBit)) {
+      int b[3];
+      float fx[3];
+      const f3 x = load3(P.cur.x, i);
+      base_of(P, x.x, x.y, x.z, b, fx);
+      if (base_in_range(P, b)) key = bucket_of(P, (meta >> 8) & kEnvMask, b);
+    }
+    P.key[i] = key;
+  }
+  const unsigned am = __ballot_sync(0xffffffffu, valid);
+  if (!valid) return;
+  const int lane = threadIdx.x & 31;
+  const unsigned peers = __match_any_sync(am, key);
+  const int leader = __ffs(peers) - 1;
+  int basecnt = 0;
+  if (lane == leader) basecnt = atomicAdd(&P.bucket_count[key], __popc(peers));
+  basecnt = __shfl_sync(peers, basecnt, leader);
+  P.rank[i] = basecnt + __popc(peers & ((1u << lane) - 1u));
+}
+
+__global__ void k_perm(SimParams P) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= P.n) return;
+  P.perm[P.bucket_start[P.key[i]] + P.rank[i]] = (int)i;
+}
+
+// Zero the nodes touched by the last P2G (phase API: the reference clears
+// the dense grid before every p2g, mpm.hpp:411).
+__global__ void k_clear(SimParams P) {
+  const int nlist = *P.n_nb;
+  const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+  constexpr int NB = kBX * kBY * kBZ;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < (long long)nlist * NB;
+       t += (long long)gridDim.x * blockDim.x) {
+    const int nb = P.nb_list[t / NB], l = (int)(t % NB);
+    const int env = nb / P.blocks_per_env, lb = nb - env * P.blocks_per_env;
+    const int gx = kBX * (lb % P.bdims[0]) + l % kBX, gy = kBY * ((lb / P.bdims[0]) % P.bdims[1]) + (l / kBX) % kBY,
+              gz = kBZ * (lb / (P.bdims[0] * P.bdims[1])) + l / (kBX * kBY);
+    if (gx >= P.dims[0] || gy >= P.dims[1] || gz >= P.dims[2]) continue;
+    const long long gi = env * P.nodes_per_env + ((long long)gz * P.dims[1] + gy) * P.dims[0] + gx;
+    P.gPM[gi] = z;
+    P.gF[gi] = z;
+    P.gV[gi] = z;
+  }
+}
+
+// Grid update (mpm.hpp:315-342) with the grid-mode penalty hook
+// (coupling.hpp:186-214); one warp per touched node block (32 nodes).
+__global__ void __launch_bounds__(256) k_grid(SimParams P) {
+  static_assert(kBX * kBY * kBZ == 32, "one warp per node block");
+  const int nlist = *P.n_nb;
+  const int lane = threadIdx.x & 31;
+  const unsigned FULL = 0xffffffffu;
+  for (int item = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; item < nlist; item += (gridDim.x * blockDim.x) >> 5) {
+    const int nb = P.nb_list[item];
+    const int env = nb / P.blocks_per_env, lb = nb - env * P.blocks_per_env;
+    const int gx = kBX * (lb % P.bdims[0]) + lane % kBX, gy = kBY * ((lb / P.bdims[0]) % P.bdims[1]) + (lane / kBX) % kBY,
+              gz = kBZ * (lb / (P.bdims[0] * P.bdims[1])) + lane / (kBX * kBY);
+    const bool inside = gx < P.dims[0] && gy < P.dims[1] && gz < P.dims[2];
+    const long long gi = env * P.nodes_per_env + ((long long)gz * P.dims[1] + gy) * P.dims[0] + gx;
+    const float4 pm = inside ? P.gPM[gi] : make_float4(0.f, 0.f, 0.f, 0.f);
+    const float4 ff = inside ? P.gF[gi] : make_float4(0.f, 0.f, 0.f, 0.f);
+    const bool live = inside && pm.w > 0.0f;
+    const float dt = P.run[env].dt_c;
+    f3 vel = {0.f, 0.f, 0.f};
+    f3 f = {ff.x, ff.y, ff.z};
+    if (live) vel = (1.0f / pm.w) * f3{pm.x, pm.y, pm.z};  // pre-force node velocity
+    if (P.grid_mode) {
+      const int s0 = P.shape_off[env], s1 = P.shape_off[env + 1];
+      const int b0 = P.body_off[env];
+      const f3 xi = {(float)(P.origin[0] + P.h * gx), (float)(P.origin[1] + P.h * gy), (float)(P.origin[2] + P.h * gz)};
+      const float scale = P.mean_mass[env] > 0.0 ? (float)(pm.w / P.mean_mass[env]) : 1.0f;
+      for (int sidx = s0; sidx < s1; ++sidx) {
+        const ShapeDev& sh = P.shapes[sidx];
+        f3 fp = {0.f, 0.f, 0.f};
+        float pen = 0.0f;
+        const bool hit = live && penalty_force(sh, P.vol_pool, xi, vel, P.r_c_grid, P.c_d, fp, pen);
+        if (hit) {
+          fp = scale * fp;
+          f = f + fp;
+        } else {
+          fp = {0.f, 0.f, 0.f};
+        }
+        if (__any_sync(FULL, hit)) {
+          const f3 com = {sh.com[0], sh.com[1], sh.com[2]};
+          const f3 tq = cross(xi - com, f3{-fp.x, -fp.y, -fp.z});
+          double r[6] = {-(double)fp.x, -(double)fp.y, -(double)fp.z, (double)tq.x, (double)tq.y, (double)tq.z};
+#pragma unroll
+          for (int k = 0; k < 6; ++k)
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) r[k] += __shfl_xor_sync(FULL, r[k], o);
+          unsigned pb = hit ? __float_as_uint(pen) : 0u;
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) pb = max(pb, __shfl_xor_sync(FULL, pb, o));
+          if (lane == 0) {
+            double* wr = P.wrench + 6 * (b0 + sh.body);
+#pragma unroll
+            for (int k = 0; k < 6; ++k) atomicAdd(wr + k, r[k]);
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+              atomicAdd(P.react + 3 * env + k, r[k]);
+              atomicAdd(P.applied + 3 * env + k, -r[k]);
+            }
+            atomicMax(&P.max_pen_bits[env], pb);
+          }
+        }
+      }
+    }
+    if (!inside) continue;
+    if (live) {
+      vel = vel + dt * (f3{P.gravity[0], P.gravity[1], P.gravity[2]} + (1.0f / pm.w) * f);
+      const int idx[3] = {gx, gy, gz};
+#pragma unroll
+      for (int ax = 0; ax < 3; ++ax) {
+        if (idx[ax] < 2) {
+          if (!((P.boundary_slip >> (2 * ax)) & 1u)) vel = {0.f, 0.f, 0.f};
+          else if (comp(vel, ax) < 0.0f) vel = ax == 0 ? f3{0.f, vel.y, vel.z} : (ax == 1 ? f3{vel.x, 0.f, vel.z} : f3{vel.x, vel.y, 0.f});
+        }
+        if (idx[ax] >= P.dims[ax] - 2) {
+          if (!((P.boundary_slip >> (2 * ax + 1)) & 1u)) vel = {0.f, 0.f, 0.f};
+          else if (comp(vel, ax) > 0.0f) vel = ax == 0 ? f3{0.f, vel.y, vel.z} : (ax == 1 ? f3{vel.x, 0.f, vel.z} : f3{vel.x, vel.y, 0.f});
+        }
+      }
+    }
+    P.gV[gi] = make_float4(vel.x, vel.y, vel.z, 0.0f);
+    if (P.clear_on_read) {
+      const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+      P.gPM[gi] = z;
+      P.gF[gi] = z;
+    } else if (P.grid_mode && live) {
+      P.gF[gi] = make_float4(f.x, f.y, f.z, 0.0f);  // the grid hook adds to grid.force
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Per-env bookkeeping.
+
+__device__ void plan_cycles(const SimParams& P, int env, EnvRun& r) {  // mpm.hpp:399-409
+  const double vmax = (double)__uint_as_float(P.vmax_bits[env]);
+  int halvings = 0;
+  while (halvings < P.max_halvings && vmax * P.dt_full / (1 << halvings) > P.cfl_h) ++halvings;
+  if (vmax * P.dt_full / (1 << halvings) > P.cfl_h) {
+    set_error(P, env, kErrCfl, 0x7fffffff);
+    r.action = kActIdle;
+    r.substeps_left = 0;
+    return;
+  }
+  r.cycles = 1 << halvings;
+  r.dt_c = (float)(P.dt_full / r.cycles);
+  r.cyc_sum += r.cycles;
+}
+
+__global__ void k_set_action(SimParams P, int action, float dt) {
+  const int env = blockIdx.x * blockDim.x + threadIdx.x;
+  if (env >= P.n_env) return;
+  EnvRun& r = P.run[env];
+  r.action = action;
+  r.dt_c = dt;
+  r.cycle = 0;
+  r.cycles = 1;
+  r.substeps_left = 0;
+  if (action == kActG2P) P.vmax_bits[env] = 0u;
+}
+
+__global__ void k_call_begin(SimParams P, int n_sub, int first_action) {
+  const int env = blockIdx.x * blockDim.x + threadIdx.x;
+  if (env >= P.n_env) return;
+  EnvRun& r = P.run[env];
+  r.substeps_left = n_sub;
+  r.soft_in_rigid = 0;
+  r.cycle = 0;
+  r.cyc_sum = 0;
+  r.next_new_sub = 0;
+  r.next_new_rigid = 0;
+  r.action = n_sub > 0 ? first_action : kActIdle;
+  if (P.err_code[env]) {
+    r.action = kActIdle;
+    r.substeps_left = 0;
+    return;
+  }
+  if (n_sub > 0 && P.integrate_rigid) rigid_env(P, env, 1);  // rigid step 0: integrate + sync
+  if (n_sub > 0) plan_cycles(P, env, r);
+  P.vmax_bits[env] = 0u;
+}
+
+__global__ void k_iter_begin(SimParams P) {
+  const int env = blockIdx.x * blockDim.x + threadIdx.x;
+  if (env >= P.n_env) return;
+  EnvRun& r = P.run[env];
+  r.next_new_sub = 0;
+  r.next_new_rigid = 0;
+  if (r.substeps_left <= 0 || P.err_code[env]) {
+    r.action = kActIdle;
+    return;
+  }
+  if (r.cycle == r.cycles - 1 && r.substeps_left == 1) {
+    r.action = kActG2P;
+  } else {
+    r.action = kActFused;
+    if (r.cycle + 1 >= r.cycles) {
+      r.next_new_sub = 1;
+      r.next_new_rigid = P.integrate_rigid && (r.soft_in_rigid + 1 == P.n_soft);
+    }
+    if (r.next_new_rigid) {
+      // end of rigid step: pending_wrenches = wrenches (coupling.hpp:288), then the
+      // next rigid step integrates with them and syncs (coupling.hpp:250-259)
+      const int b0 = P.body_off[env], b1 = P.body_off[env + 1];
+      for (int k = 6 * b0; k < 6 * b1; ++k) P.pending[k] = P.wrench[k];
+      rigid_env(P, env, 1);
+    }
+  }
+  P.vmax_bits[env] = 0u;
+}
+
+__global__ void k_iter_end(SimParams P) {
+  const int env = blockIdx.x * blockDim.x + threadIdx.x;
+  if (env >= P.n_env) return;
+  EnvRun& r = P.run[env];
+  if (r.action == kActIdle) return;
+  double ex = P.applied[3 * env] + P.react[3 * env];
+  double ey = P.applied[3 * env + 1] + P.react[3 * env + 1];
+  double ez = P.applied[3 * env + 2] + P.react[3 * env + 2];
+  const double err = sqrt(ex * ex + ey * ey + ez * ez);
+  if (err > P.balance_max[env]) P.balance_max[env] = err;
+  for (int k = 0; k < 3; ++k) P.applied[3 * env + k] = P.react[3 * env + k] = 0.0;
+  const long long n_env_p = P.env_off[env + 1] - P.env_off[env];
+  if (n_env_p > 0 && (double)P.lost_count[env] / (double)n_env_p > P.lost_threshold)
+    set_error(P, env, kErrLost, 0x7fffffff);
+  if (r.action == kActFused) {
+    if (r.next_new_sub) {
+      r.substeps_left -= 1;
+      r.soft_in_rigid = (r.soft_in_rigid + 1) % P.n_soft;
+      r.cycle = 0;
+      plan_cycles(P, env, r);
+    } else {
+      r.cycle += 1;
+    }
+  } else if (r.action == kActG2P) {
+    r.substeps_left = 0;
+    if (P.integrate_rigid) {
+      const int b0 = P.body_off[env], b1 = P.body_off[env + 1];
+      for (int k = 6 * b0; k < 6 * b1; ++k) P.pending[k] = P.wrench[k];
+    }
+  }
+  if (P.err_code[env]) r.substeps_left = 0;
+}
+
+inline unsigned nblk(long long n, int t = 256) { return (unsigned)((n + t - 1) / t); }
+
+int sm_count() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+struct Timed {
+  KernelTimer* t;
+  int id;
+  cudaStream_t s;
+  cudaEvent_t a;
+  Timed(const SimParams& P, int id_, cudaStream_t s_, int nlaunch = 1) : t(P.timer), id(id_), s(s_), a(nullptr) {
+    if (t) a = t->begin(s, nlaunch);
+  }
+  ~Timed() {
+    if (t) t->end(id, a, s);
+  }
+};
+
+}  // namespace
+
+void configure_kernels() {
+  cudaFuncSetAttribute(k_particles, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(Smem));
+}
+
+void launch_rebin(const SimParams& P, cudaStream_t s) {
+  {
+    Timed tm(P, kKBin, s);
+    if (P.n > 0) k_rebin<<<nblk(P.n), 256, 0, s>>>(P);
+  }
+  Timed tm(P, kKBucketScan, s, 4);
+  scan_exclusive(P.bucket_count, P.bucket_start, P.n_keys, P.active_buckets, P.n_active_buckets, P.scan_tmp, s);
+  if (P.n > 0) k_perm<<<nblk(P.n), 256, 0, s>>>(P);
+}
+
+void launch_clear(const SimParams& P, cudaStream_t s) {
+  Timed tm(P, kKClear, s);
+  k_clear<<<sm_count() * 4, 256, 0, s>>>(P);
+}
+
+void launch_set_action(const SimParams& P, int action, float dt, cudaStream_t s) {
+  k_set_action<<<nblk(P.n_env), 256, 0, s>>>(P, action, dt);
+}
+
+void launch_call_begin(const SimParams& P, int n_sub, int first_action, cudaStream_t s) {
+  Timed tm(P, kKPlan, s);
+  k_call_begin<<<nblk(P.n_env), 256, 0, s>>>(P, n_sub, first_action);
+}
+
+void launch_particles(const SimParams& P, cudaStream_t s) {
+  {
+    Timed tm(P, kKP2G, s);
+    k_particles<<<sm_count() * 4, kT, sizeof(Smem), s>>>(P);
+  }
+  {
+    Timed tm(P, kKBucketScan, s, 4);
+    scan_exclusive(P.bucket_count, P.bucket_start, P.n_keys, P.active_buckets, P.n_active_buckets, P.scan_tmp, s);
+    if (P.n > 0) k_perm<<<nblk(P.n), 256, 0, s>>>(P);
+  }
+  Timed tm(P, kKBlockScan, s, 3);
+  scan_exclusive(P.nb_flag, P.nb_scan, P.n_keys - 1, P.nb_list, P.n_nb, P.scan_tmp, s);
+}
+
+void launch_grid(const SimParams& P, cudaStream_t s) {
+  Timed tm(P, kKGrid, s);
+  k_grid<<<sm_count() * 8, 256, 0, s>>>(P);
+}
+
+void launch_iteration_end(const SimParams& P, cudaStream_t s) {
+  Timed tm(P, kKEnd, s);
+  k_iter_end<<<nblk(P.n_env), 256, 0, s>>>(P);
+}
+
+void launch_iteration(const SimParams& P, bool bookkeeping, bool grid_update, cudaStream_t s) {
+  if (bookkeeping) {
+    Timed tm(P, kKRigid, s);
+    k_iter_begin<<<nblk(P.n_env), 256, 0, s>>>(P);
+  }
+  launch_particles(P, s);
+  {
+    Timed tm(P, kKEnd, s);
+    k_iter_end<<<nblk(P.n_env), 256, 0, s>>>(P);
+  }
+  if (grid_update) launch_grid(P, s);
+}
+
+}  // namespace msim_impl
