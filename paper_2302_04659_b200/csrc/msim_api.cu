@@ -111,7 +111,8 @@ struct msim_gpu_ctx {
   std::vector<char> env_grid_dirty;
 
   // host-mapped control words
-  int* h_ctl = nullptr;  // [0] max cycles, [1] any error
+  int* h_ctl = nullptr;  // host-mapped control words (unused by the fused pipeline)
+  DevBuf ctl_d;          // [0] device redo flag
   int* d_ctl = nullptr;
 
   double time = 0.0;
@@ -175,6 +176,8 @@ SimParams params(msim_gpu_ctx* c) {
   P.shape_src = c->shapes_host_d.as<ShapeHost>();
   P.pending = c->pending_d.as<double>();
   P.n_running = nullptr;
+  P.any_redo = c->ctl_d.as<int>();
+  P.redo_pass = 0;
   P.cur = c->buf[c->cur];
   P.nxt = c->buf[1 - c->cur];
   P.mats = c->mats_d.as<MatParams>();
@@ -564,6 +567,8 @@ int msim_gpu_create(const msim_soft_desc* desc, const msim_material* materials, 
     CK(cudaMemset(c->n_active_d.p, 0, sizeof(int)));
     CK(c->scan_tmp_d.ensure(sizeof(int) * scan_tmp_ints(std::max(c->n_keys, (int)std::min<long long>(c->nodes_per_env + 1, INT_MAX)))));
     CK(cudaHostAlloc(&c->h_ctl, 4 * sizeof(int), cudaHostAllocMapped));
+    CK(c->ctl_d.ensure(4 * sizeof(int)));
+    CK(cudaMemset(c->ctl_d.p, 0, 4 * sizeof(int)));
     CK(cudaHostGetDevicePointer(&c->d_ctl, c->h_ctl, 0));
     carve_particles(c, 0, 0);
     carve_particles(c, 1, 0);

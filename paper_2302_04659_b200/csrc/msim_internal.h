@@ -38,9 +38,13 @@ struct EnvRun {
   int action;          // kAct* for the next launch
   int next_new_sub;    // the P2G of this launch starts a new substep
   int next_new_rigid;  // ... and a new rigid step
-  float dt_c;          // dt / cycles (current cycle)
+  float dt_c;          // dt / cycles (current cycle): grid update
   int cyc_sum;         // report: cycles executed
-  int _pad[3];
+  float dt_g2p;        // dt of the G2P in this launch
+  float dt_p2g;        // dt folded into the P2G momentum (p + dt f) in this launch;
+                       // speculated as the current cycle dt when the P2G opens a new
+                       // substep, re-done on the device when the CFL plan disagrees
+  int redo;            // this env's P2G must be redone with dt_c (speculation missed)
 };
 
 // Internal error codes latched per environment (first one wins); mapped to
@@ -97,12 +101,12 @@ struct ShapeHost {  // shape description kept on device in double for the rigid 
 // the count of kernel launches. Host-only; SimParams carries a pointer.
 enum KernelId : int {
   kKPlan = 0, kKVmax, kKClear, kKBin, kKBucketScan, kKScatter, kKP2G, kKBlockScan, kKGrid, kKG2P,
-  kKEnd, kKRigid, kKStage, kKernelIds
+  kKEnd, kKRigid, kKStage, kKRedo, kKernelIds
 };
 inline const char* kernel_name(int id) {
   static const char* names[kKernelIds] = {"k_plan", "k_vmax", "k_clear", "k_bin", "bucket_scan", "k_scatter",
                                           "k_p2g", "block_scan", "k_grid", "k_g2p", "k_cycle_end",
-                                          "k_rigid", "k_stage"};
+                                          "k_rigid", "k_stage", "p2g_redo"};
   return id >= 0 && id < kKernelIds ? names[id] : "?";
 }
 struct KernelTimer {
@@ -187,6 +191,8 @@ struct SimParams {
   const ShapeHost* shape_src;
   double* pending;           // staged wrenches (pending_wrenches)
   int* n_running;            // envs with substeps left after the last iteration
+  int* any_redo;             // device flag: some env must redo its P2G (see EnvRun::redo)
+  int redo_pass;             // this particle launch is the redo pass
 
   Particles cur, nxt;
   const msim_dev::MatParams* mats;

@@ -11,21 +11,32 @@
 //                (mpm.hpp:166-181), and in the same pass the P2G of the next
 //                cycle: penalty hook (coupling.hpp:151-172), Kirchhoff stress
 //                from the SAME principal frame (mpm.hpp:152-161), and a
-//                warp-cooperative scatter of mass/momentum/force into a
-//                shared-memory node tile (cell-sorted, 3 particles x 9 stencil
-//                rows per warp, no per-particle atomics), flushed with
-//                vector REDs. Particles are written back in bucket order with
-//                their next bucket key (the per-cycle radix-style re-sort).
+//                scatter into a shared-memory node tile: staged particles are
+//                ordered by (rank within cell, cell) so the lanes of a warp
+//                hold distinct cells, and each thread adds its particle's 27
+//                node contributions with native int32 shared atomics on a
+//                per-round fixed-point scale (no CAS loops, no conflicts).
+//                The tile goes to HBM with vector REDs. Particles are written back in bucket
+//                order with their next bucket key (the per-cycle re-sort).
 //   scans        bucket offsets + active list, node-block list
 //   k_iter_end   per env: substep/cycle counters, CFL plan (mpm.hpp:400-409),
 //                lost-fraction check, force-balance diagnostic
-//   k_grid       per touched node block: p/m + dt (g + f/m), grid-mode penalty
-//                (coupling.hpp:186-214), boundary bands (mpm.hpp:315-342);
-//                consumes (zeroes) the P2G accumulators
+//   redo         only when a CFL halving changed the next cycle's dt: the
+//                P2G of that env is redone with the planned dt
+//   k_grid       per touched node block: (p + dt f)/m + dt g, grid-mode
+//                penalty (coupling.hpp:186-214), boundary bands
+//                (mpm.hpp:315-342); consumes (zeroes) the accumulators
 //
 // Because G2P(c) and P2G(c+1) share one pass, each particle-substep reads and
 // writes x, F-I, mass, V0, meta, pid once; v and C stay in registers except
 // at the first/last cycle of a call.
+//
+// Momentum channels: the default path folds the force into the momentum,
+// p + dt f (4 channels: what grid_update consumes, mpm.hpp:321). The dt of
+// the next cycle is known inside a substep; across substeps it is
+// speculated as the current cycle's and re-done on the device if the CFL
+// plan halves differently. The phase API and grid coupling keep momentum and
+// force apart (7 channels) like MpmGrid.
 #include <cuda_runtime.h>
 
 #include <cfloat>
@@ -38,27 +49,24 @@ namespace msim_impl {
 namespace {
 
 constexpr int kT = 128;    // threads per CTA (particle kernel), 4 CTAs per SM
+constexpr int kNW = kT / 32;
 constexpr int kCap = 256;  // particles staged per round
 constexpr int GX = kBX + 2, GY = kBY + 2, GZ = kBZ + 2, GN = GX * GY * GZ;  // G2P velocity tile
 constexpr int PX = kBX + 4, PY = kBY + 4, PZ = kBZ + 4, PN = PX * PY * PZ;  // P2G node tile (origin o-1)
 constexpr int CX = kBX + 2, CY = kBY + 2, CZ = kBZ + 2, CN = CX * CY * CZ;  // P2G base cells (origin o-1)
-constexpr int kNCH = 7;    // m, momentum, force
-constexpr int kPay = 32;   // staged P2G payload floats per particle (8 x float4)
+constexpr int kPay = 36;   // staged P2G payload floats per particle (9 x float4)
 constexpr int kWs = kMaxBodiesPerEnv * 6 + 3;
 
+template <int NCH>
 struct Smem {
   float4 gtile[GN];
-  int itile[kNCH][PN];     // fixed-point node accumulators (native int shared atomics)
+  int itile[NCH][PN];      // fixed-point node accumulators (native int shared atomics)
   float pay[kCap][kPay];
-  int cnt[CN];
-  int off[CN];
-  int clist[CN];
-  int order[kCap];
+  int cellof[kCap];        // local P2G cell of each staged slot, -1 if not staged
   double wsum[kWs];
-  int n_clist;
   unsigned penmax;
   unsigned maxb[3];
-  int scan_ws[8];
+  int scan_ws[kNW];
   int scan_tot;
 };
 
@@ -73,17 +81,17 @@ __device__ __forceinline__ int warp_incl_scan(int v) {
 }
 
 // Exclusive scan of one int per thread over the block (kT threads).
-__device__ __forceinline__ int block_excl_scan(Smem& S, int v, int* total) {
-  constexpr int NW = kT / 32;
+template <class SM>
+__device__ __forceinline__ int block_excl_scan(SM& S, int v, int* total) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   int inc = warp_incl_scan(v);
   if (lane == 31) S.scan_ws[wid] = inc;
   __syncthreads();
   if (wid == 0) {
-    int s = lane < NW ? S.scan_ws[lane] : 0;
+    int s = lane < kNW ? S.scan_ws[lane] : 0;
     int si = warp_incl_scan(s);
-    if (lane < NW) S.scan_ws[lane] = si - s;
-    if (lane == NW - 1) S.scan_tot = si;
+    if (lane < kNW) S.scan_ws[lane] = si - s;
+    if (lane == kNW - 1) S.scan_tot = si;
   }
   __syncthreads();
   int r = inc - v + S.scan_ws[wid];
@@ -92,56 +100,65 @@ __device__ __forceinline__ int block_excl_scan(Smem& S, int v, int* total) {
   return r;
 }
 
-__device__ __forceinline__ float wsel(float a, float b, float c, int i) { return i == 0 ? a : (i == 1 ? b : c); }
-
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   return v;
 }
 
+// Round-to-nearest float -> int for |x| < 2^22 with one FFMA-able add: the
+// integer lands in the low mantissa bits of x + 1.5 * 2^23 (avoids F2I).
+__device__ __forceinline__ int fix_rn(float x) { return __float_as_int(x + 12582912.0f) - 0x4B400000; }
+
 // Global-memory scatter of one particle (fallback when its stencil leaves the
 // bucket's P2G tile, e.g. a particle faster than the CFL bound assumed).
+template <int NCH>
 __device__ void scatter_global(const SimParams& P, int env, const int* b, const float* w9, float m, f3 bp,
-                               const float* Ap, f3 bf, const float* Af) {
+                               const float* Ap, f3 bf, const float* Af, bool mark) {
   for (int dk = 0; dk < 3; ++dk)
     for (int dj = 0; dj < 3; ++dj)
       for (int di = 0; di < 3; ++di) {
-        float w = w9[di] * w9[3 + dj] * w9[6 + dk];
-        f3 pq = {bp.x + Ap[0] * di + Ap[1] * dj + Ap[2] * dk, bp.y + Ap[3] * di + Ap[4] * dj + Ap[5] * dk,
-                 bp.z + Ap[6] * di + Ap[7] * dj + Ap[8] * dk};
-        f3 fq = {bf.x + Af[0] * di + Af[1] * dj + Af[2] * dk, bf.y + Af[3] * di + Af[4] * dj + Af[5] * dk,
-                 bf.z + Af[6] * di + Af[7] * dj + Af[8] * dk};
+        const float w = w9[di] * w9[3 + dj] * w9[6 + dk];
+        const f3 pq = {bp.x + Ap[0] * di + Ap[1] * dj + Ap[2] * dk, bp.y + Ap[3] * di + Ap[4] * dj + Ap[5] * dk,
+                       bp.z + Ap[6] * di + Ap[7] * dj + Ap[8] * dk};
         const int gx = b[0] + di, gy = b[1] + dj, gz = b[2] + dk;
         const long long gi = env * P.nodes_per_env + ((long long)gz * P.dims[1] + gy) * P.dims[0] + gx;
         atomicAdd(&P.gPM[gi], make_float4(w * pq.x, w * pq.y, w * pq.z, w * m));
-        atomicAdd(&P.gF[gi], make_float4(w * fq.x, w * fq.y, w * fq.z, 0.0f));
-        P.nb_flag[env * P.blocks_per_env + ((gz / kBZ) * P.bdims[1] + gy / kBY) * P.bdims[0] + gx / kBX] = 1;
+        if (NCH == 7) {
+          const f3 fq = {bf.x + Af[0] * di + Af[1] * dj + Af[2] * dk, bf.y + Af[3] * di + Af[4] * dj + Af[5] * dk,
+                         bf.z + Af[6] * di + Af[7] * dj + Af[8] * dk};
+          atomicAdd(&P.gF[gi], make_float4(w * fq.x, w * fq.y, w * fq.z, 0.0f));
+        }
+        if (mark) P.nb_flag[env * P.blocks_per_env + ((gz / kBZ) * P.bdims[1] + gy / kBY) * P.bdims[0] + gx / kBX] = 1;
       }
 }
 
+template <int NCH>
 __global__ void __launch_bounds__(kT, 4) k_particles(SimParams P) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  Smem& S = *reinterpret_cast<Smem*>(smem_raw);
+  Smem<NCH>& S = *reinterpret_cast<Smem<NCH>*>(smem_raw);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const unsigned FULL = 0xffffffffu;
+  const bool redo = P.redo_pass != 0;
+  if (redo && !*P.any_redo) return;
   const int nitems = *P.n_active_buckets;
 
-  for (int t = tid; t < kNCH * PN; t += kT) (&S.itile[0][0])[t] = 0;
-  for (int t = tid; t < CN; t += kT) S.cnt[t] = 0;
+  for (int t = tid; t < NCH * PN; t += kT) (&S.itile[0][0])[t] = 0;
 
   for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
     const int key = P.active_buckets[item];
-    const int s = P.bucket_start[key], e = P.bucket_start[key + 1];
     const bool lostb = key == P.n_keys - 1;
     const int benv = lostb ? 0 : key / P.blocks_per_env;
+    if (redo && (lostb || !P.run[benv].redo)) continue;  // CTA-uniform
+    const int s = P.bucket_start[key], e = P.bucket_start[key + 1];
     const int act = lostb ? kActIdle : P.run[benv].action;
     const bool do_g2p = act == kActFused || act == kActG2P;
     const bool do_p2g = act == kActP2G || act == kActFused;
     const int lb = key - benv * P.blocks_per_env;
     const int ox = kBX * (lb % P.bdims[0]), oy = kBY * ((lb / P.bdims[0]) % P.bdims[1]),
               oz = kBZ * (lb / (P.bdims[0] * P.bdims[1]));
-    const float dt = do_g2p ? P.run[benv].dt_c : 0.0f;
+    const float dt = do_g2p ? P.run[benv].dt_g2p : 0.0f;
+    const float dtp = lostb ? 0.0f : (redo ? P.run[benv].dt_c : P.run[benv].dt_p2g);  // NCH == 4 only
     const int s0 = lostb ? 0 : P.shape_off[benv], s1 = lostb ? 0 : P.shape_off[benv + 1];
     const bool penalty = do_p2g && !P.grid_mode && s1 > s0;
 
@@ -156,7 +173,7 @@ __global__ void __launch_bounds__(kT, 4) k_particles(SimParams P) {
         S.gtile[t] = v;
       }
     }
-    if (penalty)
+    if (penalty && !redo)
       for (int t = tid; t < kWs; t += kT) S.wsum[t] = 0.0;
     if (tid == 0) S.penmax = 0u;
     __syncthreads();
@@ -283,17 +300,19 @@ __global__ void __launch_bounds__(kT, 4) k_particles(SimParams P) {
             if (!lostb || pact == kActIdle || pact == kActG2P) key_new = bucket_of(P, penv, b2);
           } else if (p2g_here) {
             // leaves the domain now: reaction-only penalty, freeze, count (mpm.hpp:239-245)
-            if (!P.grid_mode && P.shape_off[penv + 1] > P.shape_off[penv]) penalty_reaction_only(P, penv, x, v);
+            if (!redo) {
+              if (!P.grid_mode && P.shape_off[penv + 1] > P.shape_off[penv]) penalty_reaction_only(P, penv, x, v);
+              atomicAdd((unsigned long long*)&P.lost_count[penv], 1ull);
+            }
             meta |= 1u << kLostBit;
             v = {0.f, 0.f, 0.f};
             write_vc = true;
-            atomicAdd((unsigned long long*)&P.lost_count[penv], 1ull);
             b2[0] = b2[1] = b2[2] = -10;
           }
         }
         const bool now_lost = meta >> kLostBit;
         const bool scatter_me = p2g_here && !lostb && !now_lost;
-        if (P.base_dbg && valid && (p2g_here || (lostb && was_lost && (pact == kActP2G || pact == kActFused)))) {
+        if (P.base_dbg && !redo && valid && (p2g_here || (lostb && was_lost && (pact == kActP2G || pact == kActFused)))) {
           P.base_dbg[3 * pid + 0] = now_lost ? -10 : b2[0];
           P.base_dbg[3 * pid + 1] = now_lost ? -10 : b2[1];
           P.base_dbg[3 * pid + 2] = now_lost ? -10 : b2[2];
@@ -308,7 +327,7 @@ __global__ void __launch_bounds__(kT, 4) k_particles(SimParams P) {
             const bool hit = scatter_me && penalty_force(sh, P.vol_pool, x, v, P.r_c_particle, P.c_d, f, pen);
             if (!hit) f = {0.f, 0.f, 0.f};
             fext = fext + f;
-            if (__any_sync(FULL, hit)) {
+            if (!redo && __any_sync(FULL, hit)) {
               const f3 com = {sh.com[0], sh.com[1], sh.com[2]};
               const f3 tq = hit ? cross(x - com, f3{-f.x, -f.y, -f.z}) : f3{0.f, 0.f, 0.f};
               float r6[6] = {-f.x, -f.y, -f.z, tq.x, tq.y, tq.z};
@@ -334,88 +353,101 @@ __global__ void __launch_bounds__(kT, 4) k_particles(SimParams P) {
           kirchhoff_from_frame(U, eps, mp, tau);
           const float h = P.h_f;
           const float hm = h * m;
-          const float hs = -h * P.d_inv_f * V0;  // h * stress scale -(4/h^2) V0
+          const float hs = -h * P.d_inv_f * V0;  // h * (-(4/h^2) V0): stress -> force matrix
           float w9[9];
           bspline_w(fx2[0], w9);
           bspline_w(fx2[1], w9 + 3);
           bspline_w(fx2[2], w9 + 6);
+          // momentum matrix A (h-scaled) and base b = m v (+ dt f_ext) - A fx; the node
+          // contribution is w (b + A off), off in {0,1,2}^3 (dpos = h (off - fx))
+          float A[9];
+          f3 bb;
+          float Af[9];
+          f3 bf = {0.f, 0.f, 0.f};
+          if (NCH == 4) {
+            const float ds = dtp * hs;
+#pragma unroll
+            for (int k = 0; k < 9; ++k) A[k] = hm * Cm[k] + ds * tau[k];
+            bb = (m * v + dtp * fext) - matvec(A, f3{fx2[0], fx2[1], fx2[2]});
+          } else {
+#pragma unroll
+            for (int k = 0; k < 9; ++k) {
+              A[k] = hm * Cm[k];
+              Af[k] = hs * tau[k];
+            }
+            bb = m * v - matvec(A, f3{fx2[0], fx2[1], fx2[2]});
+            bf = fext - matvec(Af, f3{fx2[0], fx2[1], fx2[2]});
+          }
           const int lx = b2[0] - (ox - 1), ly = b2[1] - (oy - 1), lz = b2[2] - (oz - 1);
-          // Ap = h m C ; Af = h (-(4/h^2) V0) tau (symmetric)
-          const f3 bp = {m * v.x - hm * (Cm[0] * fx2[0] + Cm[1] * fx2[1] + Cm[2] * fx2[2]),
-                         m * v.y - hm * (Cm[3] * fx2[0] + Cm[4] * fx2[1] + Cm[5] * fx2[2]),
-                         m * v.z - hm * (Cm[6] * fx2[0] + Cm[7] * fx2[1] + Cm[8] * fx2[2])};
-          const f3 bf = {fext.x - hs * (tau[0] * fx2[0] + tau[1] * fx2[1] + tau[2] * fx2[2]),
-                         fext.y - hs * (tau[3] * fx2[0] + tau[4] * fx2[1] + tau[5] * fx2[2]),
-                         fext.z - hs * (tau[6] * fx2[0] + tau[7] * fx2[1] + tau[8] * fx2[2])};
           if (lx >= 0 && ly >= 0 && lz >= 0 && lx < CX && ly < CY && lz < CZ) {
             cell = (lz * CY + ly) * CX + lx;
             float4* p4 = reinterpret_cast<float4*>(S.pay[t]);
+            // [m wx0 wx1 wx2] [wy0 wy1 wy2 wz0] [wz1 wz2 b.x b.y] [b.z A00 A01 A02] [A10 A11 A12 A20]
+            // [A21 A22 bf.x bf.y] [bf.z Af00 Af01 Af02] [Af11 Af12 Af22 -]   (Af symmetric)
             p4[0] = make_float4(m, w9[0], w9[1], w9[2]);
             p4[1] = make_float4(w9[3], w9[4], w9[5], w9[6]);
-            p4[2] = make_float4(w9[7], w9[8], bp.x, bp.y);
-            p4[3] = make_float4(bp.z, hm * Cm[0], hm * Cm[1], hm * Cm[2]);
-            p4[4] = make_float4(hm * Cm[3], hm * Cm[4], hm * Cm[5], hm * Cm[6]);
-            p4[5] = make_float4(hm * Cm[7], hm * Cm[8], bf.x, bf.y);
-            p4[6] = make_float4(bf.z, hs * tau[0], hs * tau[1], hs * tau[2]);
-            p4[7] = make_float4(hs * tau[4], hs * tau[5], hs * tau[8], 0.f);
+            p4[2] = make_float4(w9[7], w9[8], bb.x, bb.y);
+            p4[3] = make_float4(bb.z, A[0], A[1], A[2]);
+            p4[4] = make_float4(A[3], A[4], A[5], A[6]);
+            p4[5] = make_float4(A[7], A[8], bf.x, bf.y);
+            if (NCH == 7) {
+              p4[6] = make_float4(bf.z, Af[0], Af[1], Af[2]);
+              p4[7] = make_float4(Af[4], Af[5], Af[8], 0.f);
+            }
             staged = true;
             // bounds of |b + A off| over off in {0,1,2}^3 for the fixed-point scales
             mx_m = fmaxf(mx_m, m);
-            const float ap0 = fabsf(hm) * (fabsf(Cm[0]) + fabsf(Cm[1]) + fabsf(Cm[2]));
-            const float ap1 = fabsf(hm) * (fabsf(Cm[3]) + fabsf(Cm[4]) + fabsf(Cm[5]));
-            const float ap2 = fabsf(hm) * (fabsf(Cm[6]) + fabsf(Cm[7]) + fabsf(Cm[8]));
-            mx_p = fmaxf(mx_p, fmaxf(fabsf(bp.x) + 2.f * ap0, fmaxf(fabsf(bp.y) + 2.f * ap1, fabsf(bp.z) + 2.f * ap2)));
-            const float af0 = fabsf(hs) * (fabsf(tau[0]) + fabsf(tau[1]) + fabsf(tau[2]));
-            const float af1 = fabsf(hs) * (fabsf(tau[3]) + fabsf(tau[4]) + fabsf(tau[5]));
-            const float af2 = fabsf(hs) * (fabsf(tau[6]) + fabsf(tau[7]) + fabsf(tau[8]));
-            mx_f = fmaxf(mx_f, fmaxf(fabsf(bf.x) + 2.f * af0, fmaxf(fabsf(bf.y) + 2.f * af1, fabsf(bf.z) + 2.f * af2)));
-          } else {
-            float Ap[9], Af[9];
-#pragma unroll
-            for (int k = 0; k < 9; ++k) {
-              Ap[k] = hm * Cm[k];
-              Af[k] = hs * tau[k];
+            const float a0 = fabsf(A[0]) + fabsf(A[1]) + fabsf(A[2]);
+            const float a1 = fabsf(A[3]) + fabsf(A[4]) + fabsf(A[5]);
+            const float a2 = fabsf(A[6]) + fabsf(A[7]) + fabsf(A[8]);
+            mx_p = fmaxf(mx_p, fmaxf(fabsf(bb.x) + 2.f * a0, fmaxf(fabsf(bb.y) + 2.f * a1, fabsf(bb.z) + 2.f * a2)));
+            if (NCH == 7) {
+              const float f0 = fabsf(Af[0]) + fabsf(Af[1]) + fabsf(Af[2]);
+              const float f1 = fabsf(Af[3]) + fabsf(Af[4]) + fabsf(Af[5]);
+              const float f2 = fabsf(Af[6]) + fabsf(Af[7]) + fabsf(Af[8]);
+              mx_f = fmaxf(mx_f, fmaxf(fabsf(bf.x) + 2.f * f0, fmaxf(fabsf(bf.y) + 2.f * f1, fabsf(bf.z) + 2.f * f2)));
             }
-            scatter_global(P, penv, b2, w9, m, bp, Ap, bf, Af);
+          } else {
+            scatter_global<NCH>(P, penv, b2, w9, m, bb, A, bf, Af, !redo);
           }
         }
-        int rank_in_cell = 0;
-        if (staged) rank_in_cell = atomicAdd(&S.cnt[cell], 1);
-        if (valid) S.order[t] = staged ? ((cell << 16) | rank_in_cell) : -1;
+        if (t < kCap) S.cellof[t] = staged ? cell : -1;
 
-        // ---------------- write back in bucket order (the re-sort)
-        if (valid) {
-          P.nxt.x[0][j] = x.x; P.nxt.x[1][j] = x.y; P.nxt.x[2][j] = x.z;
-#pragma unroll
-          for (int k = 0; k < 9; ++k) P.nxt.G[k][j] = G[k];
-          P.nxt.mass[j] = m;
-          P.nxt.vol0[j] = V0;
-          P.nxt.meta[j] = meta;
-          P.nxt.pid[j] = pid;
-          if (write_vc) {
-            P.nxt.v[0][j] = v.x; P.nxt.v[1][j] = v.y; P.nxt.v[2][j] = v.z;
-#pragma unroll
-            for (int k = 0; k < 9; ++k) P.nxt.C[k][j] = Cm[k];
-          }
-          if (now_lost) key_new = P.n_keys - 1;
-          P.key[j] = key_new;
-        }
-        {  // next bucket key: warp-aggregated count
-          const unsigned am = __ballot_sync(FULL, valid);
+        if (!redo) {
+          // ---------------- write back in bucket order (the re-sort)
           if (valid) {
-            const unsigned peers = __match_any_sync(am, key_new);
-            const int leader = __ffs(peers) - 1;
-            int basecnt = 0;
-            if (lane == leader) basecnt = atomicAdd(&P.bucket_count[key_new], __popc(peers));
-            basecnt = __shfl_sync(peers, basecnt, leader);
-            P.rank[j] = basecnt + __popc(peers & ((1u << lane) - 1u));
-          }
-        }
-        if (do_g2p) {  // per-env max speed (bucket env-uniform): warp max -> one atomic
-          float sp = speed;
+            P.nxt.x[0][j] = x.x; P.nxt.x[1][j] = x.y; P.nxt.x[2][j] = x.z;
 #pragma unroll
-          for (int o = 16; o > 0; o >>= 1) sp = fmaxf(sp, __shfl_xor_sync(FULL, sp, o));
-          if (lane == 0 && sp >= 0.0f) float_bits_max(&P.vmax_bits[benv], sp);
+            for (int k = 0; k < 9; ++k) P.nxt.G[k][j] = G[k];
+            P.nxt.mass[j] = m;
+            P.nxt.vol0[j] = V0;
+            P.nxt.meta[j] = meta;
+            P.nxt.pid[j] = pid;
+            if (write_vc) {
+              P.nxt.v[0][j] = v.x; P.nxt.v[1][j] = v.y; P.nxt.v[2][j] = v.z;
+#pragma unroll
+              for (int k = 0; k < 9; ++k) P.nxt.C[k][j] = Cm[k];
+            }
+            if (now_lost) key_new = P.n_keys - 1;
+            P.key[j] = key_new;
+          }
+          {  // next bucket key: warp-aggregated count
+            const unsigned am = __ballot_sync(FULL, valid);
+            if (valid) {
+              const unsigned peers = __match_any_sync(am, key_new);
+              const int leader = __ffs(peers) - 1;
+              int basecnt = 0;
+              if (lane == leader) basecnt = atomicAdd(&P.bucket_count[key_new], __popc(peers));
+              basecnt = __shfl_sync(peers, basecnt, leader);
+              P.rank[j] = basecnt + __popc(peers & ((1u << lane) - 1u));
+            }
+          }
+          if (do_g2p) {  // per-env max speed (bucket env-uniform): warp max -> one atomic
+            float sp = speed;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) sp = fmaxf(sp, __shfl_xor_sync(FULL, sp, o));
+            if (lane == 0 && sp >= 0.0f) float_bits_max(&P.vmax_bits[benv], sp);
+          }
         }
       }
       if (!do_p2g) {
@@ -436,111 +468,78 @@ __global__ void __launch_bounds__(kT, 4) k_particles(SimParams P) {
       }
       __syncthreads();
 
-      // ---------------- cell offsets + non-empty cell list
+      // ---------------- per-thread scatter of one staged particle into the fixed-point tile
       {
-        int n0 = 0, n1 = 0;
-        const int c0 = 2 * tid, c1 = 2 * tid + 1;
-        if (c0 < CN) n0 = S.cnt[c0];
-        if (c1 < CN) n1 = S.cnt[c1];
-        int tot;
-        const int o = block_excl_scan(S, n0 + n1, &tot);
-        const int ne = block_excl_scan(S, (n0 > 0) + (n1 > 0), &tot);
-        if (c0 < CN) {
-          S.off[c0] = o;
-          if (n0 > 0) S.clist[ne] = c0;
-        }
-        if (c1 < CN) {
-          S.off[c1] = o + n0;
-          if (n1 > 0) S.clist[ne + (n0 > 0)] = c1;
-        }
-        if (tid == 0) S.n_clist = tot;
-        __syncthreads();
-        int codes[kCap / kT];
-#pragma unroll
-        for (int q = 0; q < kCap / kT; ++q) {
-          const int t = q * kT + tid;
-          codes[q] = t < rn ? S.order[t] : -1;
-        }
-        __syncthreads();
-#pragma unroll
-        for (int q = 0; q < kCap / kT; ++q)
-          if (codes[q] >= 0) S.order[S.off[codes[q] >> 16] + (codes[q] & 0xFFFF)] = q * kT + tid;
-        __syncthreads();
-      }
-
-      // ---------------- warp-cooperative scatter: lane = (particle group g, stencil row (dj, dk))
-      {
+        // fixed-point scale: every contribution |w (b + A off)| <= bound -> |x| <= 2^22, so a
+        // node sum of <= kCap = 256 contributions stays below 2^30 (no int32 overflow)
         const float bm = __uint_as_float(S.maxb[0]), bpm = __uint_as_float(S.maxb[1]), bfm = __uint_as_float(S.maxb[2]);
-        const float lim = 1073741824.0f / (float)rn;  // 2^30 / rn
-        const float sc_m = bm > 0.f ? lim / bm : 0.f;
-        const float sc_p = bpm > 0.f ? lim / bpm : 0.f;
-        const float sc_f = bfm > 0.f ? lim / bfm : 0.f;
-        const int grp = lane / 9, row = lane % 9, dj = row % 3, dk = row / 3;
-        const float fdj = (float)dj, fdk = (float)dk;
-        const int ncl = S.n_clist;
-        for (int ci = warp; ci < ncl; ci += kT / 32) {
-          const int c = S.clist[ci];
-          const int n = S.cnt[c], base = S.off[c];
-          float acc[3][kNCH];
+        const float sc_m = bm > 0.f ? 4194304.0f / bm : 0.f;
+        const float sc_p = bpm > 0.f ? 4194304.0f / bpm : 0.f;
+        const float sc_f = bfm > 0.f ? 4194304.0f / bfm : 0.f;
+        // Lane-strided slots: the 32 lanes of a warp take slots 8 apart, i.e. particles
+        // spread over the whole bucket, so their stencils rarely share a node (the
+        // staged order follows the particles' spatial order, neighbours share cells).
+        constexpr int kStride = kCap / 32;
 #pragma unroll
-          for (int a = 0; a < 3; ++a)
-#pragma unroll
-            for (int q = 0; q < kNCH; ++q) acc[a][q] = 0.f;
-          if (grp < 3) {
-            for (int k = grp; k < n; k += 3) {
-              const float4* p4 = reinterpret_cast<const float4*>(S.pay[S.order[base + k]]);
-              // [0]=(m,wx0,wx1,wx2) [1]=(wy0,wy1,wy2,wz0) [2]=(wz1,wz2,bp.x,bp.y) [3]=(bp.z,Ap00,Ap01,Ap02)
-              // [4]=(Ap10,Ap11,Ap12,Ap20) [5]=(Ap21,Ap22,bf.x,bf.y) [6]=(bf.z,Af00,Af01,Af02) [7]=(Af11,Af12,Af22,-)
-              const float4 q0 = p4[0], q1 = p4[1], q2 = p4[2], q3 = p4[3], q4 = p4[4], q5 = p4[5], q6 = p4[6],
-                           q7 = p4[7];
-              const float wy = wsel(q1.x, q1.y, q1.z, dj);
-              const float wz = wsel(q1.w, q2.x, q2.y, dk);
-              const float wyz = wy * wz;
-              const float rpx = q2.z + q3.z * fdj + q3.w * fdk;
-              const float rpy = q2.w + q4.y * fdj + q4.z * fdk;
-              const float rpz = q3.x + q5.x * fdj + q5.y * fdk;
-              const float cpx = q3.y, cpy = q4.x, cpz = q4.w;
-              // Af symmetric: row0 (Af00, Af01, Af02), row1 (Af01, Af11, Af12), row2 (Af02, Af12, Af22)
-              const float rfx = q5.z + q6.z * fdj + q6.w * fdk;
-              const float rfy = q5.w + q7.x * fdj + q7.y * fdk;
-              const float rfz = q6.x + q7.y * fdj + q7.z * fdk;
-              const float cfx = q6.y, cfy = q6.z, cfz = q6.w;
-              const float m = q0.x;
-              const float w0 = wyz * q0.y, w1 = wyz * q0.z, w2 = wyz * q0.w;
-              acc[0][3] += w0 * m; acc[1][3] += w1 * m; acc[2][3] += w2 * m;
-              acc[0][0] += w0 * rpx; acc[0][1] += w0 * rpy; acc[0][2] += w0 * rpz;
-              acc[1][0] += w1 * (rpx + cpx); acc[1][1] += w1 * (rpy + cpy); acc[1][2] += w1 * (rpz + cpz);
-              acc[2][0] += w2 * (rpx + 2.f * cpx); acc[2][1] += w2 * (rpy + 2.f * cpy); acc[2][2] += w2 * (rpz + 2.f * cpz);
-              acc[0][4] += w0 * rfx; acc[0][5] += w0 * rfy; acc[0][6] += w0 * rfz;
-              acc[1][4] += w1 * (rfx + cfx); acc[1][5] += w1 * (rfy + cfy); acc[1][6] += w1 * (rfz + cfz);
-              acc[2][4] += w2 * (rfx + 2.f * cfx); acc[2][5] += w2 * (rfy + 2.f * cfy); acc[2][6] += w2 * (rfz + 2.f * cfz);
-            }
+        for (int q = 0; q < kStride / kNW; ++q) {
+          const int t = lane * kStride + warp * (kStride / kNW) + q;
+          const int c = t < rn ? S.cellof[t] : -1;
+          if (c < 0) continue;
+          const float4* p4 = reinterpret_cast<const float4*>(S.pay[t]);
+          const float4 q0 = p4[0], q1 = p4[1], q2 = p4[2], q3 = p4[3], q4 = p4[4], q5 = p4[5];
+          const float wx[3] = {q0.y, q0.z, q0.w}, wy[3] = {q1.x, q1.y, q1.z}, wz[3] = {q1.w, q2.x, q2.y};
+          const float ms = q0.x * sc_m;
+          // A row-major: A00 q3.y A01 q3.z A02 q3.w A10 q4.x A11 q4.y A12 q4.z A20 q4.w A21 q5.x A22 q5.y
+          float4 qf6 = make_float4(0.f, 0.f, 0.f, 0.f), qf7 = qf6;
+          if (NCH == 7) {
+            qf6 = p4[6];
+            qf7 = p4[7];
           }
+          const int cx = c % CX, cy = (c / CX) % CY, cz = c / (CX * CY);
 #pragma unroll
-          for (int a = 0; a < 3; ++a)
+          for (int dk = 0; dk < 3; ++dk) {
 #pragma unroll
-            for (int q = 0; q < kNCH; ++q) {
-              const float s1 = __shfl_down_sync(FULL, acc[a][q], 9);
-              const float s2 = __shfl_down_sync(FULL, acc[a][q], 18);
-              acc[a][q] += s1 + s2;
-            }
-          if (lane < 9) {
-            const int cx = c % CX, cy = (c / CX) % CY, cz = c / (CX * CY);
+            for (int dj = 0; dj < 3; ++dj) {
+              const float wyz = wy[dj] * wz[dk];
+              float rx = q2.z + q3.z * dj + q3.w * dk;
+              float ry = q2.w + q4.y * dj + q4.z * dk;
+              float rz = q3.x + q5.x * dj + q5.y * dk;
+              float fxr = 0.f, fyr = 0.f, fzr = 0.f;
+              if (NCH == 7) {
+                fxr = q5.z + qf6.z * dj + qf6.w * dk;  // bf.x + Af01 dj + Af02 dk
+                fyr = q5.w + qf7.x * dj + qf7.y * dk;  // bf.y + Af11 dj + Af12 dk
+                fzr = qf6.x + qf7.y * dj + qf7.z * dk; // bf.z + Af12 dj + Af22 dk
+              }
+              const int nt = ((cz + dk) * PY + (cy + dj)) * PX + cx;
 #pragma unroll
-            for (int a = 0; a < 3; ++a) {
-              const int nt = ((cz + dk) * PY + (cy + dj)) * PX + (cx + a);
-#pragma unroll
-              for (int q = 0; q < kNCH; ++q) {
-                const float sc = q == 3 ? sc_m : (q < 3 ? sc_p : sc_f);
-                atomicAdd(&S.itile[q][nt], __float2int_rn(acc[a][q] * sc));
+              for (int di = 0; di < 3; ++di) {
+                const float w = wyz * wx[di];
+                const float wp = w * sc_p;
+                atomicAdd(&S.itile[3][nt + di], fix_rn(w * ms));
+                atomicAdd(&S.itile[0][nt + di], fix_rn(wp * rx));
+                atomicAdd(&S.itile[1][nt + di], fix_rn(wp * ry));
+                atomicAdd(&S.itile[2][nt + di], fix_rn(wp * rz));
+                rx += q3.y; ry += q4.x; rz += q4.w;  // + column 0 (A00, A10, A20)
+                if (NCH == 7) {
+                  const float wf = w * sc_f;
+                  atomicAdd(&S.itile[4 % NCH][nt + di], fix_rn(wf * fxr));
+                  atomicAdd(&S.itile[5 % NCH][nt + di], fix_rn(wf * fyr));
+                  atomicAdd(&S.itile[6 % NCH][nt + di], fix_rn(wf * fzr));
+                  fxr += qf6.y; fyr += qf6.z; fzr += qf6.w;  // + column 0 (Af00, Af01, Af02)
+                }
               }
             }
           }
         }
+        float sc[NCH];
+        sc[3] = sc_m;
+        sc[0] = sc[1] = sc[2] = sc_p;
+        if (NCH == 7) sc[4 % NCH] = sc[5 % NCH] = sc[6 % NCH] = sc_f;
         __syncthreads();
         // ---------------- flush the round's node tile (vector REDs) + touched node blocks
-        const float qm = sc_m > 0.f ? 1.0f / sc_m : 0.f, qp = sc_p > 0.f ? 1.0f / sc_p : 0.f,
-                    qf = sc_f > 0.f ? 1.0f / sc_f : 0.f;
+        float qs[NCH];
+#pragma unroll
+        for (int q = 0; q < NCH; ++q) qs[q] = sc[q] > 0.f ? 1.0f / sc[q] : 0.f;
         for (int t = tid; t < PN; t += kT) {
           const int im = S.itile[3][t];
           if (im != 0) {
@@ -548,22 +547,23 @@ __global__ void __launch_bounds__(kT, 4) k_particles(SimParams P) {
             const int gx = ox - 1 + lx, gy = oy - 1 + ly, gz = oz - 1 + lz;
             if (gx >= 0 && gy >= 0 && gz >= 0 && gx < P.dims[0] && gy < P.dims[1] && gz < P.dims[2]) {
               const long long gi = benv * P.nodes_per_env + ((long long)gz * P.dims[1] + gy) * P.dims[0] + gx;
-              atomicAdd(&P.gPM[gi], make_float4(qp * (float)S.itile[0][t], qp * (float)S.itile[1][t],
-                                                qp * (float)S.itile[2][t], qm * (float)im));
-              atomicAdd(&P.gF[gi], make_float4(qf * (float)S.itile[4][t], qf * (float)S.itile[5][t],
-                                               qf * (float)S.itile[6][t], 0.0f));
-              P.nb_flag[benv * P.blocks_per_env + ((gz / kBZ) * P.bdims[1] + gy / kBY) * P.bdims[0] + gx / kBX] = 1;
+              atomicAdd(&P.gPM[gi], make_float4(qs[0] * (float)S.itile[0][t], qs[1] * (float)S.itile[1][t],
+                                                qs[2] * (float)S.itile[2][t], qs[3] * (float)im));
+              if (NCH == 7)
+                atomicAdd(&P.gF[gi], make_float4(qs[4] * (float)S.itile[4][t], qs[5] * (float)S.itile[5][t],
+                                                 qs[6] * (float)S.itile[6][t], 0.0f));
+              if (!redo)
+                P.nb_flag[benv * P.blocks_per_env + ((gz / kBZ) * P.bdims[1] + gy / kBY) * P.bdims[0] + gx / kBX] = 1;
             }
           }
 #pragma unroll
-          for (int q = 0; q < kNCH; ++q) S.itile[q][t] = 0;
+          for (int q = 0; q < NCH; ++q) S.itile[q][t] = 0;
         }
-        for (int c = tid; c < CN; c += kT) S.cnt[c] = 0;
         __syncthreads();
       }
     }
 
-    if (penalty) {
+    if (penalty && !redo) {
       const int b0 = P.body_off[benv], nb = min(P.body_off[benv + 1] - b0, kMaxBodiesPerEnv);
       for (int t = tid; t < nb * 6; t += kT) {
         const double val = S.wsum[t];
@@ -652,7 +652,7 @@ __global__ void __launch_bounds__(256) k_grid(SimParams P) {
     const bool inside = gx < P.dims[0] && gy < P.dims[1] && gz < P.dims[2];
     const long long gi = env * P.nodes_per_env + ((long long)gz * P.dims[1] + gy) * P.dims[0] + gx;
     const float4 pm = inside ? P.gPM[gi] : make_float4(0.f, 0.f, 0.f, 0.f);
-    const float4 ff = inside ? P.gF[gi] : make_float4(0.f, 0.f, 0.f, 0.f);
+    const float4 ff = (inside && P.split) ? P.gF[gi] : make_float4(0.f, 0.f, 0.f, 0.f);
     const bool live = inside && pm.w > 0.0f;
     const float dt = P.run[env].dt_c;
     f3 vel = {0.f, 0.f, 0.f};
@@ -719,12 +719,15 @@ __global__ void __launch_bounds__(256) k_grid(SimParams P) {
     if (P.clear_on_read) {
       const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
       P.gPM[gi] = z;
-      P.gF[gi] = z;
+      if (P.split) P.gF[gi] = z;
     } else if (P.grid_mode && live) {
       P.gF[gi] = make_float4(f.x, f.y, f.z, 0.0f);  // the grid hook adds to grid.force
     }
   }
 }
+
+// ---------------------------------------------------------------------------
+// Per-env bookkeeping.
 
 // ---------------------------------------------------------------------------
 // Per-env bookkeeping.
@@ -746,18 +749,21 @@ __device__ void plan_cycles(const SimParams& P, int env, EnvRun& r) {  // mpm.hp
 
 __global__ void k_set_action(SimParams P, int action, float dt) {
   const int env = blockIdx.x * blockDim.x + threadIdx.x;
+  if (env == 0) *P.any_redo = 0;
   if (env >= P.n_env) return;
   EnvRun& r = P.run[env];
   r.action = action;
-  r.dt_c = dt;
+  r.dt_c = r.dt_g2p = r.dt_p2g = dt;
   r.cycle = 0;
   r.cycles = 1;
   r.substeps_left = 0;
+  r.redo = 0;
   if (action == kActG2P) P.vmax_bits[env] = 0u;
 }
 
 __global__ void k_call_begin(SimParams P, int n_sub, int first_action) {
   const int env = blockIdx.x * blockDim.x + threadIdx.x;
+  if (env == 0) *P.any_redo = 0;
   if (env >= P.n_env) return;
   EnvRun& r = P.run[env];
   r.substeps_left = n_sub;
@@ -766,6 +772,7 @@ __global__ void k_call_begin(SimParams P, int n_sub, int first_action) {
   r.cyc_sum = 0;
   r.next_new_sub = 0;
   r.next_new_rigid = 0;
+  r.redo = 0;
   r.action = n_sub > 0 ? first_action : kActIdle;
   if (P.err_code[env]) {
     r.action = kActIdle;
@@ -774,19 +781,25 @@ __global__ void k_call_begin(SimParams P, int n_sub, int first_action) {
   }
   if (n_sub > 0 && P.integrate_rigid) rigid_env(P, env, 1);  // rigid step 0: integrate + sync
   if (n_sub > 0) plan_cycles(P, env, r);
+  r.dt_g2p = 0.0f;
+  r.dt_p2g = r.dt_c;  // the first P2G knows its dt exactly
   P.vmax_bits[env] = 0u;
 }
 
 __global__ void k_iter_begin(SimParams P) {
   const int env = blockIdx.x * blockDim.x + threadIdx.x;
+  if (env == 0) *P.any_redo = 0;
   if (env >= P.n_env) return;
   EnvRun& r = P.run[env];
   r.next_new_sub = 0;
   r.next_new_rigid = 0;
+  r.redo = 0;
   if (r.substeps_left <= 0 || P.err_code[env]) {
     r.action = kActIdle;
     return;
   }
+  r.dt_g2p = r.dt_c;
+  r.dt_p2g = r.dt_c;  // same substep: exact; new substep: speculated (same cycle count)
   if (r.cycle == r.cycles - 1 && r.substeps_left == 1) {
     r.action = kActG2P;
   } else {
@@ -826,6 +839,11 @@ __global__ void k_iter_end(SimParams P) {
       r.soft_in_rigid = (r.soft_in_rigid + 1) % P.n_soft;
       r.cycle = 0;
       plan_cycles(P, env, r);
+      // the fused P2G folded dt_p2g into the momentum; a different plan needs a redo
+      if (!P.split && r.substeps_left > 0 && !P.err_code[env] && r.dt_c != r.dt_p2g) {
+        r.redo = 1;
+        atomicExch(P.any_redo, 1);
+      }
     } else {
       r.cycle += 1;
     }
@@ -837,6 +855,25 @@ __global__ void k_iter_end(SimParams P) {
     }
   }
   if (P.err_code[env]) r.substeps_left = 0;
+}
+
+// Redo pass, step 1: zero the P2G accumulators of envs whose speculated dt
+// missed (their node blocks are in the node-block list of this launch).
+__global__ void k_redo_clear(SimParams P) {
+  if (!*P.any_redo) return;
+  const int nlist = *P.n_nb;
+  const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+  constexpr int NB = kBX * kBY * kBZ;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < (long long)nlist * NB;
+       t += (long long)gridDim.x * blockDim.x) {
+    const int nb = P.nb_list[t / NB], l = (int)(t % NB);
+    const int env = nb / P.blocks_per_env, lb = nb - env * P.blocks_per_env;
+    if (!P.run[env].redo) continue;
+    const int gx = kBX * (lb % P.bdims[0]) + l % kBX, gy = kBY * ((lb / P.bdims[0]) % P.bdims[1]) + (l / kBX) % kBY,
+              gz = kBZ * (lb / (P.bdims[0] * P.bdims[1])) + l / (kBX * kBY);
+    if (gx >= P.dims[0] || gy >= P.dims[1] || gz >= P.dims[2]) continue;
+    P.gPM[env * P.nodes_per_env + ((long long)gz * P.dims[1] + gy) * P.dims[0] + gx] = z;
+  }
 }
 
 inline unsigned nblk(long long n, int t = 256) { return (unsigned)((n + t - 1) / t); }
@@ -865,10 +902,18 @@ struct Timed {
   }
 };
 
+void particle_kernel(const SimParams& P, cudaStream_t s) {
+  if (P.split)
+    k_particles<7><<<sm_count() * 4, kT, sizeof(Smem<7>), s>>>(P);
+  else
+    k_particles<4><<<sm_count() * 4, kT, sizeof(Smem<4>), s>>>(P);
+}
+
 }  // namespace
 
 void configure_kernels() {
-  cudaFuncSetAttribute(k_particles, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(Smem));
+  cudaFuncSetAttribute(k_particles<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(Smem<4>));
+  cudaFuncSetAttribute(k_particles<7>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(Smem<7>));
 }
 
 void launch_rebin(const SimParams& P, cudaStream_t s) {
@@ -898,7 +943,9 @@ void launch_call_begin(const SimParams& P, int n_sub, int first_action, cudaStre
 void launch_particles(const SimParams& P, cudaStream_t s) {
   {
     Timed tm(P, kKP2G, s);
-    k_particles<<<sm_count() * 4, kT, sizeof(Smem), s>>>(P);
+    SimParams Q = P;
+    Q.redo_pass = 0;
+    particle_kernel(Q, s);
   }
   {
     Timed tm(P, kKBucketScan, s, 4);
@@ -928,6 +975,15 @@ void launch_iteration(const SimParams& P, bool bookkeeping, bool grid_update, cu
   {
     Timed tm(P, kKEnd, s);
     k_iter_end<<<nblk(P.n_env), 256, 0, s>>>(P);
+  }
+  if (bookkeeping && !P.split) {
+    // speculated-dt misses (CFL halving changed between substeps): redo those envs' P2G.
+    // Both kernels exit immediately when no env needs it.
+    Timed tm(P, kKRedo, s, 2);
+    k_redo_clear<<<sm_count() * 2, 256, 0, s>>>(P);
+    SimParams Q = P;
+    Q.redo_pass = 1;
+    particle_kernel(Q, s);
   }
   if (grid_update) launch_grid(P, s);
 }
