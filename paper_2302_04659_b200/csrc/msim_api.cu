@@ -178,6 +178,7 @@ SimParams params(msim_gpu_ctx* c) {
   P.n_running = nullptr;
   P.any_redo = c->ctl_d.as<int>();
   P.redo_pass = 0;
+  P.hooks = 1;
   P.cur = c->buf[c->cur];
   P.nxt = c->buf[1 - c->cur];
   P.mats = c->mats_d.as<MatParams>();
@@ -829,6 +830,7 @@ static int manual_phase(msim_gpu_ctx* c, int which) {
       SimParams P = params(c);
       launch_set_action(P, kActP2G, (float)c->desc.dt, s);
       P.clear_on_read = 0;
+      P.hooks = 0;  // p2g() is hook-free (mpm.hpp:199); soft_substep installs the hooks
       launch_particles(P, s);
       launch_iteration_end(P, s);
       swap_buffers(c);
@@ -838,6 +840,7 @@ static int manual_phase(msim_gpu_ctx* c, int which) {
       SimParams P = params(c);
       launch_set_action(P, kActP2G, (float)c->desc.dt, s);
       P.clear_on_read = 0;
+      P.hooks = 0;
       launch_grid(P, s);
     } else {  // g2p_advect
       if (!c->perm_valid) launch_rebin(params(c), s), c->perm_valid = true;

@@ -193,6 +193,7 @@ struct SimParams {
   int* n_running;            // envs with substeps left after the last iteration
   int* any_redo;             // device flag: some env must redo its P2G (see EnvRun::redo)
   int redo_pass;             // this particle launch is the redo pass
+  int hooks;                 // run the penalty hooks (0: hook-free phase API, like p2g())
 
   Particles cur, nxt;
   const msim_dev::MatParams* mats;

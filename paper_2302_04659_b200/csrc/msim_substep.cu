@@ -160,7 +160,7 @@ __global__ void __launch_bounds__(kT, 4) k_particles(SimParams P) {
     const float dt = do_g2p ? P.run[benv].dt_g2p : 0.0f;
     const float dtp = lostb ? 0.0f : (redo ? P.run[benv].dt_c : P.run[benv].dt_p2g);  // NCH == 4 only
     const int s0 = lostb ? 0 : P.shape_off[benv], s1 = lostb ? 0 : P.shape_off[benv + 1];
-    const bool penalty = do_p2g && !P.grid_mode && s1 > s0;
+    const bool penalty = do_p2g && P.hooks && !P.grid_mode && s1 > s0;
 
     __syncthreads();  // smem reuse across items
     if (do_g2p) {
@@ -301,7 +301,7 @@ __global__ void __launch_bounds__(kT, 4) k_particles(SimParams P) {
           } else if (p2g_here) {
             // leaves the domain now: reaction-only penalty, freeze, count (mpm.hpp:239-245)
             if (!redo) {
-              if (!P.grid_mode && P.shape_off[penv + 1] > P.shape_off[penv]) penalty_reaction_only(P, penv, x, v);
+              if (P.hooks && !P.grid_mode && P.shape_off[penv + 1] > P.shape_off[penv]) penalty_reaction_only(P, penv, x, v);
               atomicAdd((unsigned long long*)&P.lost_count[penv], 1ull);
             }
             meta |= 1u << kLostBit;
@@ -658,7 +658,7 @@ __global__ void __launch_bounds__(256) k_grid(SimParams P) {
     f3 vel = {0.f, 0.f, 0.f};
     f3 f = {ff.x, ff.y, ff.z};
     if (live) vel = (1.0f / pm.w) * f3{pm.x, pm.y, pm.z};  // pre-force node velocity
-    if (P.grid_mode) {
+    if (P.grid_mode && P.hooks) {
       const int s0 = P.shape_off[env], s1 = P.shape_off[env + 1];
       const int b0 = P.body_off[env];
       const f3 xi = {(float)(P.origin[0] + P.h * gx), (float)(P.origin[1] + P.h * gy), (float)(P.origin[2] + P.h * gz)};
