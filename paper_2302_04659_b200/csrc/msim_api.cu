@@ -105,7 +105,9 @@ struct msim_gpu_ctx {
   bool grid_clean = true;    // P2G accumulators are zero (fused stepping consumes them)
 
   // binning + grid
-  DevBuf key_d, rank_d, bucket_count_d, bucket_start_d, active_buckets_d, n_active_d, perm_d,
+  int bset = 0;  // which of the two bucket-structure sets the next particle launch reads
+  DevBuf bucket_start_d[2], active_buckets_d[2], n_active_d[2], perm_d[2];
+  DevBuf key_d, rank_d, bucket_count_d,
       base_dbg_d;
   DevBuf gPM_d, gF_d, gV_d, nb_flag_d, nb_scan_d, nb_list_d, n_nb_d, scan_tmp_d;
   std::vector<char> env_grid_dirty;
@@ -199,10 +201,15 @@ SimParams params(msim_gpu_ctx* c) {
   P.key = c->key_d.as<int>();
   P.rank = c->rank_d.as<int>();
   P.bucket_count = c->bucket_count_d.as<int>();
-  P.bucket_start = c->bucket_start_d.as<int>();
-  P.active_buckets = c->active_buckets_d.as<int>();
-  P.n_active_buckets = c->n_active_d.as<int>();
-  P.perm = c->perm_d.as<int>();
+  const int rs = c->bset, ws = 1 - c->bset;
+  P.bucket_start = c->bucket_start_d[rs].as<int>();
+  P.active_buckets = c->active_buckets_d[rs].as<int>();
+  P.n_active_buckets = c->n_active_d[rs].as<int>();
+  P.perm = c->perm_d[rs].as<int>();
+  P.bucket_start_w = c->bucket_start_d[ws].as<int>();
+  P.active_buckets_w = c->active_buckets_d[ws].as<int>();
+  P.n_active_buckets_w = c->n_active_d[ws].as<int>();
+  P.perm_w = c->perm_d[ws].as<int>();
   P.base_dbg = c->record_binning ? c->base_dbg_d.as<int>() : nullptr;
   P.gPM = c->gPM_d.as<float4>();
   P.gF = c->gF_d.as<float4>();
@@ -261,7 +268,8 @@ void alloc_binning(msim_gpu_ctx* c) {
   long long n = std::max<long long>(c->n, 1);
   CK(c->key_d.ensure(sizeof(int) * n));
   CK(c->rank_d.ensure(sizeof(int) * n));
-  CK(c->perm_d.ensure(sizeof(int) * n));
+  CK(c->perm_d[0].ensure(sizeof(int) * n));
+  CK(c->perm_d[1].ensure(sizeof(int) * n));
   if (c->record_binning) {
     CK(c->base_dbg_d.ensure(sizeof(int) * 3 * n));
     CK(cudaMemsetAsync(c->base_dbg_d.p, 0xff, sizeof(int) * 3 * n, c->stream));
@@ -415,7 +423,10 @@ void prepare(msim_gpu_ctx* c, bool need_vmax) {
 }
 
 // After a particle launch the other buffer holds the particles (bucket order).
-void swap_buffers(msim_gpu_ctx* c) { c->cur ^= 1; }
+void swap_buffers(msim_gpu_ctx* c) {
+  c->cur ^= 1;
+  c->bset ^= 1;  // the bucket structure built after the launch is read by the next one
+}
 
 // n_sub soft substeps of every env (soft_substep, mpm.hpp:397-421), or the
 // rigid/soft part of env_step when integrate_rigid (coupling.hpp:248-293).
@@ -561,11 +572,14 @@ int msim_gpu_create(const msim_soft_desc* desc, const msim_material* materials, 
     CK(cudaMemset(c->nb_flag_d.p, 0, sizeof(int) * nblocks));
     CK(cudaMemset(c->n_nb_d.p, 0, sizeof(int)));
     CK(c->bucket_count_d.ensure(sizeof(int) * c->n_keys));
-    CK(c->bucket_start_d.ensure(sizeof(int) * (c->n_keys + 1)));
-    CK(c->active_buckets_d.ensure(sizeof(int) * c->n_keys));
-    CK(c->n_active_d.ensure(sizeof(int)));
+    for (int k = 0; k < 2; ++k) {
+      CK(c->bucket_start_d[k].ensure(sizeof(int) * (c->n_keys + 1)));
+      CK(c->active_buckets_d[k].ensure(sizeof(int) * c->n_keys));
+      CK(c->n_active_d[k].ensure(sizeof(int)));
+      CK(cudaMemset(c->n_active_d[k].p, 0, sizeof(int)));
+    }
     CK(cudaMemset(c->bucket_count_d.p, 0, sizeof(int) * c->n_keys));
-    CK(cudaMemset(c->n_active_d.p, 0, sizeof(int)));
+
     CK(c->scan_tmp_d.ensure(sizeof(int) * scan_tmp_ints(std::max(c->n_keys, (int)std::min<long long>(c->nodes_per_env + 1, INT_MAX)))));
     CK(cudaHostAlloc(&c->h_ctl, 4 * sizeof(int), cudaHostAllocMapped));
     CK(c->ctl_d.ensure(4 * sizeof(int)));

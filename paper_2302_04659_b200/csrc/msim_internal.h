@@ -221,7 +221,11 @@ struct SimParams {
   int* bucket_start;             // n_keys + 1
   int* active_buckets;           // list
   int* n_active_buckets;
-  int* perm;
+  int* perm;                     // read set: sorted slot -> particle index in cur
+  int* perm_w;                   // write set (built after the particle kernel for the next launch)
+  int* bucket_start_w;
+  int* active_buckets_w;
+  int* n_active_buckets_w;
   int* base_dbg;                 // optional: base per pid (3 ints), -10 if lost
 
   // grid (float4 per node)

@@ -614,7 +614,7 @@ __global__ void __launch_bounds__(256) k_rebin(SimParams P) {
 __global__ void k_perm(SimParams P) {
   const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (i >= P.n) return;
-  P.perm[P.bucket_start[P.key[i]] + P.rank[i]] = (int)i;
+  P.perm_w[P.bucket_start_w[P.key[i]] + P.rank[i]] = (int)i;
 }
 
 // Zero the nodes touched by the last P2G (phase API: the reference clears
@@ -921,9 +921,15 @@ void launch_rebin(const SimParams& P, cudaStream_t s) {
     Timed tm(P, kKBin, s);
     if (P.n > 0) k_rebin<<<nblk(P.n), 256, 0, s>>>(P);
   }
+  // keys of the stored positions describe the NEXT particle launch: write the read set
+  SimParams Q = P;
+  Q.perm_w = P.perm;
+  Q.bucket_start_w = P.bucket_start;
+  Q.active_buckets_w = P.active_buckets;
+  Q.n_active_buckets_w = P.n_active_buckets;
   Timed tm(P, kKBucketScan, s, 4);
-  scan_exclusive(P.bucket_count, P.bucket_start, P.n_keys, P.active_buckets, P.n_active_buckets, P.scan_tmp, s);
-  if (P.n > 0) k_perm<<<nblk(P.n), 256, 0, s>>>(P);
+  scan_exclusive(Q.bucket_count, Q.bucket_start_w, Q.n_keys, Q.active_buckets_w, Q.n_active_buckets_w, Q.scan_tmp, s);
+  if (Q.n > 0) k_perm<<<nblk(Q.n), 256, 0, s>>>(Q);
 }
 
 void launch_clear(const SimParams& P, cudaStream_t s) {
@@ -949,7 +955,9 @@ void launch_particles(const SimParams& P, cudaStream_t s) {
   }
   {
     Timed tm(P, kKBucketScan, s, 4);
-    scan_exclusive(P.bucket_count, P.bucket_start, P.n_keys, P.active_buckets, P.n_active_buckets, P.scan_tmp, s);
+    // the next launch's bucket structure goes to the write set: the redo pass of this
+    // launch still reads this launch's perm / bucket offsets
+    scan_exclusive(P.bucket_count, P.bucket_start_w, P.n_keys, P.active_buckets_w, P.n_active_buckets_w, P.scan_tmp, s);
     if (P.n > 0) k_perm<<<nblk(P.n), 256, 0, s>>>(P);
   }
   Timed tm(P, kKBlockScan, s, 3);

@@ -1,0 +1,151 @@
+"""More parity cases of the CUDA path against the CPU oracle: CFL halving
+(including the device-side speculative-dt redo), grid-mode coupling, every
+collider type (plane, sphere, box, capsule, SDF volume) with scripted
+motion, slip boundaries, n_soft > 1 (the wrench summation quirk,
+SURVEY App. A.1 #14), particles leaving the domain, batched envs with
+different cycle counts. Tolerances: x, v 1e-4 normwise relative; per-body
+force 1e-3 (floor 1e-6 N); lost flags exact."""
+import numpy as np
+import pytest
+
+from gpu_helpers import rel
+from oracle.oracle_py import OracleWorld
+from paper_2302_04659_b200 import GpuWorld, SimulationDiverged, abi
+from paper_2302_04659_b200.scenes import (SOFT_CLAY, STIFF_CLAY, V0_SOFT, BodySpec, Scene, ShapeSpec, block_env,
+                                          box_sdf_volume, lattice_span, quat_from_axis_angle, soft_contact)
+
+pytestmark = pytest.mark.gpu
+
+
+def compare(scene, steps=1, gw=None, envs=None, wrench=True, tol_x=1e-4, tol_v=1e-4):
+    gw = gw or GpuWorld(scene)
+    envs = range(len(scene.envs)) if envs is None else envs
+    ows = {e: OracleWorld(scene, env=e) for e in envs}
+    for _ in range(steps):
+        gw.env_step()
+        for o in ows.values():
+            o.env_step()
+    worst = 0.0
+    for e, o in ows.items():
+        pg, po = gw.particles(e), o.particles()
+        ex = np.linalg.norm(pg["x"] - po["x"]) / np.linalg.norm(po["x"])
+        ev = rel(pg["v"], po["v"])
+        assert ex < tol_x, (e, ex)
+        assert ev < tol_v, (e, ev)
+        assert np.array_equal(pg["lost"], po["lost"]), e
+        worst = max(worst, ev)
+        if wrench and scene.envs[e].bodies:
+            fg, _ = gw.wrenches(e, pending=True)
+            fo, _ = o.wrenches(pending=True)
+            for b in range(len(fo)):
+                assert np.linalg.norm(fg[b] - fo[b]) / max(np.linalg.norm(fo[b]), 1e-6) < 1e-3, (e, b, fg[b], fo[b])
+        assert gw.report(e).cfl_cycles >= 0
+    return gw, ows, worst
+
+
+def small_block(seed, lo=(0.10, 0.10, 0.10), n=(10, 10, 6), v=None, mat=SOFT_CLAY, mid=0):
+    env = block_env(lo, n, mid, mat, V0_SOFT, seed=seed, vel_seed=seed + 1)
+    if v is not None:
+        env.v = env.v + np.asarray(v)
+    return env
+
+
+def test_cfl_halving_and_redo_batched():
+    """Env 0 crosses the CFL threshold during the step (cycles 1 -> 2: the fused
+    P2G speculated dt must be re-done); env 1 halves every substep; env 2 never."""
+    envs = [small_block(11), small_block(13, v=(9.0, 0, 0)), small_block(15)]
+    envs[0].v = np.tile([0.0, 0.0, -7.95], (envs[0].n, 1))  # free fall crosses 0.4 h / dt = 8 m/s mid-step
+    envs[0].x[:, 2] += 0.30
+    envs[1].x[:, 0] -= 0.05
+    scene = Scene(name="cfl", dims=(64, 64, 64), h=0.01, dt=5e-4, envs=envs, n_rigid=25)
+    gw, ows, _ = compare(scene)
+    cyc = [gw.report(e).cfl_cycles for e in range(3)]
+    assert cyc[1] == 50 and cyc[2] == 25 and 25 < cyc[0] < 50, cyc
+
+
+def test_grid_coupling_mode():
+    """penalty_grid (coupling.hpp:186-214): node forces scaled by m_i / mean particle mass."""
+    env = small_block(21, lo=(0.10, 0.10, 0.041), n=(10, 10, 7))
+    env.v = np.tile([0.02, 0.0, -0.1], (env.n, 1))
+    floor = BodySpec(mode=abi.BODY_KINEMATIC, t=(0, 0, 0.04))
+    env.bodies = [floor]
+    env.shapes = [ShapeSpec(abi.SHAPE_PLANE, 0, params=(0, 0, 1, 0))]
+    scene = Scene(name="grid", dims=(32, 32, 32), h=0.01, dt=2e-4, envs=[env], n_rigid=4,
+                  coupling_mode=abi.COUPLING_GRID)
+    gw, ows, _ = compare(scene, steps=2)
+
+
+def test_all_collider_types_scripted():
+    """Plane (tilted), sphere, box, capsule and an SDF volume (software trilinear,
+    sdf.hpp:46-62) on scripted bodies moving/rotating into a clay slab."""
+    env = small_block(31, lo=(0.12, 0.12, 0.03), n=(30, 30, 8))
+    top = 0.03 + lattice_span(8, V0_SOFT)
+    dims, org, vox, smp = box_sdf_volume((0.02, 0.02, 0.015), 0.005, 0.015)
+    bodies = [
+        BodySpec(mode=abi.BODY_KINEMATIC, q=quat_from_axis_angle((1, 0, 0), 0.05), t=(0, 0, 0.026)),
+        BodySpec(mode=abi.BODY_SCRIPTED, t=(0.16, 0.16, top + 0.018), v=(0.0, 0.0, -0.05), w=(0, 0, 1.0)),
+        BodySpec(mode=abi.BODY_SCRIPTED, q=quat_from_axis_angle((0, 1, 1), 0.4), t=(0.20, 0.16, top + 0.012),
+                 v=(0.01, 0.0, -0.04)),
+        BodySpec(mode=abi.BODY_SCRIPTED, q=quat_from_axis_angle((1, 0, 0), 1.5707963), t=(0.16, 0.22, top + 0.008),
+                 v=(0.0, -0.01, -0.03), w=(0.2, 0, 0)),
+        BodySpec(mode=abi.BODY_SCRIPTED, t=(0.22, 0.22, top + 0.016), v=(0.0, 0.0, -0.05), w=(0, 0.5, 0)),
+    ]
+    shapes = [
+        ShapeSpec(abi.SHAPE_PLANE, 0, params=(0, 0, 1, 0), **soft_contact()),
+        ShapeSpec(abi.SHAPE_SPHERE, 1, params=(0.02,), **soft_contact()),
+        ShapeSpec(abi.SHAPE_BOX, 2, params=(0.02, 0.015, 0.01), local_t=(0.0, 0.0, 0.002), **soft_contact()),
+        ShapeSpec(abi.SHAPE_CAPSULE, 3, params=(0.02, 0.008), **soft_contact()),
+        ShapeSpec(abi.SHAPE_VOLUME, 4, vol_dims=dims, vol_origin=org, vol_voxel=vox, vol_samples=smp, **soft_contact()),
+    ]
+    env.bodies, env.shapes = bodies, shapes
+    scene = Scene(name="shapes", dims=(40, 40, 40), h=0.01, dt=5e-4, envs=[env], c_d=0.05)
+    gw, ows, _ = compare(scene, steps=2)
+    fg, _ = gw.wrenches(0, pending=True)
+    assert np.count_nonzero(np.linalg.norm(fg, axis=1)) >= 3  # several colliders in contact
+
+
+def test_slip_boundaries_and_stiff_material():
+    env = small_block(41, lo=(0.10, 0.10, 0.025), n=(12, 12, 6), v=(0.3, -0.2, -0.5), mat=STIFF_CLAY, mid=1)
+    scene = Scene(name="slip", dims=(32, 32, 32), h=0.01, dt=2e-4, envs=[env], materials=[SOFT_CLAY, STIFF_CLAY],
+                  boundary=(1, 1, 1, 1, 1, 1))
+    compare(scene, steps=2)
+
+
+def test_nsoft2_dynamic_body_wrench_quirk():
+    """n_soft = 2: wrenches summed over both substeps, applied once with
+    dt_rigid = n_soft dt at the next rigid step (coupling.hpp:248-251, :288)."""
+    env = small_block(51, lo=(0.10, 0.10, 0.06), n=(10, 10, 7))
+    ball = BodySpec(mode=abi.BODY_DYNAMIC, t=(0.12, 0.12, 0.115), v=(0, 0, -0.5), mass=0.05, inertia=(8e-6,) * 3)
+    env.bodies = [ball]
+    env.shapes = [ShapeSpec(abi.SHAPE_SPHERE, 0, params=(0.015,))]
+    scene = Scene(name="nsoft2", dims=(32, 32, 32), h=0.01, dt=2e-4, envs=[env], n_rigid=5, n_soft=2)
+    gw, ows, _ = compare(scene, steps=6)
+    bg, bo = gw.bodies(0)[0], ows[0].bodies()[0]
+    assert np.allclose(np.array(bg.t), np.array(bo.t), atol=1e-7)
+    assert abs(bg.v[2] - bo.v[2]) <= 1e-3 * abs(bo.v[2])
+
+
+def test_particles_leaving_domain_are_frozen():
+    """Lost particles: frozen with v = 0 and counted once (mpm.hpp:239-245)."""
+    env = small_block(61, lo=(0.03, 0.10, 0.10), n=(8, 8, 8), v=(-0.5, 0, 0))
+    env.x[:7, 0] = -0.05  # outside the grid: flagged by the first P2G
+    env.x[7:9, 2] = 0.5
+    scene = Scene(name="lost", dims=(32, 32, 32), h=0.01, dt=5e-4, envs=[env], gravity=(0, 0, 0),
+                  lost_fraction_threshold=1.0, n_rigid=25)
+    gw, ows, _ = compare(scene, steps=2)
+    assert gw.lost_count(0) == ows[0].lost_count() > 0
+
+
+def test_divergence_errors_match_reference_semantics():
+    env = small_block(71)
+    scene = Scene(name="cfl_err", dims=(32, 32, 32), h=0.01, dt=1e-3, envs=[env])
+    scene.envs[0].v = np.tile([500.0, 0, 0], (env.n, 1))
+    gw = GpuWorld(scene)
+    with pytest.raises(SimulationDiverged, match="CFL"):
+        gw.env_step()
+    env = small_block(73, lo=(0.05, 0.10, 0.10), n=(6, 6, 6))
+    env.x[:5, 0] = -0.05  # 5 / 216 > lost_fraction_threshold 0.01
+    scene = Scene(name="lost_err", dims=(32, 32, 32), h=0.01, dt=5e-4, envs=[env], gravity=(0, 0, 0))
+    gw = GpuWorld(scene)
+    with pytest.raises(SimulationDiverged, match="lost particle fraction"):
+        gw.env_step()
