@@ -30,9 +30,11 @@ sys.path.insert(0, ROOT)
 
 import numpy as np  # noqa: E402
 
-BYTES_PER_PS = 268.0        # fp32 SoA compulsory particle traffic per particle-substep
-P2G_BYTES = 112.0           # P2G read x, v, C, F, Jp, mass, V0, material
-G2P_BYTES = 156.0           # G2P read x, F, Jp, material (56) + write x, v, C, F, Jp (100)
+BYTES_PER_PS = 268.0        # BASELINE.md / SURVEY.md §8d: algorithmic bytes per particle-substep
+                            #   P2G read 112 + G2P read 56 + G2P write 100 (fp32 SoA)
+# k_particles runs G2P of one cycle and P2G of the next in one pass: one launch
+# is one particle-substep of every particle, so its algorithmic bytes per launch
+# are 268 B x particles.
 METRIC = "particle-substeps/sec and env-steps/sec per GPU, % HBM roofline, 1/2/4/8 B200"
 
 
@@ -172,6 +174,17 @@ def cpu_baseline_sample(scene_env_fn, substeps):
     return ps / t_total, f"2 config-D envs (write + pinch) x 1 env step (25 substeps), {ps} particle-substeps"
 
 
+def load_traffic(kernel: str):
+    """dram__bytes_read.sum + dram__bytes_write.sum per particle of the dominant kernel,
+    from the committed ncu --set full capture (profiles/traffic.json), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            t = json.load(f)
+        return t[kernel]["dram_bytes_per_particle"], t[kernel].get("source", "")
+    except Exception:
+        return None, None
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -186,12 +199,21 @@ def run_ours(args):
         torch.cuda.set_device(0)
 
     from paper_2302_04659_b200 import GpuWorld, abi
-    from paper_2302_04659_b200.scenes import config_d
+    from paper_2302_04659_b200.dist import StepStats, allreduce_stats, weak_first_env
+    from paper_2302_04659_b200.scenes import config_d, config_e
 
     lib = abi.load()
-    n_envs = args.envs
     t_setup = time.perf_counter()
-    scene = config_d(n_envs=n_envs, first_env=rank * n_envs)
+    if args.config == "E":
+        scene = config_e()
+        n_envs = 1
+        workload = ("E: 4M mixed soft/stiff clay (clay-only parity variant), 256^3 grid h=0.005, 8 moving colliders "
+                    "(boxes, spheres, capsules, SDF volume), 25 substeps/env step, replica per GPU")
+    else:
+        n_envs = args.envs
+        scene = config_d(n_envs=n_envs, first_env=weak_first_env(n_envs, rank))
+        workload = ("D: batched write/pinch von Mises firm clay, 16384 particles/env, 32^3 grid/env, "
+                    "25 substeps/env step, per-rank envs")
     gw = GpuWorld(scene, device=local)
     ctx = gw.ctx
     setup_s = time.perf_counter() - t_setup
@@ -216,8 +238,15 @@ def run_ours(args):
     l0 = lib.msim_gpu_launches(ctx)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ev0.record(stream)
+    stats = StepStats()
     for _ in range(args.steps):
-        gw.env_step()
+        rep = gw.env_step()
+        # per-env-step statistics exchange (the only collective)
+        st = StepStats(n_part * S, n_envs, rep.cfl_cycles, rep.lost_particles, rep.max_penetration,
+                       rep.max_force_balance_error)
+        st = allreduce_stats(st, device=torch.device("cuda", local)) if world > 1 else st
+        stats.particle_substeps += st.particle_substeps
+        stats.env_steps += st.env_steps
     ev1.record(stream)
     torch.cuda.synchronize()
     barrier()
@@ -252,16 +281,14 @@ def run_ours(args):
     # dominant kernel and its roofline (algorithmic bytes per launch / avg launch time)
     dom = max(kernels, key=lambda k: kernels[k]["total_ms"])
     peak, peak_src = peaks()
-    alg_bytes = {"k_p2g": P2G_BYTES, "k_g2p": G2P_BYTES}
-    per_launch_units = n_part  # one launch processes every particle of the rank once
-    if dom in alg_bytes:
-        dom_bytes = alg_bytes[dom] * per_launch_units
-    else:
-        dom_bytes = None
+    # one k_particles launch = one particle-substep of every particle of the rank
+    dom_bytes = BYTES_PER_PS * n_part if dom == "k_particles" else None
     achieved = dom_bytes / (kernels[dom]["avg_ms"] / 1e3) / 1e9 if dom_bytes else None
+    tpp, tsrc = load_traffic(dom)
+    traffic = args.traffic if args.traffic is not None else (tpp * n_part if tpp else None)
     roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "frac": (achieved / peak) if achieved else None, "traffic": args.traffic,
-                "alg_bytes_per_launch": dom_bytes, "avg_launch_ms": kernels[dom]["avg_ms"],
+                "frac": (achieved / peak) if achieved else None, "traffic": traffic,
+                "traffic_source": tsrc, "alg_bytes_per_launch": dom_bytes, "avg_launch_ms": kernels[dom]["avg_ms"],
                 "share_of_step": kernels[dom]["total_ms"] / kstep / max(step_ms_instr, 1e-9),
                 "peak_source": peak_src}
     path_achieved = value / world * BYTES_PER_PS / 1e9
@@ -312,8 +339,7 @@ def run_ours(args):
             "data": "synthetic (seeded jittered lattices, seeding.hpp algorithm)",
             "env_steps_per_s": env_steps,
             "per_gpu": {"particle_substeps_per_s": value / world, "env_steps_per_s": env_steps / world},
-            "config": {"workload": "D: batched write/pinch von Mises firm clay, 16384 particles/env, 32^3 grid/env, "
-                                   "25 substeps/env step, per-rank envs", "envs_per_gpu": n_envs,
+            "config": {"workload": workload, "envs_per_gpu": n_envs,
                        "particles_per_gpu": n_part, "substeps_per_env_step": S, "dt": scene.dt,
                        "parallelism": f"env-sharded x{world} (no data-path collective)",
                        "l2": "inputs larger than L2 (particle state 2 x %.2f GB)" % (n_part * 112 / 1e9)},
@@ -326,6 +352,7 @@ def run_ours(args):
                     "h2d_bytes_per_step": nb * C.sizeof(abi.Body), "d2h_bytes_per_step": nb * 48 + C.sizeof(rep)},
             "cpu_baseline": cpu,
             "setup_s": setup_s,
+            "stats": {"particle_substeps": stats.particle_substeps, "env_steps": stats.env_steps},
         }
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -340,6 +367,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--envs", type=int, default=1024, help="config-D envs per GPU")
+    ap.add_argument("--config", choices=["D", "E"], default="D", help="workload (SURVEY.md App. B)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--traffic", type=float, default=None, help="ncu dram bytes per launch of the dominant kernel")
     args = ap.parse_args()

@@ -105,8 +105,8 @@ enum KernelId : int {
 };
 inline const char* kernel_name(int id) {
   static const char* names[kKernelIds] = {"k_plan", "k_vmax", "k_clear", "k_bin", "bucket_scan", "k_scatter",
-                                          "k_p2g", "block_scan", "k_grid", "k_g2p", "k_cycle_end",
-                                          "k_rigid", "k_stage", "p2g_redo"};
+                                          "k_particles", "block_scan", "k_grid", "k_g2p", "k_iter_end",
+                                          "k_iter_begin", "k_stage", "p2g_redo"};
   return id >= 0 && id < kKernelIds ? names[id] : "?";
 }
 struct KernelTimer {

@@ -1,0 +1,62 @@
+"""Multi-GPU plumbing: one process per GPU, environments sharded across ranks,
+one collective per env step for the step statistics.
+
+Environments are independent worlds (shell.hpp:392-397): no halo,
+no particle migration, so the data path has no collective. The only exchange
+is the per-env-step stats vector (particle-substeps, CFL cycles, lost
+particles, max penetration, max force-balance error), all-reduced with NCCL
+over NVLink on GPU ranks (gloo on CPU for the tests)."""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import torch
+import torch.distributed as dist
+
+
+def shard(n_total: int, rank: int, world: int) -> tuple[int, int]:
+    """Contiguous env range [lo, hi) of a rank (strong scaling of a fixed batch)."""
+    base, extra = divmod(n_total, world)
+    lo = rank * base + min(rank, extra)
+    return lo, lo + base + (1 if rank < extra else 0)
+
+
+def weak_first_env(n_per_rank: int, rank: int) -> int:
+    """First global env id of a rank when every rank owns n_per_rank envs (weak scaling)."""
+    return rank * n_per_rank
+
+
+@dataclass
+class StepStats:
+    particle_substeps: float = 0.0
+    env_steps: float = 0.0
+    cfl_cycles: float = 0.0
+    lost_particles: float = 0.0
+    max_penetration: float = 0.0
+    max_force_balance_error: float = 0.0
+
+    @classmethod
+    def from_reports(cls, reports, particles_per_env, substeps):
+        s = cls()
+        for r, n in zip(reports, particles_per_env):
+            s.particle_substeps += n * substeps
+            s.env_steps += 1
+            s.cfl_cycles += r.cfl_cycles
+            s.lost_particles += r.lost_particles
+            s.max_penetration = max(s.max_penetration, r.max_penetration)
+            s.max_force_balance_error = max(s.max_force_balance_error, r.max_force_balance_error)
+        return s
+
+
+def allreduce_stats(s: StepStats, device=None) -> StepStats:
+    """Sum the counters and max the diagnostics over all ranks (2 tiny collectives)."""
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return s
+    dev = device if device is not None else ("cuda" if dist.get_backend() == "nccl" else "cpu")
+    sums = torch.tensor([s.particle_substeps, s.env_steps, s.cfl_cycles, s.lost_particles], dtype=torch.float64,
+                        device=dev)
+    maxs = torch.tensor([s.max_penetration, s.max_force_balance_error], dtype=torch.float64, device=dev)
+    dist.all_reduce(sums, op=dist.ReduceOp.SUM)
+    dist.all_reduce(maxs, op=dist.ReduceOp.MAX)
+    a, b = sums.tolist(), maxs.tolist()
+    return StepStats(a[0], a[1], a[2], a[3], b[0], b[1])
