@@ -182,11 +182,13 @@ _SIGS = {
 _lib = None
 
 
-def load(path: str = LIB_PATH) -> C.CDLL:
-    """Load libmsim_gpu.so (raises if it is missing: there is no fallback)."""
+def load(path: str | None = None) -> C.CDLL:
+    """Load libmsim_gpu.so (raises if it is missing: there is no fallback).
+    MSIM_GPU_LIB overrides the path (profiling builds of the same sources)."""
     global _lib
     if _lib is not None:
         return _lib
+    path = path or os.environ.get("MSIM_GPU_LIB", LIB_PATH)
     if not os.path.exists(path):
         raise ImportError(
             f"{path} not found: build the CUDA library first (python -c 'import __graft_entry__ as g; g.build()')"

@@ -122,7 +122,13 @@ __device__ __forceinline__ void hencky_frame(const float* G, float* U, float* ep
   float e02 = G[2] + G[6] + (G[0] * G[6] + G[1] * G[7] + G[2] * G[8]);
   float e12 = G[5] + G[7] + (G[3] * G[6] + G[4] * G[7] + G[5] * G[8]);
   float d[3];
+#ifdef MSIM_ABLATE_EIGEN  // profiling-only build: frame = identity (wrong physics)
+  d[0] = e00; d[1] = e11; d[2] = e22;
+  for (int i = 0; i < 9; ++i) U[i] = (i % 4 == 0) ? 1.0f : 0.0f;
+  (void)e01; (void)e02; (void)e12;
+#else
   sym_eigen3(e00, e11, e22, e01, e02, e12, d, U);
+#endif
 #pragma unroll
   for (int i = 0; i < 3; ++i) eps[i] = 0.5f * log1pf(fmaxf(d[i], -0.99999994f));
 }

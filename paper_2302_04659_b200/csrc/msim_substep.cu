@@ -39,6 +39,8 @@
 // force apart (7 channels) like MpmGrid.
 #include <cuda_runtime.h>
 
+#include <cuda_pipeline.h>
+
 #include <cfloat>
 
 #include "msim_common.cuh"
@@ -52,16 +54,28 @@ constexpr int kT = 128;    // threads per CTA (particle kernel), 4 CTAs per SM
 constexpr int kNW = kT / 32;
 constexpr int kCap = 256;  // particles staged per round
 constexpr int GX = kBX + 2, GY = kBY + 2, GZ = kBZ + 2, GN = GX * GY * GZ;  // G2P velocity tile
-constexpr int PX = kBX + 4, PY = kBY + 4, PZ = kBZ + 4, PN = PX * PY * PZ;  // P2G node tile (origin o-1)
+constexpr int PX = kBX + 4, PY = kBY + 4, PZ = kBZ + 4;  // P2G node tile (origin o-1)
+// z-layer stride padded from 64 to 68 words: the 32 base cells of a bucket then
+// hit 32 distinct shared-memory banks for every stencil offset (searched offline)
+constexpr int kTZS = PX * PY + 4;
+constexpr int PN = PZ * kTZS;
 constexpr int CX = kBX + 2, CY = kBY + 2, CZ = kBZ + 2, CN = CX * CY * CZ;  // P2G base cells (origin o-1)
-constexpr int kPay = 36;   // staged P2G payload floats per particle (9 x float4)
+template <int NCH> constexpr int pay_floats() { return NCH == 4 ? 24 : 32; }  // staged P2G payload
+#ifdef MSIM_ABLATE_PREFETCH  // profiling-only build: no cp.async staging of the next bucket
+constexpr bool kPrefetch = false;
+#else
+constexpr bool kPrefetch = true;
+#endif
+constexpr int kInF = 16;   // prefetched particle fields: x[3], G[9], mass, V0, meta, pid
 constexpr int kWs = kMaxBodiesPerEnv * 6 + 3;
 
 template <int NCH>
 struct Smem {
   float4 gtile[GN];
   int itile[NCH][PN];      // fixed-point node accumulators (native int shared atomics)
-  float pay[kCap][kPay];
+  float4 pay[pay_floats<NCH>() / 4][kCap];  // float4 k of slot t at pay[k][t]: conflict-free
+  float inbuf[kInF][kCap]; // next bucket's particles, staged with cp.async (LDGSTS) one item ahead
+  int nperm[kCap];         // next bucket's perm indices (cp.async, issued at the start of this bucket)
   int cellof[kCap];        // local P2G cell of each staged slot, -1 if not staged
   double wsum[kWs];
   unsigned penmax;
@@ -106,6 +120,15 @@ __device__ __forceinline__ float warp_sum(float v) {
   return v;
 }
 
+__device__ __forceinline__ int gcd_i(int a, int b) {
+  while (b) {
+    const int t = a % b;
+    a = b;
+    b = t;
+  }
+  return a;
+}
+
 // Round-to-nearest float -> int for |x| < 2^22 with one FFMA-able add: the
 // integer lands in the low mantissa bits of x + 1.5 * 2^23 (avoids F2I).
 __device__ __forceinline__ int fix_rn(float x) { return __float_as_int(x + 12582912.0f) - 0x4B400000; }
@@ -145,7 +168,60 @@ __global__ void __launch_bounds__(kT, 4) k_particles(SimParams P) {
 
   for (int t = tid; t < NCH * PN; t += kT) (&S.itile[0][0])[t] = 0;
 
+  // Software pipeline over this CTA's buckets: the first round of bucket k+1 is
+  // copied global -> shared (cp.async, one 4-byte LDGSTS per field) while bucket
+  // k scatters and flushes; its perm indices are loaded one bucket earlier still.
+  // Each thread copies only its own slots t = q kT + tid, so a cp.async wait
+  // (no barrier) makes nperm[t] visible to the thread that consumes it.
+  constexpr int kSlots = kCap / kT;
+  auto fetch_perm = [&](int ns, int nrn) {
+#pragma unroll
+    for (int q = 0; q < kSlots; ++q) {
+      const int t = q * kT + tid;
+      if (t < nrn) __pipeline_memcpy_async(&S.nperm[t], &P.perm[ns + t], 4);
+    }
+    __pipeline_commit();
+  };
+  auto fetch_fields = [&](int nrn) {  // call after the perm group landed
+#pragma unroll
+    for (int q = 0; q < kSlots; ++q) {
+      const int t = q * kT + tid;
+      if (t >= nrn) continue;
+      const int i = S.nperm[t];
+#pragma unroll
+      for (int a = 0; a < 3; ++a) __pipeline_memcpy_async(&S.inbuf[a][t], &P.cur.x[a][i], 4);
+#pragma unroll
+      for (int k = 0; k < 9; ++k) __pipeline_memcpy_async(&S.inbuf[3 + k][t], &P.cur.G[k][i], 4);
+      __pipeline_memcpy_async(&S.inbuf[12][t], &P.cur.mass[i], 4);
+      __pipeline_memcpy_async(&S.inbuf[13][t], &P.cur.vol0[i], 4);
+      __pipeline_memcpy_async(&S.inbuf[14][t], &P.cur.meta[i], 4);
+      __pipeline_memcpy_async(&S.inbuf[15][t], &P.cur.pid[i], 4);
+    }
+    __pipeline_commit();
+  };
+  int pf_item = -1;
+  if (kPrefetch && !redo && (int)blockIdx.x < nitems) {
+    const int k0 = P.active_buckets[blockIdx.x];
+    const int s0p = P.bucket_start[k0], n0p = min(kCap, P.bucket_start[k0 + 1] - s0p);
+    fetch_perm(s0p, n0p);
+    __pipeline_wait_prior(0);
+    fetch_fields(n0p);
+    pf_item = blockIdx.x;
+  }
+
   for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
+    // perm indices of this CTA's next bucket: copied now, consumed after this
+    // bucket's per-particle phase to launch the copy of its particle fields
+    const int nxt = item + (int)gridDim.x;
+    const bool pf_next = kPrefetch && !redo && nxt < nitems;
+    int n_rn = 0;
+    if (pf_next) {
+      const int nk = P.active_buckets[nxt];
+      const int n_s = P.bucket_start[nk];
+      n_rn = min(kCap, P.bucket_start[nk + 1] - n_s);
+      fetch_perm(n_s, n_rn);
+    }
+    const bool staged_in = pf_item == item;
     const int key = P.active_buckets[item];
     const bool lostb = key == P.n_keys - 1;
     const int benv = lostb ? 0 : key / P.blocks_per_env;
@@ -176,6 +252,10 @@ __global__ void __launch_bounds__(kT, 4) k_particles(SimParams P) {
     if (penalty && !redo)
       for (int t = tid; t < kWs; t += kT) S.wsum[t] = 0.0;
     if (tid == 0) S.penmax = 0u;
+    if (staged_in) {  // this bucket's fields landed (the perm group just issued may still fly)
+      if (pf_next) __pipeline_wait_prior(1);
+      else __pipeline_wait_prior(0);
+    }
     __syncthreads();
 
     for (int r0 = s; r0 < e; r0 += kCap) {
@@ -188,8 +268,9 @@ __global__ void __launch_bounds__(kT, 4) k_particles(SimParams P) {
         const int t = trip * kT + tid;
         const bool valid = t < rn;
         const int j = r0 + t;
-        const int i = valid ? P.perm[j] : 0;
-        unsigned meta = valid ? P.cur.meta[i] : (1u << kLostBit);
+        const bool from_smem = staged_in && r0 == s;  // CTA-uniform
+        const int i = (valid && !from_smem) ? P.perm[j] : 0;
+        unsigned meta = valid ? (from_smem ? __float_as_uint(S.inbuf[14][t]) : P.cur.meta[i]) : (1u << kLostBit);
         const int penv = (meta >> 8) & kEnvMask;
         const bool was_lost = meta >> kLostBit;
         const int pact = lostb ? (valid ? P.run[penv].action : kActIdle) : act;
@@ -197,7 +278,14 @@ __global__ void __launch_bounds__(kT, 4) k_particles(SimParams P) {
         float G[9], Cm[9];
         float m = 0.f, V0 = 0.f;
         int pid = 0;
-        if (valid) {
+        if (valid && from_smem) {
+          x = {S.inbuf[0][t], S.inbuf[1][t], S.inbuf[2][t]};
+#pragma unroll
+          for (int k = 0; k < 9; ++k) G[k] = S.inbuf[3 + k][t];
+          m = S.inbuf[12][t];
+          V0 = S.inbuf[13][t];
+          pid = __float_as_int(S.inbuf[15][t]);
+        } else if (valid) {
           x = load3(P.cur.x, i);
 #pragma unroll
           for (int k = 0; k < 9; ++k) G[k] = P.cur.G[k][i];
@@ -210,9 +298,10 @@ __global__ void __launch_bounds__(kT, 4) k_particles(SimParams P) {
         }
         const bool read_vc = valid && (lostb || !do_g2p);
         if (read_vc) {
-          v = load3(P.cur.v, i);
+          const int iv = from_smem ? P.perm[j] : i;  // rare actions (first P2G of a call, lost bucket)
+          v = load3(P.cur.v, iv);
 #pragma unroll
-          for (int k = 0; k < 9; ++k) Cm[k] = P.cur.C[k][i];
+          for (int k = 0; k < 9; ++k) Cm[k] = P.cur.C[k][iv];
         } else {
 #pragma unroll
           for (int k = 0; k < 9; ++k) Cm[k] = 0.f;
@@ -234,6 +323,9 @@ __global__ void __launch_bounds__(kT, 4) k_particles(SimParams P) {
           bspline_w(fx[1], wy);
           bspline_w(fx[2], wz);
           f3 vs = {0.f, 0.f, 0.f}, Sx = {0.f, 0.f, 0.f}, Sy = {0.f, 0.f, 0.f}, Sz = {0.f, 0.f, 0.f};
+#ifdef MSIM_ABLATE_G2P  // profiling-only build: no grid gather (lx >= 0 always)
+          if (lx < 0)
+#endif
 #pragma unroll
           for (int dk = 0; dk < 3; ++dk)
 #pragma unroll
@@ -381,18 +473,17 @@ __global__ void __launch_bounds__(kT, 4) k_particles(SimParams P) {
           const int lx = b2[0] - (ox - 1), ly = b2[1] - (oy - 1), lz = b2[2] - (oz - 1);
           if (lx >= 0 && ly >= 0 && lz >= 0 && lx < CX && ly < CY && lz < CZ) {
             cell = (lz * CY + ly) * CX + lx;
-            float4* p4 = reinterpret_cast<float4*>(S.pay[t]);
             // [m wx0 wx1 wx2] [wy0 wy1 wy2 wz0] [wz1 wz2 b.x b.y] [b.z A00 A01 A02] [A10 A11 A12 A20]
             // [A21 A22 bf.x bf.y] [bf.z Af00 Af01 Af02] [Af11 Af12 Af22 -]   (Af symmetric)
-            p4[0] = make_float4(m, w9[0], w9[1], w9[2]);
-            p4[1] = make_float4(w9[3], w9[4], w9[5], w9[6]);
-            p4[2] = make_float4(w9[7], w9[8], bb.x, bb.y);
-            p4[3] = make_float4(bb.z, A[0], A[1], A[2]);
-            p4[4] = make_float4(A[3], A[4], A[5], A[6]);
-            p4[5] = make_float4(A[7], A[8], bf.x, bf.y);
-            if (NCH == 7) {
-              p4[6] = make_float4(bf.z, Af[0], Af[1], Af[2]);
-              p4[7] = make_float4(Af[4], Af[5], Af[8], 0.f);
+            S.pay[0][t] = make_float4(m, w9[0], w9[1], w9[2]);
+            S.pay[1][t] = make_float4(w9[3], w9[4], w9[5], w9[6]);
+            S.pay[2][t] = make_float4(w9[7], w9[8], bb.x, bb.y);
+            S.pay[3][t] = make_float4(bb.z, A[0], A[1], A[2]);
+            S.pay[4][t] = make_float4(A[3], A[4], A[5], A[6]);
+            S.pay[5][t] = make_float4(A[7], A[8], bf.x, bf.y);
+            if constexpr (NCH == 7) {
+              S.pay[6][t] = make_float4(bf.z, Af[0], Af[1], Af[2]);
+              S.pay[7][t] = make_float4(Af[4], Af[5], Af[8], 0.f);
             }
             staged = true;
             // bounds of |b + A off| over off in {0,1,2}^3 for the fixed-point scales
@@ -450,10 +541,13 @@ __global__ void __launch_bounds__(kT, 4) k_particles(SimParams P) {
           }
         }
       }
-      if (!do_p2g) {
-        __syncthreads();
-        continue;
+      __syncthreads();  // inbuf consumed: start copying the next bucket behind this one's scatter
+      if (r0 == s && pf_next) {
+        __pipeline_wait_prior(0);
+        fetch_fields(n_rn);
+        pf_item = nxt;
       }
+      if (!do_p2g) continue;
       // fixed-point scales of this round: |node sum| <= rn * max bound < 2^30 / scale
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) {
@@ -476,24 +570,29 @@ __global__ void __launch_bounds__(kT, 4) k_particles(SimParams P) {
         const float sc_m = bm > 0.f ? 4194304.0f / bm : 0.f;
         const float sc_p = bpm > 0.f ? 4194304.0f / bpm : 0.f;
         const float sc_f = bfm > 0.f ? 4194304.0f / bfm : 0.f;
-        // Lane-strided slots: the 32 lanes of a warp take slots 8 apart, i.e. particles
-        // spread over the whole bucket, so their stencils rarely share a node (the
-        // staged order follows the particles' spatial order, neighbours share cells).
-        constexpr int kStride = kCap / 32;
-#pragma unroll
-        for (int q = 0; q < kStride / kNW; ++q) {
-          const int t = lane * kStride + warp * (kStride / kNW) + q;
-          const int c = t < rn ? S.cellof[t] : -1;
+        // Golden-ratio spread: consecutive lanes take staged slots ~0.618 rn apart
+        // (odd, coprime with rn: a bijection on [0, rn)), i.e. particles spread over
+        // the whole bucket, so a warp's 27-node stencils rarely share a node (staged
+        // order follows the particles' spatial order, neighbours share cells).
+        // The payload reads pay[k][t] stay free of bank conflicts (odd g: t distinct mod 8).
+        int g = ((int)(0.618034f * (float)rn)) | 1;
+        while (gcd_i(g, rn) != 1) g += 2;
+        for (int u = tid; u < rn; u += kT) {
+          const int t = (int)(((long long)u * g) % rn);
+          const int c = S.cellof[t];
           if (c < 0) continue;
-          const float4* p4 = reinterpret_cast<const float4*>(S.pay[t]);
-          const float4 q0 = p4[0], q1 = p4[1], q2 = p4[2], q3 = p4[3], q4 = p4[4], q5 = p4[5];
+#ifdef MSIM_ABLATE_SCATTER  // profiling-only build: no shared atomics
+          if (c >= 0) continue;
+#endif
+          const float4 q0 = S.pay[0][t], q1 = S.pay[1][t], q2 = S.pay[2][t], q3 = S.pay[3][t], q4 = S.pay[4][t],
+                       q5 = S.pay[5][t];
           const float wx[3] = {q0.y, q0.z, q0.w}, wy[3] = {q1.x, q1.y, q1.z}, wz[3] = {q1.w, q2.x, q2.y};
           const float ms = q0.x * sc_m;
           // A row-major: A00 q3.y A01 q3.z A02 q3.w A10 q4.x A11 q4.y A12 q4.z A20 q4.w A21 q5.x A22 q5.y
           float4 qf6 = make_float4(0.f, 0.f, 0.f, 0.f), qf7 = qf6;
-          if (NCH == 7) {
-            qf6 = p4[6];
-            qf7 = p4[7];
+          if constexpr (NCH == 7) {
+            qf6 = S.pay[6][t];
+            qf7 = S.pay[7][t];
           }
           const int cx = c % CX, cy = (c / CX) % CY, cz = c / (CX * CY);
 #pragma unroll
@@ -510,7 +609,7 @@ __global__ void __launch_bounds__(kT, 4) k_particles(SimParams P) {
                 fyr = q5.w + qf7.x * dj + qf7.y * dk;  // bf.y + Af11 dj + Af12 dk
                 fzr = qf6.x + qf7.y * dj + qf7.z * dk; // bf.z + Af12 dj + Af22 dk
               }
-              const int nt = ((cz + dk) * PY + (cy + dj)) * PX + cx;
+              const int nt = (cz + dk) * kTZS + (cy + dj) * PX + cx;
 #pragma unroll
               for (int di = 0; di < 3; ++di) {
                 const float w = wyz * wx[di];
@@ -542,8 +641,8 @@ __global__ void __launch_bounds__(kT, 4) k_particles(SimParams P) {
         for (int q = 0; q < NCH; ++q) qs[q] = sc[q] > 0.f ? 1.0f / sc[q] : 0.f;
         for (int t = tid; t < PN; t += kT) {
           const int im = S.itile[3][t];
-          if (im != 0) {
-            const int lx = t % PX, ly = (t / PX) % PY, lz = t / (PX * PY);
+          if (im != 0) {  // (the 4 padding words per z-layer are never written)
+            const int lz = t / kTZS, rem = t - lz * kTZS, ly = rem / PX, lx = rem - ly * PX;
             const int gx = ox - 1 + lx, gy = oy - 1 + ly, gz = oz - 1 + lz;
             if (gx >= 0 && gy >= 0 && gz >= 0 && gx < P.dims[0] && gy < P.dims[1] && gz < P.dims[2]) {
               const long long gi = benv * P.nodes_per_env + ((long long)gz * P.dims[1] + gy) * P.dims[0] + gx;
