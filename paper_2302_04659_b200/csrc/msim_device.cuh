@@ -111,23 +111,52 @@ __device__ __forceinline__ float det_I_plus(const float* G) {
   return 1.0f + tr + m2 + dg;
 }
 
+// Symmetric 3x3 {a00, a11, a22, a01, a02, a12}.
+struct Sym {
+  float a00, a11, a22, a01, a02, a12;
+};
+// A B for symmetric A, B that commute (polynomials of one matrix): the
+// product is symmetric, so only its upper triangle is formed (18 FMA).
+__device__ __forceinline__ Sym sym_mul(const Sym& A, const Sym& B) {
+  return {A.a00 * B.a00 + A.a01 * B.a01 + A.a02 * B.a02, A.a01 * B.a01 + A.a11 * B.a11 + A.a12 * B.a12,
+          A.a02 * B.a02 + A.a12 * B.a12 + A.a22 * B.a22, A.a00 * B.a01 + A.a01 * B.a11 + A.a02 * B.a12,
+          A.a00 * B.a02 + A.a01 * B.a12 + A.a02 * B.a22, A.a01 * B.a02 + A.a11 * B.a12 + A.a12 * B.a22};
+}
+// A B + c I
+__device__ __forceinline__ Sym sym_mul_add_id(const Sym& A, const Sym& B, float c) {
+  Sym r = sym_mul(A, B);
+  r.a00 += c;
+  r.a11 += c;
+  r.a22 += c;
+  return r;
+}
+__device__ __forceinline__ Sym sym_scale_add_id(const Sym& A, float s, float c) {
+  return {s * A.a00 + c, s * A.a11 + c, s * A.a22 + c, s * A.a01, s * A.a02, s * A.a12};
+}
+__device__ __forceinline__ float sym_norm2(const Sym& A) {
+  return A.a00 * A.a00 + A.a11 * A.a11 + A.a22 * A.a22 + 2.0f * (A.a01 * A.a01 + A.a02 * A.a02 + A.a12 * A.a12);
+}
+
+// E = F F^T - I = G + G^T + G G^T
+__device__ __forceinline__ Sym left_strain(const float* G) {
+  return {2.0f * G[0] + (G[0] * G[0] + G[1] * G[1] + G[2] * G[2]),
+          2.0f * G[4] + (G[3] * G[3] + G[4] * G[4] + G[5] * G[5]),
+          2.0f * G[8] + (G[6] * G[6] + G[7] * G[7] + G[8] * G[8]),
+          G[1] + G[3] + (G[0] * G[3] + G[1] * G[4] + G[2] * G[5]),
+          G[2] + G[6] + (G[0] * G[6] + G[1] * G[7] + G[2] * G[8]),
+          G[5] + G[7] + (G[3] * G[6] + G[4] * G[7] + G[5] * G[8])};
+}
+
 // Left principal frame of F = I + G: U (columns) and Hencky strains
 // eps_i = log(sigma_i) = 0.5*log1p(e_i), e = eig(F F^T - I).
 __device__ __forceinline__ void hencky_frame(const float* G, float* U, float* eps) {
-  // E = G + G^T + G G^T
-  float e00 = 2.0f * G[0] + (G[0] * G[0] + G[1] * G[1] + G[2] * G[2]);
-  float e11 = 2.0f * G[4] + (G[3] * G[3] + G[4] * G[4] + G[5] * G[5]);
-  float e22 = 2.0f * G[8] + (G[6] * G[6] + G[7] * G[7] + G[8] * G[8]);
-  float e01 = G[1] + G[3] + (G[0] * G[3] + G[1] * G[4] + G[2] * G[5]);
-  float e02 = G[2] + G[6] + (G[0] * G[6] + G[1] * G[7] + G[2] * G[8]);
-  float e12 = G[5] + G[7] + (G[3] * G[6] + G[4] * G[7] + G[5] * G[8]);
+  const Sym E = left_strain(G);
   float d[3];
 #ifdef MSIM_ABLATE_EIGEN  // profiling-only build: frame = identity (wrong physics)
-  d[0] = e00; d[1] = e11; d[2] = e22;
+  d[0] = E.a00; d[1] = E.a11; d[2] = E.a22;
   for (int i = 0; i < 9; ++i) U[i] = (i % 4 == 0) ? 1.0f : 0.0f;
-  (void)e01; (void)e02; (void)e12;
 #else
-  sym_eigen3(e00, e11, e22, e01, e02, e12, d, U);
+  sym_eigen3(E.a00, E.a11, E.a22, E.a01, E.a02, E.a12, d, U);
 #endif
 #pragma unroll
   for (int i = 0; i < 3; ++i) eps[i] = 0.5f * log1pf(fmaxf(d[i], -0.99999994f));
@@ -146,44 +175,104 @@ __device__ __forceinline__ void sym_from_frame(const float* U, const float* s, f
     }
 }
 
-// Kirchhoff stress tau = U diag(2 mu eps + lambda tr eps) U^T (mpm.hpp:152-161).
-__device__ __forceinline__ void kirchhoff_from_frame(const float* U, const float* eps,
-                                                     const MatParams& m, float* tau) {
-  float tr = eps[0] + eps[1] + eps[2];
-  float p[3] = {m.two_mu * eps[0] + m.lambda * tr, m.two_mu * eps[1] + m.lambda * tr,
-                m.two_mu * eps[2] + m.lambda * tr};
-  sym_from_frame(U, p, tau);
+// Hencky strain TENSOR eps = 0.5 log(F F^T) = 0.5 log1p(E) in the spatial
+// frame, i.e. U diag(log sigma) U^T, as a matrix function instead of an
+// eigen-decomposition: with Z = E (2I + E)^-1 (eigenvalues z = e / (2 + e)),
+//   0.5 log1p(e) = atanh(z) = z + z^3/3 + z^5/5 + ...,
+// summed to z^11 by Horner in Z^2. Every factor is a polynomial in E, so all
+// products commute and stay symmetric. For ||Z||_F <= 1/4 the truncation is
+// below 2e-9 absolute (strains of |e| <~ 0.6, i.e. every elastic state of the
+// clays, whose yield caps the deviatoric strain at 0.04-0.2); larger strains
+// take the cyclic-Jacobi frame. Same function of F as the reference's
+// SVD-based log(sigma) (mpm.hpp:152-161), to fp32 rounding relative to the strain.
+__device__ __forceinline__ Sym hencky_strain(const float* G) {
+  const Sym E = left_strain(G);
+  const Sym B = {2.0f + E.a00, 2.0f + E.a11, 2.0f + E.a22, E.a01, E.a02, E.a12};
+  const Sym Cf = {B.a11 * B.a22 - B.a12 * B.a12, B.a00 * B.a22 - B.a02 * B.a02, B.a00 * B.a11 - B.a01 * B.a01,
+                  B.a02 * B.a12 - B.a01 * B.a22, B.a01 * B.a12 - B.a02 * B.a11, B.a01 * B.a02 - B.a00 * B.a12};
+  const float inv_det = 1.0f / (B.a00 * Cf.a00 + B.a01 * Cf.a01 + B.a02 * Cf.a02);  // det B >= 1
+  Sym Z = sym_mul(E, Cf);
+  Z = sym_scale_add_id(Z, inv_det, 0.0f);
+#ifndef MSIM_ABLATE_EIGEN
+  if (sym_norm2(Z) <= 0.0625f) {
+#endif
+    const Sym W = sym_mul(Z, Z);
+    Sym q = sym_scale_add_id(W, 1.0f / 11.0f, 1.0f / 9.0f);
+    q = sym_mul_add_id(W, q, 1.0f / 7.0f);
+    q = sym_mul_add_id(W, q, 1.0f / 5.0f);
+    q = sym_mul_add_id(W, q, 1.0f / 3.0f);
+    q = sym_mul_add_id(W, q, 1.0f);
+    return sym_mul(Z, q);
+#ifndef MSIM_ABLATE_EIGEN
+  }
+  float U[9], e[3], S[9];
+  hencky_frame(G, U, e);
+  sym_from_frame(U, e, S);
+  return {S[0], S[4], S[8], S[1], S[2], S[5]};
+#endif
 }
 
-// Von Mises radial return (mpm.hpp:166-181) applied to the displacement
-// gradient in place. Returns true if the state yielded. eps is updated to
-// the projected strains (the principal frame U is unchanged), so the caller
-// can form the next Kirchhoff stress without another decomposition.
-__device__ __forceinline__ bool von_mises_project(float* G, const float* U, float* eps,
-                                                  const MatParams& m) {
-  float mean = (eps[0] + eps[1] + eps[2]) * (1.0f / 3.0f);
-  float dev[3] = {eps[0] - mean, eps[1] - mean, eps[2] - mean};
-  float dev_norm = sqrtf(dev[0] * dev[0] + dev[1] * dev[1] + dev[2] * dev[2]);
-  float sdn = m.two_mu * dev_norm;
-  if (sdn <= m.yield_thr) return false;
-  float k = m.yield_thr / sdn;
-  float sm1[3];
-#pragma unroll
-  for (int i = 0; i < 3; ++i) {
-    float e_new = mean + dev[i] * k;
-    sm1[i] = expm1f(e_new - eps[i]);  // sigma'/sigma - 1
-    eps[i] = e_new;
+// expm1 of a symmetric matrix: Taylor to M^7 / 7! on M / 2^s with
+// ||M / 2^s||_F <= 1/4, then s doublings X <- X (2I + X), i.e.
+// exp(2A) - I = (exp(A) - I)(exp(A) + I): no cancellation against I.
+__device__ __forceinline__ Sym sym_expm1(Sym M) {
+  const float n2 = sym_norm2(M);
+  int s = 0;
+  if (n2 > 0.0625f) {
+    s = (int)ceilf(0.5f * log2f(n2 * 16.0f));
+    const float sc = exp2f((float)-s);
+    M = sym_scale_add_id(M, sc, 0.0f);
   }
-  // F' = U diag(s) U^T F  =>  G' = (S - I)(I + G) + G
-  float Sm[9];
-  sym_from_frame(U, sm1, Sm);
+  Sym q = sym_scale_add_id(M, 1.0f / 5040.0f, 1.0f / 720.0f);
+  q = sym_mul_add_id(M, q, 1.0f / 120.0f);
+  q = sym_mul_add_id(M, q, 1.0f / 24.0f);
+  q = sym_mul_add_id(M, q, 1.0f / 6.0f);
+  q = sym_mul_add_id(M, q, 0.5f);
+  q = sym_mul_add_id(M, q, 1.0f);
+  Sym X = sym_mul(M, q);
+  for (int i = 0; i < s; ++i) {
+    const Sym X2 = sym_mul(X, X);
+    X = {2.0f * X.a00 + X2.a00, 2.0f * X.a11 + X2.a11, 2.0f * X.a22 + X2.a22,
+         2.0f * X.a01 + X2.a01, 2.0f * X.a02 + X2.a02, 2.0f * X.a12 + X2.a12};
+  }
+  return X;
+}
+
+// Kirchhoff stress tau = 2 mu eps + lambda tr(eps) I (mpm.hpp:152-161: the
+// principal-frame formula U diag(2 mu eps_i + lambda tr) U^T as a tensor).
+__device__ __forceinline__ void kirchhoff_from_strain(const Sym& eps, const MatParams& m, float* tau) {
+  const float lt = m.lambda * (eps.a00 + eps.a11 + eps.a22);
+  tau[0] = m.two_mu * eps.a00 + lt;
+  tau[4] = m.two_mu * eps.a11 + lt;
+  tau[8] = m.two_mu * eps.a22 + lt;
+  tau[1] = tau[3] = m.two_mu * eps.a01;
+  tau[2] = tau[6] = m.two_mu * eps.a02;
+  tau[5] = tau[7] = m.two_mu * eps.a12;
+}
+
+// Von Mises radial return (mpm.hpp:166-181) on the strain tensor: with
+// dev = eps - tr(eps)/3 I and k = thr / (2 mu |dev|) < 1 the projected
+// strain is eps + (k - 1) dev, and F' = exp((k - 1) dev) F (the reference's
+// U diag(sigma') V^T), applied to G in place as G' = G + X + X G with
+// X = expm1((k - 1) dev). eps is updated so the caller forms the next
+// Kirchhoff stress without another decomposition. Returns true if yielded.
+__device__ __forceinline__ bool von_mises_project_strain(float* G, Sym& eps, const MatParams& m) {
+  const float mean = (eps.a00 + eps.a11 + eps.a22) * (1.0f / 3.0f);
+  const Sym dev = {eps.a00 - mean, eps.a11 - mean, eps.a22 - mean, eps.a01, eps.a02, eps.a12};
+  const float sdn = m.two_mu * sqrtf(sym_norm2(dev));
+  if (sdn <= m.yield_thr) return false;
+  const float km1 = m.yield_thr / sdn - 1.0f;
+  const Sym M = sym_scale_add_id(dev, km1, 0.0f);
+  eps = {eps.a00 + M.a00, eps.a11 + M.a11, eps.a22 + M.a22, eps.a01 + M.a01, eps.a02 + M.a02, eps.a12 + M.a12};
+  const Sym X = sym_expm1(M);
+  const float Xm[9] = {X.a00, X.a01, X.a02, X.a01, X.a11, X.a12, X.a02, X.a12, X.a22};
   float Gn[9];
 #pragma unroll
   for (int r = 0; r < 3; ++r)
 #pragma unroll
     for (int c = 0; c < 3; ++c)
-      Gn[r * 3 + c] = G[r * 3 + c] + Sm[r * 3 + c] + Sm[r * 3 + 0] * G[0 * 3 + c] +
-                      Sm[r * 3 + 1] * G[1 * 3 + c] + Sm[r * 3 + 2] * G[2 * 3 + c];
+      Gn[r * 3 + c] = G[r * 3 + c] + Xm[r * 3 + c] + Xm[r * 3 + 0] * G[0 * 3 + c] + Xm[r * 3 + 1] * G[1 * 3 + c] +
+                      Xm[r * 3 + 2] * G[2 * 3 + c];
 #pragma unroll
   for (int i = 0; i < 9; ++i) G[i] = Gn[i];
   return true;

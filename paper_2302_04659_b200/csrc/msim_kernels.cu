@@ -246,15 +246,14 @@ __global__ void k_constitutive(MatParams m, long long n, const double* F, double
     atomicOr(bad, 1);
     return;
   }
-  float U[9], eps[3];
-  hencky_frame(G, U, eps);
+  Sym eps = hencky_strain(G);
   if (tau) {
     float t[9];
-    kirchhoff_from_frame(U, eps, m, t);
+    kirchhoff_from_strain(eps, m, t);
     for (int k = 0; k < 9; ++k) tau[9 * i + k] = t[k];
   }
   if (Fp) {
-    von_mises_project(G, U, eps, m);
+    von_mises_project_strain(G, eps, m);
     for (int k = 0; k < 9; ++k) Fp[9 * i + k] = (double)G[k] + ((k % 4 == 0) ? 1.0 : 0.0);
   }
 }

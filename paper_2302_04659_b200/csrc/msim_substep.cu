@@ -120,14 +120,21 @@ __device__ __forceinline__ float warp_sum(float v) {
   return v;
 }
 
-__device__ __forceinline__ int gcd_i(int a, int b) {
-  while (b) {
-    const int t = a % b;
-    a = b;
-    b = t;
+constexpr int gcd_c(int a, int b) { return b ? gcd_c(b, a % b) : a; }
+// Scatter slot stride per round size rn: odd, coprime with rn, ~0.618 rn (see k_particles)
+struct SpreadTable {
+  unsigned char g[kCap + 1];
+};
+constexpr SpreadTable make_spread() {
+  SpreadTable t{};
+  for (int rn = 1; rn <= kCap; ++rn) {
+    int g = ((int)(0.618034 * rn)) | 1;
+    while (gcd_c(g, rn) != 1) g += 2;
+    t.g[rn] = (unsigned char)g;
   }
-  return a;
+  return t;
 }
+__constant__ SpreadTable kSpread = make_spread();
 
 // Round-to-nearest float -> int for |x| < 2^22 with one FFMA-able add: the
 // integer lands in the low mantissa bits of x + 1.5 * 2^23 (avoids F2I).
@@ -309,7 +316,7 @@ __global__ void __launch_bounds__(kT, 4) k_particles(SimParams P) {
         bool write_vc = valid && (lostb || act != kActFused);
         const bool live = valid && !lostb && !was_lost && act != kActIdle;
         float speed = -1.0f;
-        float U[9], eps[3];
+        Sym eps = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};  // Hencky strain tensor (one evaluation per substep)
         const MatParams mp = P.mats[meta & 0xFFu];
 
         // ---------------- G2P of this cycle (mpm.hpp:346-379)
@@ -358,12 +365,12 @@ __global__ void __launch_bounds__(kT, 4) k_particles(SimParams P) {
                 Gn[r * 3 + c] = G[r * 3 + c] + dt * (Cm[r * 3 + c] + Cm[r * 3 + 0] * G[0 * 3 + c] +
                                                      Cm[r * 3 + 1] * G[1 * 3 + c] + Cm[r * 3 + 2] * G[2 * 3 + c]);
             if (!(det_I_plus(Gn) > 0.0f)) set_error(P, penv, kErrDetReturn, pid);
-            hencky_frame(Gn, U, eps);
-            von_mises_project(Gn, U, eps, mp);
+            eps = hencky_strain(Gn);
+            von_mises_project_strain(Gn, eps, mp);
 #pragma unroll
             for (int k = 0; k < 9; ++k) G[k] = Gn[k];
           } else if (do_p2g) {
-            hencky_frame(G, U, eps);
+            eps = hencky_strain(G);
           }
           bool bad = false;
 #pragma unroll
@@ -375,7 +382,7 @@ __global__ void __launch_bounds__(kT, 4) k_particles(SimParams P) {
           if (!(speed >= 0.0f)) speed = FLT_MAX;
         } else if (live && do_p2g) {
           if (!(det_I_plus(G) > 0.0f)) set_error(P, penv, kErrDetStress, pid);
-          hencky_frame(G, U, eps);
+          eps = hencky_strain(G);
         }
 
         // ---------------- binning of the (new) position + P2G payload of the next cycle
@@ -442,7 +449,7 @@ __global__ void __launch_bounds__(kT, 4) k_particles(SimParams P) {
 
         if (scatter_me) {
           float tau[9];
-          kirchhoff_from_frame(U, eps, mp, tau);
+          kirchhoff_from_strain(eps, mp, tau);
           const float h = P.h_f;
           const float hm = h * m;
           const float hs = -h * P.d_inv_f * V0;  // h * (-(4/h^2) V0): stress -> force matrix
@@ -575,10 +582,10 @@ __global__ void __launch_bounds__(kT, 4) k_particles(SimParams P) {
         // the whole bucket, so a warp's 27-node stencils rarely share a node (staged
         // order follows the particles' spatial order, neighbours share cells).
         // The payload reads pay[k][t] stay free of bank conflicts (odd g: t distinct mod 8).
-        int g = ((int)(0.618034f * (float)rn)) | 1;
-        while (gcd_i(g, rn) != 1) g += 2;
-        for (int u = tid; u < rn; u += kT) {
-          const int t = (int)(((long long)u * g) % rn);
+        const int g = kSpread.g[rn];
+        const int dstep = (kT * g) % rn;
+        int t = tid < rn ? (tid * g) % rn : 0;
+        for (int u = tid; u < rn; u += kT, t = t + dstep >= rn ? t + dstep - rn : t + dstep) {
           const int c = S.cellof[t];
           if (c < 0) continue;
 #ifdef MSIM_ABLATE_SCATTER  // profiling-only build: no shared atomics

@@ -1,9 +1,11 @@
 """Summarise an ncu report: key SOL metrics + top source lines by stall samples.
-Usage: python profiles/ncu_summary.py report.ncu-rep [top_n]"""
+Usage: python profiles/ncu_summary.py report.ncu-rep [top_n] [file:lo-hi=region ...]
+NCU_LAUNCH=i selects the i-th profiled launch of a multi-launch report."""
 import collections
 import csv
 import io
 import subprocess
+import os
 import sys
 
 rep = sys.argv[1]
@@ -11,7 +13,8 @@ top = int(sys.argv[2]) if len(sys.argv) > 2 else 25
 
 
 def run(*a):
-    return subprocess.run(["ncu", "-i", rep, *a], capture_output=True, text=True).stdout
+    sel = ["--launch-skip", os.environ["NCU_LAUNCH"], "--launch-count", "1"] if "NCU_LAUNCH" in os.environ else []
+    return subprocess.run(["ncu", "-i", rep, *sel, *a], capture_output=True, text=True).stdout
 
 
 det = list(csv.reader(io.StringIO(run("--page", "details", "--csv"))))
