@@ -61,11 +61,18 @@ constexpr int kTZS = PX * PY + 4;
 constexpr int PN = PZ * kTZS;
 constexpr int CX = kBX + 2, CY = kBY + 2, CZ = kBZ + 2, CN = CX * CY * CZ;  // P2G base cells (origin o-1)
 template <int NCH> constexpr int pay_floats() { return NCH == 4 ? 24 : 32; }  // staged P2G payload
-#ifdef MSIM_ABLATE_PREFETCH  // profiling-only build: no cp.async staging of the next bucket
-constexpr bool kPrefetch = false;
-#else
+// cp.async staging of the next bucket's particles (variant build): measured
+// neutral on B200 (the 4 co-resident CTAs already overlap the loads), and its
+// 17 KB of shared memory cost a CTA per SM, so the default build leaves it out.
+#ifdef MSIM_PREFETCH
 constexpr bool kPrefetch = true;
+#else
+constexpr bool kPrefetch = false;
 #endif
+#ifndef MSIM_CTAS_PER_SM
+#define MSIM_CTAS_PER_SM 5  // measured: 4 -> 1.12, 5 -> 1.05, 6 -> 1.10 ms per launch (config D, 256 envs)
+#endif
+constexpr int kCtasPerSm = MSIM_CTAS_PER_SM;
 constexpr int kInF = 16;   // prefetched particle fields: x[3], G[9], mass, V0, meta, pid
 constexpr int kWs = kMaxBodiesPerEnv * 6 + 3;
 
@@ -74,8 +81,8 @@ struct Smem {
   float4 gtile[GN];
   int itile[NCH][PN];      // fixed-point node accumulators (native int shared atomics)
   float4 pay[pay_floats<NCH>() / 4][kCap];  // float4 k of slot t at pay[k][t]: conflict-free
-  float inbuf[kInF][kCap]; // next bucket's particles, staged with cp.async (LDGSTS) one item ahead
-  int nperm[kCap];         // next bucket's perm indices (cp.async, issued at the start of this bucket)
+  float inbuf[kPrefetch ? kInF : 1][kPrefetch ? kCap : 1];  // next bucket's particles (cp.async)
+  int nperm[kPrefetch ? kCap : 1];  // next bucket's perm indices (cp.async, issued at this bucket's start)
   int cellof[kCap];        // local P2G cell of each staged slot, -1 if not staged
   double wsum[kWs];
   unsigned penmax;
@@ -164,7 +171,7 @@ __device__ void scatter_global(const SimParams& P, int env, const int* b, const 
 }
 
 template <int NCH>
-__global__ void __launch_bounds__(kT, 4) k_particles(SimParams P) {
+__global__ void __launch_bounds__(kT, kCtasPerSm) k_particles(SimParams P) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Smem<NCH>& S = *reinterpret_cast<Smem<NCH>*>(smem_raw);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -1010,9 +1017,9 @@ struct Timed {
 
 void particle_kernel(const SimParams& P, cudaStream_t s) {
   if (P.split)
-    k_particles<7><<<sm_count() * 4, kT, sizeof(Smem<7>), s>>>(P);
+    k_particles<7><<<sm_count() * kCtasPerSm, kT, sizeof(Smem<7>), s>>>(P);
   else
-    k_particles<4><<<sm_count() * 4, kT, sizeof(Smem<4>), s>>>(P);
+    k_particles<4><<<sm_count() * kCtasPerSm, kT, sizeof(Smem<4>), s>>>(P);
 }
 
 }  // namespace
