@@ -39,8 +39,6 @@
 // force apart (7 channels) like MpmGrid.
 #include <cuda_runtime.h>
 
-#include <cuda_pipeline.h>
-
 #include <cfloat>
 
 #include "msim_common.cuh"
@@ -50,8 +48,7 @@ using namespace msim_dev;
 namespace msim_impl {
 namespace {
 
-constexpr int kT = 128;    // threads per CTA (particle kernel), 4 CTAs per SM
-constexpr int kNW = kT / 32;
+constexpr int kT = 128;    // threads per CTA (particle kernel), kCtasPerSm CTAs per SM
 constexpr int kCap = 256;  // particles staged per round
 constexpr int GX = kBX + 2, GY = kBY + 2, GZ = kBZ + 2, GN = GX * GY * GZ;  // G2P velocity tile
 constexpr int PX = kBX + 4, PY = kBY + 4, PZ = kBZ + 4;  // P2G node tile (origin o-1)
@@ -59,67 +56,35 @@ constexpr int PX = kBX + 4, PY = kBY + 4, PZ = kBZ + 4;  // P2G node tile (origi
 // hit 32 distinct shared-memory banks for every stencil offset (searched offline)
 constexpr int kTZS = PX * PY + 4;
 constexpr int PN = PZ * kTZS;
-constexpr int CX = kBX + 2, CY = kBY + 2, CZ = kBZ + 2, CN = CX * CY * CZ;  // P2G base cells (origin o-1)
+constexpr int CX = kBX + 2, CY = kBY + 2, CZ = kBZ + 2;  // P2G base cells (origin o-1)
 template <int NCH> constexpr int pay_floats() { return NCH == 4 ? 24 : 32; }  // staged P2G payload
-// cp.async staging of the next bucket's particles (variant build): measured
-// neutral on B200 (the 4 co-resident CTAs already overlap the loads), and its
-// 17 KB of shared memory cost a CTA per SM, so the default build leaves it out.
-#ifdef MSIM_PREFETCH
-constexpr bool kPrefetch = true;
-#else
-constexpr bool kPrefetch = false;
-#endif
 #ifndef MSIM_CTAS_PER_SM
 #define MSIM_CTAS_PER_SM 5  // measured: 4 -> 1.12, 5 -> 1.05, 6 -> 1.10 ms per launch (config D, 256 envs)
 #endif
 constexpr int kCtasPerSm = MSIM_CTAS_PER_SM;
-constexpr int kInF = 16;   // prefetched particle fields: x[3], G[9], mass, V0, meta, pid
 constexpr int kWs = kMaxBodiesPerEnv * 6 + 3;
+
+// Bucket-uniform values of k_particles, kept in shared memory and re-read at
+// each use (volatile): held in registers across the per-particle phase they
+// were spilled to local memory (measured 15 % of the executed instructions).
+struct ItemCtx {
+  int key, benv, s, e, act, ox, oy, oz, s0, s1;
+  float dt, dtp;
+  int lostb, do_g2p, do_p2g, penalty;
+};
 
 template <int NCH>
 struct Smem {
   float4 gtile[GN];
   int itile[NCH][PN];      // fixed-point node accumulators (native int shared atomics)
   float4 pay[pay_floats<NCH>() / 4][kCap];  // float4 k of slot t at pay[k][t]: conflict-free
-  float inbuf[kPrefetch ? kInF : 1][kPrefetch ? kCap : 1];  // next bucket's particles (cp.async)
-  int nperm[kPrefetch ? kCap : 1];  // next bucket's perm indices (cp.async, issued at this bucket's start)
   int cellof[kCap];        // local P2G cell of each staged slot, -1 if not staged
   double wsum[kWs];
   unsigned penmax;
   unsigned maxb[3];
-  int scan_ws[kNW];
-  int scan_tot;
+  ItemCtx ic;              // the current bucket's uniform context (read back instead of held in registers)
 };
 
-__device__ __forceinline__ int warp_incl_scan(int v) {
-  const int lane = threadIdx.x & 31;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    int t = __shfl_up_sync(0xffffffffu, v, o);
-    if (lane >= o) v += t;
-  }
-  return v;
-}
-
-// Exclusive scan of one int per thread over the block (kT threads).
-template <class SM>
-__device__ __forceinline__ int block_excl_scan(SM& S, int v, int* total) {
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  int inc = warp_incl_scan(v);
-  if (lane == 31) S.scan_ws[wid] = inc;
-  __syncthreads();
-  if (wid == 0) {
-    int s = lane < kNW ? S.scan_ws[lane] : 0;
-    int si = warp_incl_scan(s);
-    if (lane < kNW) S.scan_ws[lane] = si - s;
-    if (lane == kNW - 1) S.scan_tot = si;
-  }
-  __syncthreads();
-  int r = inc - v + S.scan_ws[wid];
-  *total = S.scan_tot;
-  __syncthreads();
-  return r;
-}
 
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll
@@ -170,110 +135,17 @@ __device__ void scatter_global(const SimParams& P, int env, const int* b, const 
       }
 }
 
+// The rounds of one bucket (<= kCap particles each): per-particle phase, then
+// the fixed-point scatter and flush. Bucket-uniform values come from S.ic.
 template <int NCH>
-__global__ void __launch_bounds__(kT, kCtasPerSm) k_particles(SimParams P) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  Smem<NCH>& S = *reinterpret_cast<Smem<NCH>*>(smem_raw);
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+__device__ __forceinline__ void item_rounds(const SimParams& P, Smem<NCH>& S, bool redo) {
+  const int tid = threadIdx.x, lane = tid & 31;
   const unsigned FULL = 0xffffffffu;
-  const bool redo = P.redo_pass != 0;
-  if (redo && !*P.any_redo) return;
-  const int nitems = *P.n_active_buckets;
+  volatile ItemCtx& IC = S.ic;
+  {
 
-  for (int t = tid; t < NCH * PN; t += kT) (&S.itile[0][0])[t] = 0;
-
-  // Software pipeline over this CTA's buckets: the first round of bucket k+1 is
-  // copied global -> shared (cp.async, one 4-byte LDGSTS per field) while bucket
-  // k scatters and flushes; its perm indices are loaded one bucket earlier still.
-  // Each thread copies only its own slots t = q kT + tid, so a cp.async wait
-  // (no barrier) makes nperm[t] visible to the thread that consumes it.
-  constexpr int kSlots = kCap / kT;
-  auto fetch_perm = [&](int ns, int nrn) {
-#pragma unroll
-    for (int q = 0; q < kSlots; ++q) {
-      const int t = q * kT + tid;
-      if (t < nrn) __pipeline_memcpy_async(&S.nperm[t], &P.perm[ns + t], 4);
-    }
-    __pipeline_commit();
-  };
-  auto fetch_fields = [&](int nrn) {  // call after the perm group landed
-#pragma unroll
-    for (int q = 0; q < kSlots; ++q) {
-      const int t = q * kT + tid;
-      if (t >= nrn) continue;
-      const int i = S.nperm[t];
-#pragma unroll
-      for (int a = 0; a < 3; ++a) __pipeline_memcpy_async(&S.inbuf[a][t], &P.cur.x[a][i], 4);
-#pragma unroll
-      for (int k = 0; k < 9; ++k) __pipeline_memcpy_async(&S.inbuf[3 + k][t], &P.cur.G[k][i], 4);
-      __pipeline_memcpy_async(&S.inbuf[12][t], &P.cur.mass[i], 4);
-      __pipeline_memcpy_async(&S.inbuf[13][t], &P.cur.vol0[i], 4);
-      __pipeline_memcpy_async(&S.inbuf[14][t], &P.cur.meta[i], 4);
-      __pipeline_memcpy_async(&S.inbuf[15][t], &P.cur.pid[i], 4);
-    }
-    __pipeline_commit();
-  };
-  int pf_item = -1;
-  if (kPrefetch && !redo && (int)blockIdx.x < nitems) {
-    const int k0 = P.active_buckets[blockIdx.x];
-    const int s0p = P.bucket_start[k0], n0p = min(kCap, P.bucket_start[k0 + 1] - s0p);
-    fetch_perm(s0p, n0p);
-    __pipeline_wait_prior(0);
-    fetch_fields(n0p);
-    pf_item = blockIdx.x;
-  }
-
-  for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
-    // perm indices of this CTA's next bucket: copied now, consumed after this
-    // bucket's per-particle phase to launch the copy of its particle fields
-    const int nxt = item + (int)gridDim.x;
-    const bool pf_next = kPrefetch && !redo && nxt < nitems;
-    int n_rn = 0;
-    if (pf_next) {
-      const int nk = P.active_buckets[nxt];
-      const int n_s = P.bucket_start[nk];
-      n_rn = min(kCap, P.bucket_start[nk + 1] - n_s);
-      fetch_perm(n_s, n_rn);
-    }
-    const bool staged_in = pf_item == item;
-    const int key = P.active_buckets[item];
-    const bool lostb = key == P.n_keys - 1;
-    const int benv = lostb ? 0 : key / P.blocks_per_env;
-    if (redo && (lostb || !P.run[benv].redo)) continue;  // CTA-uniform
-    const int s = P.bucket_start[key], e = P.bucket_start[key + 1];
-    const int act = lostb ? kActIdle : P.run[benv].action;
-    const bool do_g2p = act == kActFused || act == kActG2P;
-    const bool do_p2g = act == kActP2G || act == kActFused;
-    const int lb = key - benv * P.blocks_per_env;
-    const int ox = kBX * (lb % P.bdims[0]), oy = kBY * ((lb / P.bdims[0]) % P.bdims[1]),
-              oz = kBZ * (lb / (P.bdims[0] * P.bdims[1]));
-    const float dt = do_g2p ? P.run[benv].dt_g2p : 0.0f;
-    const float dtp = lostb ? 0.0f : (redo ? P.run[benv].dt_c : P.run[benv].dt_p2g);  // NCH == 4 only
-    const int s0 = lostb ? 0 : P.shape_off[benv], s1 = lostb ? 0 : P.shape_off[benv + 1];
-    const bool penalty = do_p2g && P.hooks && !P.grid_mode && s1 > s0;
-
-    __syncthreads();  // smem reuse across items
-    if (do_g2p) {
-      for (int t = tid; t < GN; t += kT) {
-        const int lx = t % GX, ly = (t / GX) % GY, lz = t / (GX * GY);
-        const int gx = ox + lx, gy = oy + ly, gz = oz + lz;
-        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (gx < P.dims[0] && gy < P.dims[1] && gz < P.dims[2])
-          v = P.gV[benv * P.nodes_per_env + ((long long)gz * P.dims[1] + gy) * P.dims[0] + gx];
-        S.gtile[t] = v;
-      }
-    }
-    if (penalty && !redo)
-      for (int t = tid; t < kWs; t += kT) S.wsum[t] = 0.0;
-    if (tid == 0) S.penmax = 0u;
-    if (staged_in) {  // this bucket's fields landed (the perm group just issued may still fly)
-      if (pf_next) __pipeline_wait_prior(1);
-      else __pipeline_wait_prior(0);
-    }
-    __syncthreads();
-
-    for (int r0 = s; r0 < e; r0 += kCap) {
-      const int rn = min(kCap, e - r0);
+    for (int r0 = IC.s; r0 < IC.e; r0 += kCap) {
+      const int rn = min(kCap, IC.e - r0);
       const int trips = (rn + kT - 1) / kT;
       if (tid < 3) S.maxb[tid] = 0u;
       float mx_m = 0.f, mx_p = 0.f, mx_f = 0.f;
@@ -282,24 +154,16 @@ __global__ void __launch_bounds__(kT, kCtasPerSm) k_particles(SimParams P) {
         const int t = trip * kT + tid;
         const bool valid = t < rn;
         const int j = r0 + t;
-        const bool from_smem = staged_in && r0 == s;  // CTA-uniform
-        const int i = (valid && !from_smem) ? P.perm[j] : 0;
-        unsigned meta = valid ? (from_smem ? __float_as_uint(S.inbuf[14][t]) : P.cur.meta[i]) : (1u << kLostBit);
+        const int i = valid ? P.perm[j] : 0;
+        unsigned meta = valid ? P.cur.meta[i] : (1u << kLostBit);
         const int penv = (meta >> 8) & kEnvMask;
         const bool was_lost = meta >> kLostBit;
-        const int pact = lostb ? (valid ? P.run[penv].action : kActIdle) : act;
+        const int pact = IC.lostb ? (valid ? P.run[penv].action : kActIdle) : IC.act;
         f3 x = {0.f, 0.f, 0.f}, v = {0.f, 0.f, 0.f};
         float G[9], Cm[9];
         float m = 0.f, V0 = 0.f;
         int pid = 0;
-        if (valid && from_smem) {
-          x = {S.inbuf[0][t], S.inbuf[1][t], S.inbuf[2][t]};
-#pragma unroll
-          for (int k = 0; k < 9; ++k) G[k] = S.inbuf[3 + k][t];
-          m = S.inbuf[12][t];
-          V0 = S.inbuf[13][t];
-          pid = __float_as_int(S.inbuf[15][t]);
-        } else if (valid) {
+        if (valid) {
           x = load3(P.cur.x, i);
 #pragma unroll
           for (int k = 0; k < 9; ++k) G[k] = P.cur.G[k][i];
@@ -310,28 +174,27 @@ __global__ void __launch_bounds__(kT, kCtasPerSm) k_particles(SimParams P) {
 #pragma unroll
           for (int k = 0; k < 9; ++k) G[k] = 0.f;
         }
-        const bool read_vc = valid && (lostb || !do_g2p);
+        const bool read_vc = valid && (IC.lostb || !IC.do_g2p);
         if (read_vc) {
-          const int iv = from_smem ? P.perm[j] : i;  // rare actions (first P2G of a call, lost bucket)
-          v = load3(P.cur.v, iv);
+          v = load3(P.cur.v, i);
 #pragma unroll
-          for (int k = 0; k < 9; ++k) Cm[k] = P.cur.C[k][iv];
+          for (int k = 0; k < 9; ++k) Cm[k] = P.cur.C[k][i];
         } else {
 #pragma unroll
           for (int k = 0; k < 9; ++k) Cm[k] = 0.f;
         }
-        bool write_vc = valid && (lostb || act != kActFused);
-        const bool live = valid && !lostb && !was_lost && act != kActIdle;
+        bool write_vc = valid && (IC.lostb || IC.act != kActFused);
+        const bool live = valid && !IC.lostb && !was_lost && IC.act != kActIdle;
         float speed = -1.0f;
         Sym eps = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};  // Hencky strain tensor (one evaluation per substep)
         const MatParams mp = P.mats[meta & 0xFFu];
 
         // ---------------- G2P of this cycle (mpm.hpp:346-379)
-        if (live && do_g2p) {
+        if (live && IC.do_g2p) {
           int b[3];
           float fx[3];
           base_of(P, x.x, x.y, x.z, b, fx);
-          const int lx = b[0] - ox, ly = b[1] - oy, lz = b[2] - oz;
+          const int lx = b[0] - IC.ox, ly = b[1] - IC.oy, lz = b[2] - IC.oz;
           float wx[3], wy[3], wz[3];
           bspline_w(fx[0], wx);
           bspline_w(fx[1], wy);
@@ -362,21 +225,21 @@ __global__ void __launch_bounds__(kT, kCtasPerSm) k_particles(SimParams P) {
           Cm[3] = k4h * (Sx.y - vs.y * fx[0]); Cm[4] = k4h * (Sy.y - vs.y * fx[1]); Cm[5] = k4h * (Sz.y - vs.y * fx[2]);
           Cm[6] = k4h * (Sx.z - vs.z * fx[0]); Cm[7] = k4h * (Sy.z - vs.z * fx[1]); Cm[8] = k4h * (Sz.z - vs.z * fx[2]);
           v = vs;
-          x = x + dt * vs;
-          if (dt != 0.0f) {
+          x = x + IC.dt * vs;
+          if (IC.dt != 0.0f) {
             float Gn[9];
 #pragma unroll
             for (int r = 0; r < 3; ++r)
 #pragma unroll
               for (int c = 0; c < 3; ++c)
-                Gn[r * 3 + c] = G[r * 3 + c] + dt * (Cm[r * 3 + c] + Cm[r * 3 + 0] * G[0 * 3 + c] +
+                Gn[r * 3 + c] = G[r * 3 + c] + IC.dt * (Cm[r * 3 + c] + Cm[r * 3 + 0] * G[0 * 3 + c] +
                                                      Cm[r * 3 + 1] * G[1 * 3 + c] + Cm[r * 3 + 2] * G[2 * 3 + c]);
             if (!(det_I_plus(Gn) > 0.0f)) set_error(P, penv, kErrDetReturn, pid);
             eps = hencky_strain(Gn);
             von_mises_project_strain(Gn, eps, mp);
 #pragma unroll
             for (int k = 0; k < 9; ++k) G[k] = Gn[k];
-          } else if (do_p2g) {
+          } else if (IC.do_p2g) {
             eps = hencky_strain(G);
           }
           bool bad = false;
@@ -387,9 +250,17 @@ __global__ void __launch_bounds__(kT, kCtasPerSm) k_particles(SimParams P) {
           if (bad) set_error(P, penv, kErrNan, pid);
           speed = norm(v);
           if (!(speed >= 0.0f)) speed = FLT_MAX;
-        } else if (live && do_p2g) {
+        } else if (live && IC.do_p2g) {
           if (!(det_I_plus(G) > 0.0f)) set_error(P, penv, kErrDetStress, pid);
           eps = hencky_strain(G);
+        }
+
+        if (!redo && valid) {  // G is final here: store it now so it does not live on in registers
+#pragma unroll
+          for (int k = 0; k < 9; ++k) P.nxt.G[k][j] = G[k];
+          P.nxt.mass[j] = m;
+          P.nxt.vol0[j] = V0;
+          P.nxt.pid[j] = pid;
         }
 
         // ---------------- binning of the (new) position + P2G payload of the next cycle
@@ -399,13 +270,13 @@ __global__ void __launch_bounds__(kT, kCtasPerSm) k_particles(SimParams P) {
         int b2[3] = {-10, -10, -10};
         float fx2[3] = {0.f, 0.f, 0.f};
         f3 fext = {0.f, 0.f, 0.f};
-        const bool p2g_here = valid && !was_lost && (lostb ? (pact == kActP2G || pact == kActFused) : do_p2g);
+        const bool p2g_here = valid && !was_lost && (IC.lostb ? (pact == kActP2G || pact == kActFused) : IC.do_p2g);
         if (valid && !was_lost) {
           base_of(P, x.x, x.y, x.z, b2, fx2);
           if (base_in_range(P, b2)) {
-            if (!lostb || pact == kActIdle || pact == kActG2P) key_new = bucket_of(P, penv, b2);
+            if (!IC.lostb || pact == kActIdle || pact == kActG2P) key_new = bucket_of(P, penv, b2);
           } else if (p2g_here) {
-            // leaves the domain now: reaction-only penalty, freeze, count (mpm.hpp:239-245)
+            // leaves the domain now: reaction-only IC.penalty, freeze, count (mpm.hpp:239-245)
             if (!redo) {
               if (P.hooks && !P.grid_mode && P.shape_off[penv + 1] > P.shape_off[penv]) penalty_reaction_only(P, penv, x, v);
               atomicAdd((unsigned long long*)&P.lost_count[penv], 1ull);
@@ -417,16 +288,16 @@ __global__ void __launch_bounds__(kT, kCtasPerSm) k_particles(SimParams P) {
           }
         }
         const bool now_lost = meta >> kLostBit;
-        const bool scatter_me = p2g_here && !lostb && !now_lost;
-        if (P.base_dbg && !redo && valid && (p2g_here || (lostb && was_lost && (pact == kActP2G || pact == kActFused)))) {
+        const bool scatter_me = p2g_here && !IC.lostb && !now_lost;
+        if (P.base_dbg && !redo && valid && (p2g_here || (IC.lostb && was_lost && (pact == kActP2G || pact == kActFused)))) {
           P.base_dbg[3 * pid + 0] = now_lost ? -10 : b2[0];
           P.base_dbg[3 * pid + 1] = now_lost ? -10 : b2[1];
           P.base_dbg[3 * pid + 2] = now_lost ? -10 : b2[2];
         }
 
-        // penalty hook: warp-cooperative per shape (coupling.hpp:151-172)
-        if (penalty) {
-          for (int sidx = s0; sidx < s1; ++sidx) {
+        // IC.penalty hook: warp-cooperative per shape (coupling.hpp:151-172)
+        if (IC.penalty) {
+          for (int sidx = IC.s0; sidx < IC.s1; ++sidx) {
             const ShapeDev& sh = P.shapes[sidx];
             f3 f = {0.f, 0.f, 0.f};
             float pen = 0.f;
@@ -464,17 +335,17 @@ __global__ void __launch_bounds__(kT, kCtasPerSm) k_particles(SimParams P) {
           bspline_w(fx2[0], w9);
           bspline_w(fx2[1], w9 + 3);
           bspline_w(fx2[2], w9 + 6);
-          // momentum matrix A (h-scaled) and base b = m v (+ dt f_ext) - A fx; the node
+          // momentum matrix A (h-scaled) and base b = m v (+ IC.dt f_ext) - A fx; the node
           // contribution is w (b + A off), off in {0,1,2}^3 (dpos = h (off - fx))
           float A[9];
           f3 bb;
           float Af[9];
           f3 bf = {0.f, 0.f, 0.f};
           if (NCH == 4) {
-            const float ds = dtp * hs;
+            const float ds = IC.dtp * hs;
 #pragma unroll
             for (int k = 0; k < 9; ++k) A[k] = hm * Cm[k] + ds * tau[k];
-            bb = (m * v + dtp * fext) - matvec(A, f3{fx2[0], fx2[1], fx2[2]});
+            bb = (m * v + IC.dtp * fext) - matvec(A, f3{fx2[0], fx2[1], fx2[2]});
           } else {
 #pragma unroll
             for (int k = 0; k < 9; ++k) {
@@ -484,7 +355,7 @@ __global__ void __launch_bounds__(kT, kCtasPerSm) k_particles(SimParams P) {
             bb = m * v - matvec(A, f3{fx2[0], fx2[1], fx2[2]});
             bf = fext - matvec(Af, f3{fx2[0], fx2[1], fx2[2]});
           }
-          const int lx = b2[0] - (ox - 1), ly = b2[1] - (oy - 1), lz = b2[2] - (oz - 1);
+          const int lx = b2[0] - (IC.ox - 1), ly = b2[1] - (IC.oy - 1), lz = b2[2] - (IC.oz - 1);
           if (lx >= 0 && ly >= 0 && lz >= 0 && lx < CX && ly < CY && lz < CZ) {
             cell = (lz * CY + ly) * CX + lx;
             // [m wx0 wx1 wx2] [wy0 wy1 wy2 wz0] [wz1 wz2 b.x b.y] [b.z A00 A01 A02] [A10 A11 A12 A20]
@@ -522,12 +393,7 @@ __global__ void __launch_bounds__(kT, kCtasPerSm) k_particles(SimParams P) {
           // ---------------- write back in bucket order (the re-sort)
           if (valid) {
             P.nxt.x[0][j] = x.x; P.nxt.x[1][j] = x.y; P.nxt.x[2][j] = x.z;
-#pragma unroll
-            for (int k = 0; k < 9; ++k) P.nxt.G[k][j] = G[k];
-            P.nxt.mass[j] = m;
-            P.nxt.vol0[j] = V0;
             P.nxt.meta[j] = meta;
-            P.nxt.pid[j] = pid;
             if (write_vc) {
               P.nxt.v[0][j] = v.x; P.nxt.v[1][j] = v.y; P.nxt.v[2][j] = v.z;
 #pragma unroll
@@ -547,21 +413,15 @@ __global__ void __launch_bounds__(kT, kCtasPerSm) k_particles(SimParams P) {
               P.rank[j] = basecnt + __popc(peers & ((1u << lane) - 1u));
             }
           }
-          if (do_g2p) {  // per-env max speed (bucket env-uniform): warp max -> one atomic
+          if (IC.do_g2p) {  // per-env max speed (bucket env-uniform): warp max -> one atomic
             float sp = speed;
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) sp = fmaxf(sp, __shfl_xor_sync(FULL, sp, o));
-            if (lane == 0 && sp >= 0.0f) float_bits_max(&P.vmax_bits[benv], sp);
+            if (lane == 0 && sp >= 0.0f) float_bits_max(&P.vmax_bits[IC.benv], sp);
           }
         }
       }
-      __syncthreads();  // inbuf consumed: start copying the next bucket behind this one's scatter
-      if (r0 == s && pf_next) {
-        __pipeline_wait_prior(0);
-        fetch_fields(n_rn);
-        pf_item = nxt;
-      }
-      if (!do_p2g) continue;
+      if (!IC.do_p2g) continue;
       // fixed-point scales of this round: |node sum| <= rn * max bound < 2^30 / scale
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) {
@@ -657,16 +517,16 @@ __global__ void __launch_bounds__(kT, kCtasPerSm) k_particles(SimParams P) {
           const int im = S.itile[3][t];
           if (im != 0) {  // (the 4 padding words per z-layer are never written)
             const int lz = t / kTZS, rem = t - lz * kTZS, ly = rem / PX, lx = rem - ly * PX;
-            const int gx = ox - 1 + lx, gy = oy - 1 + ly, gz = oz - 1 + lz;
+            const int gx = IC.ox - 1 + lx, gy = IC.oy - 1 + ly, gz = IC.oz - 1 + lz;
             if (gx >= 0 && gy >= 0 && gz >= 0 && gx < P.dims[0] && gy < P.dims[1] && gz < P.dims[2]) {
-              const long long gi = benv * P.nodes_per_env + ((long long)gz * P.dims[1] + gy) * P.dims[0] + gx;
+              const long long gi = IC.benv * P.nodes_per_env + ((long long)gz * P.dims[1] + gy) * P.dims[0] + gx;
               atomicAdd(&P.gPM[gi], make_float4(qs[0] * (float)S.itile[0][t], qs[1] * (float)S.itile[1][t],
                                                 qs[2] * (float)S.itile[2][t], qs[3] * (float)im));
               if (NCH == 7)
                 atomicAdd(&P.gF[gi], make_float4(qs[4] * (float)S.itile[4][t], qs[5] * (float)S.itile[5][t],
                                                  qs[6] * (float)S.itile[6][t], 0.0f));
               if (!redo)
-                P.nb_flag[benv * P.blocks_per_env + ((gz / kBZ) * P.bdims[1] + gy / kBY) * P.bdims[0] + gx / kBX] = 1;
+                P.nb_flag[IC.benv * P.blocks_per_env + ((gz / kBZ) * P.bdims[1] + gy / kBY) * P.bdims[0] + gx / kBX] = 1;
             }
           }
 #pragma unroll
@@ -676,8 +536,8 @@ __global__ void __launch_bounds__(kT, kCtasPerSm) k_particles(SimParams P) {
       }
     }
 
-    if (penalty && !redo) {
-      const int b0 = P.body_off[benv], nb = min(P.body_off[benv + 1] - b0, kMaxBodiesPerEnv);
+    if (IC.penalty && !redo) {
+      const int b0 = P.body_off[IC.benv], nb = min(P.body_off[IC.benv + 1] - b0, kMaxBodiesPerEnv);
       for (int t = tid; t < nb * 6; t += kT) {
         const double val = S.wsum[t];
         if (val != 0.0) atomicAdd(P.wrench + 6 * b0 + t, val);
@@ -685,14 +545,68 @@ __global__ void __launch_bounds__(kT, kCtasPerSm) k_particles(SimParams P) {
       if (tid < 3) {
         const double a = S.wsum[6 * kMaxBodiesPerEnv + tid];
         if (a != 0.0) {
-          atomicAdd(P.applied + 3 * benv + tid, a);
+          atomicAdd(P.applied + 3 * IC.benv + tid, a);
           double r = 0.0;
           for (int bb = 0; bb < nb; ++bb) r += S.wsum[6 * bb + tid];
-          atomicAdd(P.react + 3 * benv + tid, r);
+          atomicAdd(P.react + 3 * IC.benv + tid, r);
         }
       }
-      if (tid == 0 && S.penmax) atomicMax(&P.max_pen_bits[benv], S.penmax);
+      if (tid == 0 && S.penmax) atomicMax(&P.max_pen_bits[IC.benv], S.penmax);
     }
+  }
+}
+
+template <int NCH>
+__global__ void __launch_bounds__(kT, kCtasPerSm) k_particles(SimParams P) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  Smem<NCH>& S = *reinterpret_cast<Smem<NCH>*>(smem_raw);
+  const int tid = threadIdx.x;
+  const bool redo = P.redo_pass != 0;
+  if (redo && !*P.any_redo) return;
+  const int nitems = *P.n_active_buckets;
+
+  for (int t = tid; t < NCH * PN; t += kT) (&S.itile[0][0])[t] = 0;
+
+  volatile ItemCtx& IC = S.ic;
+  for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
+    const int key = P.active_buckets[item];
+    const bool lostb = key == P.n_keys - 1;
+    const int benv = lostb ? 0 : key / P.blocks_per_env;
+    if (redo && (lostb || !P.run[benv].redo)) continue;  // CTA-uniform
+    const int s = P.bucket_start[key], e = P.bucket_start[key + 1];
+    const int act = lostb ? kActIdle : P.run[benv].action;
+    const bool do_g2p = act == kActFused || act == kActG2P;
+    const bool do_p2g = act == kActP2G || act == kActFused;
+    const int lb = key - benv * P.blocks_per_env;
+    const int ox = kBX * (lb % P.bdims[0]), oy = kBY * ((lb / P.bdims[0]) % P.bdims[1]),
+              oz = kBZ * (lb / (P.bdims[0] * P.bdims[1]));
+    const float dt = do_g2p ? P.run[benv].dt_g2p : 0.0f;
+    const float dtp = lostb ? 0.0f : (redo ? P.run[benv].dt_c : P.run[benv].dt_p2g);  // NCH == 4 only
+    const int s0 = lostb ? 0 : P.shape_off[benv], s1 = lostb ? 0 : P.shape_off[benv + 1];
+    const bool penalty = do_p2g && P.hooks && !P.grid_mode && s1 > s0;
+
+    __syncthreads();  // smem reuse across items
+    if (do_g2p) {
+      for (int t = tid; t < GN; t += kT) {
+        const int lx = t % GX, ly = (t / GX) % GY, lz = t / (GX * GY);
+        const int gx = ox + lx, gy = oy + ly, gz = oz + lz;
+        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (gx < P.dims[0] && gy < P.dims[1] && gz < P.dims[2])
+          v = P.gV[benv * P.nodes_per_env + ((long long)gz * P.dims[1] + gy) * P.dims[0] + gx];
+        S.gtile[t] = v;
+      }
+    }
+    if (penalty && !redo)
+      for (int t = tid; t < kWs; t += kT) S.wsum[t] = 0.0;
+    if (tid == 0) {
+      S.penmax = 0u;
+      IC.key = key; IC.benv = benv; IC.s = s; IC.e = e; IC.act = act;
+      IC.ox = ox; IC.oy = oy; IC.oz = oz; IC.s0 = s0; IC.s1 = s1;
+      IC.dt = dt; IC.dtp = dtp;
+      IC.lostb = lostb; IC.do_g2p = do_g2p; IC.do_p2g = do_p2g; IC.penalty = penalty;
+    }
+    __syncthreads();
+    item_rounds<NCH>(P, S, redo);
   }
 }
 
