@@ -18,7 +18,7 @@ __device__ __forceinline__ unsigned float_bits_max(unsigned* addr, float v) {
   return atomicMax(addr, __float_as_uint(v));
 }
 
-__device__ __forceinline__ void set_error(const SimParams& P, int env, int code, int pid) {
+static __device__ MSIM_COLD void set_error(const SimParams& P, int env, int code, int pid) {
   atomicCAS(&P.err_code[env], 0, code);  // first error of the env wins
   atomicMin(&P.err_pid[env], pid);
 }
@@ -206,7 +206,7 @@ __device__ inline void rigid_env(const SimParams& P, int env, int integrate) {
 
 // Particle leaving the domain this cycle: its penalty reaction still counts
 // (the hook runs before p2g's loss detection, coupling.hpp:266-274).
-__device__ inline void penalty_reaction_only(const SimParams& P, int env, f3 x, f3 v) {
+static __device__ MSIM_COLD void penalty_reaction_only(const SimParams& P, int env, f3 x, f3 v) {
   const int s0 = P.shape_off[env], s1 = P.shape_off[env + 1];
   const int b0 = P.body_off[env];
   for (int s = s0; s < s1; ++s) {

@@ -7,6 +7,16 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+// Rarely executed device paths (errors, volume SDF lookups, the global-memory
+// scatter fallback). Inlined: out of line (variant build MSIM_OUTLINE_COLD)
+// the k_particles launch took 1.24 ms instead of 0.98 ms (config D, 256 envs):
+// a call site constrains the caller's register allocation even when cold.
+#ifdef MSIM_OUTLINE_COLD
+#define MSIM_COLD __noinline__
+#else
+#define MSIM_COLD __forceinline__
+#endif
+
 namespace msim_dev {
 
 // ---------------------------------------------------------------------------
@@ -175,6 +185,15 @@ __device__ __forceinline__ void sym_from_frame(const float* U, const float* s, f
     }
 }
 
+// Large-strain path of hencky_strain: the principal frame by cyclic Jacobi.
+// (Inlined: as a call it cost 60 % more kernel time.)
+__device__ __forceinline__ Sym hencky_strain_jacobi(const float* G) {
+  float U[9], e[3], S[9];
+  hencky_frame(G, U, e);
+  sym_from_frame(U, e, S);
+  return {S[0], S[4], S[8], S[1], S[2], S[5]};
+}
+
 // Hencky strain TENSOR eps = 0.5 log(F F^T) = 0.5 log1p(E) in the spatial
 // frame, i.e. U diag(log sigma) U^T, as a matrix function instead of an
 // eigen-decomposition: with Z = E (2I + E)^-1 (eigenvalues z = e / (2 + e)),
@@ -205,10 +224,7 @@ __device__ __forceinline__ Sym hencky_strain(const float* G) {
     return sym_mul(Z, q);
 #ifndef MSIM_ABLATE_EIGEN
   }
-  float U[9], e[3], S[9];
-  hencky_frame(G, U, e);
-  sym_from_frame(U, e, S);
-  return {S[0], S[4], S[8], S[1], S[2], S[5]};
+  return hencky_strain_jacobi(G);
 #endif
 }
 
@@ -312,7 +328,9 @@ struct ShapeDev {
 __device__ __forceinline__ float vol_at(const float* s, const ShapeDev& sh, int i, int j, int k) {
   return s[((long long)k * sh.vol_dims[1] + j) * sh.vol_dims[0] + i];
 }
-__device__ __forceinline__ float vol_interp(const float* pool, const ShapeDev& sh, f3 p) {
+// Out of line: 7 calls per in-band particle would otherwise be inlined into the
+// particle kernel (instruction-cache pressure); volumes are the rare shape type.
+static __device__ MSIM_COLD float vol_interp(const float* pool, const ShapeDev& sh, f3 p) {
   const float* s = pool + sh.vol_off;
   float inv = 1.0f / sh.vol_voxel;
   f3 local = {(p.x - sh.vol_origin[0]) * inv, (p.y - sh.vol_origin[1]) * inv,

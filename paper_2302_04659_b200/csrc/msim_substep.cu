@@ -115,7 +115,7 @@ __device__ __forceinline__ int fix_rn(float x) { return __float_as_int(x + 12582
 // Global-memory scatter of one particle (fallback when its stencil leaves the
 // bucket's P2G tile, e.g. a particle faster than the CFL bound assumed).
 template <int NCH>
-__device__ void scatter_global(const SimParams& P, int env, const int* b, const float* w9, float m, f3 bp,
+__device__ MSIM_COLD void scatter_global(const SimParams& P, int env, const int* b, const float* w9, float m, f3 bp,
                                const float* Ap, f3 bf, const float* Af, bool mark) {
   for (int dk = 0; dk < 3; ++dk)
     for (int dj = 0; dj < 3; ++dj)
