@@ -552,7 +552,8 @@ __device__ __forceinline__ void item_rounds(const SimParams& P, Smem<NCH>& S, bo
 #pragma unroll
           for (int q = 0; q < NCH; ++q) S.itile[q][t] = 0;
         }
-        __syncthreads();
+        // no barrier here: the next round touches itile / maxb only after its
+        // post-staging barrier, and the item loop starts with one
       }
     }
 
