@@ -367,6 +367,7 @@ void upload_bodies(msim_gpu_ctx* c) {
         o.vol_off = (long long)pool.size();
         const auto& smp = c->vol_h[e][s];
         pool.insert(pool.end(), smp.begin(), smp.end());
+        o.vol_min = smp.empty() ? 0.0 : (double)*std::min_element(smp.begin(), smp.end());
       }
       sh.push_back(o);
     }
@@ -1074,7 +1075,6 @@ int msim_gpu_read_report(msim_gpu_ctx* c, int env, msim_step_report* r) {
     unsigned pen = 0;
     double bal = 0.0;
     long long lost = 0;
-    int cyc = 0;
     cudaStream_t s = c->stream;
     CK(cudaMemcpyAsync(&pen, c->max_pen_d.as<unsigned>() + env, sizeof pen, cudaMemcpyDeviceToHost, s));
     CK(cudaMemcpyAsync(&bal, c->balance_d.as<double>() + env, sizeof bal, cudaMemcpyDeviceToHost, s));
@@ -1088,7 +1088,6 @@ int msim_gpu_read_report(msim_gpu_ctx* c, int env, msim_step_report* r) {
     r->max_force_balance_error = bal;
     r->lost_particles = lost;
     r->cfl_cycles = run.cyc_sum;
-    (void)cyc;
     return MSIM_OK;
   });
 }

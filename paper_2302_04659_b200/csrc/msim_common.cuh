@@ -201,6 +201,33 @@ __device__ inline void rigid_env(const SimParams& P, int env, int integrate) {
     }
     d.vol_voxel = (float)sh.vol_voxel;
     d.vol_off = sh.vol_off;
+    // culling bound (shape_may_touch): world x = R (local - tinv)
+    if (sh.type == 0) {  // plane: phi = n . (Ri x + tinv) - d = (R n) . x + n . tinv - d
+      double nw[3];
+      qrot(wq, sh.p, nw);
+      for (int k = 0; k < 3; ++k) d.bnd[k] = (float)nw[k];
+      d.bnd[3] = (float)(sh.p[0] * -it[0] + sh.p[1] * -it[1] + sh.p[2] * -it[2] - sh.p[3]);
+      d.bplane = 1;
+    } else {
+      double lc[3] = {0.0, 0.0, 0.0}, rad = 0.0;
+      if (sh.type == 1) rad = sh.p[0];
+      else if (sh.type == 2) rad = sqrt(sh.p[0] * sh.p[0] + sh.p[1] * sh.p[1] + sh.p[2] * sh.p[2]);
+      else if (sh.type == 3) rad = sh.p[0] + sh.p[1];
+      else {  // volume: box half-diagonal, phi >= vol_min + distance outside the box
+        double hd2 = 0.0;
+        for (int k = 0; k < 3; ++k) {
+          const double ext = (sh.vol_dims[k] - 1) * sh.vol_voxel;
+          lc[k] = sh.vol_origin[k] + 0.5 * ext;
+          hd2 += 0.25 * ext * ext;
+        }
+        rad = sqrt(hd2) + fmax(0.0, -sh.vol_min);
+      }
+      double wc[3];
+      qrot(wq, lc, wc);
+      for (int k = 0; k < 3; ++k) d.bnd[k] = (float)(wc[k] + wt[k]);
+      d.bnd[3] = (float)rad;
+      d.bplane = 0;
+    }
   }
 }
 

@@ -321,7 +321,23 @@ struct ShapeDev {
   float vol_origin[3];
   float vol_voxel;
   long long vol_off;  // offset into the volume sample pool
+  // Conservative world-space bound of the region where phi can be < r_c:
+  // bounded shapes: sphere (bnd[0..2] centre, bnd[3] radius, phi >= |x - c| - r);
+  // planes (bplane): phi(x) = bnd[0..2] . x + bnd[3] exactly.
+  float bnd[4];
+  int bplane;
 };
+
+// Can the point x be within r_c of the shape (phi < r_c)? A bound test of a
+// few FMAs ahead of the SDF: a warp whose particles are all far from a
+// collider skips its transform + SDF + gradient. Conservative by a relative
+// margin (fp32 rounding of the bound vs the SDF).
+__device__ __forceinline__ bool shape_may_touch(const ShapeDev& sh, f3 x, float r_c) {
+  const float margin = r_c + 1e-4f * (fabsf(x.x) + fabsf(x.y) + fabsf(x.z) + fabsf(sh.bnd[3])) + 1e-6f;
+  if (sh.bplane) return sh.bnd[0] * x.x + sh.bnd[1] * x.y + sh.bnd[2] * x.z + sh.bnd[3] < margin;
+  const float dx = x.x - sh.bnd[0], dy = x.y - sh.bnd[1], dz = x.z - sh.bnd[2], rm = sh.bnd[3] + margin;
+  return dx * dx + dy * dy + dz * dz < rm * rm;
+}
 
 // Trilinear SDF volume lookup with clamping (sdf.hpp:46-62), software
 // interpolation (texture filtering would use 8-bit weights).

@@ -95,6 +95,7 @@ struct ShapeHost {  // shape description kept on device in double for the rigid 
   double vol_origin[3];
   double vol_voxel;
   long long vol_off;
+  double vol_min;  // smallest SDF sample (bounds phi outside the volume box)
 };
 
 // Per-kernel CUDA-event timing on the context stream (bench / profiling) and

@@ -62,6 +62,11 @@ template <int NCH> constexpr int pay_floats() { return NCH == 4 ? 24 : 32; }  //
 #define MSIM_CTAS_PER_SM 5  // measured: 4 -> 1.12, 5 -> 1.05, 6 -> 1.10 ms per launch (config D, 256 envs)
 #endif
 constexpr int kCtasPerSm = MSIM_CTAS_PER_SM;
+#ifdef MSIM_NO_CULL  // variant build: no bounding test ahead of the collider SDFs
+constexpr bool kNoCull = true;
+#else
+constexpr bool kNoCull = false;
+#endif
 // Loop unrolling of the 27-node stencils: the kernel is issue/latency bound
 // with a large instruction footprint, and rolled scatter loops measured faster
 // (ms per launch, D 256 envs: all unrolled 0.975, z rolled 0.961, z and y
@@ -320,7 +325,8 @@ __device__ __forceinline__ void item_rounds(const SimParams& P, Smem<NCH>& S, bo
             const ShapeDev& sh = P.shapes[sidx];
             f3 f = {0.f, 0.f, 0.f};
             float pen = 0.f;
-            const bool hit = scatter_me && penalty_force(sh, P.vol_pool, x, v, P.r_c_particle, P.c_d, f, pen);
+            const bool hit = scatter_me && (kNoCull || shape_may_touch(sh, x, P.r_c_particle)) &&
+                             penalty_force(sh, P.vol_pool, x, v, P.r_c_particle, P.c_d, f, pen);
             if (!hit) f = {0.f, 0.f, 0.f};
             fext = fext + f;
             if (!redo && __any_sync(FULL, hit)) {
@@ -715,7 +721,8 @@ __global__ void __launch_bounds__(256) k_grid(SimParams P) {
         const ShapeDev& sh = P.shapes[sidx];
         f3 fp = {0.f, 0.f, 0.f};
         float pen = 0.0f;
-        const bool hit = live && penalty_force(sh, P.vol_pool, xi, vel, P.r_c_grid, P.c_d, fp, pen);
+        const bool hit = live && shape_may_touch(sh, xi, P.r_c_grid) &&
+                         penalty_force(sh, P.vol_pool, xi, vel, P.r_c_grid, P.c_d, fp, pen);
         if (hit) {
           fp = scale * fp;
           f = f + fp;
