@@ -5,6 +5,7 @@
 // reference test it ports. Output: one "PASS name" / "FAIL name: msg" line
 // per test, exit code = number of failures.
 #include "msim_oracle.hpp"
+#include "msim_oracle_tasks.hpp"
 
 #include <cstdio>
 #include <sstream>
@@ -1044,6 +1045,230 @@ TEST(Svd, ReconstructionAndOrthogonality) {  // contract of Eigen::JacobiSVD (mp
     EXPECT((s.V.transpose() * s.V - M3::Identity()).norm() < 1e-13);
     EXPECT(s.s.x >= 0 && s.s.y >= 0 && s.s.z >= 0);
   }
+}
+
+// ---- test_sdf.cpp (mesh baking, :151-182) -----------------------------------
+TEST(BakeMesh, UnitCubeAgainstAnalyticBox) {  // test_sdf.cpp:151-164
+  double voxel = 0.05;
+  SdfVolume vol = bake_mesh_sdf(make_box_mesh(V3(0.5, 0.5, 0.5)), voxel, 3 * voxel);
+  Shape analytic = mk(ShapeType::Box);
+  analytic.half_extents = V3(0.5, 0.5, 0.5);
+  Shape baked = mk(ShapeType::Volume);
+  baked.volume = std::make_shared<SdfVolume>(vol);
+  auto g = rng(17);
+  for (int i = 0; i < 1000; ++i) {
+    V3 p = random_vec3(g, -0.7, 0.7);
+    EXPECT_NEAR(sdf_eval(baked, p), sdf_eval(analytic, p), voxel);
+  }
+}
+TEST(BakeMesh, CenterSample) {  // :166-170
+  double voxel = 0.1;
+  SdfVolume vol = bake_mesh_sdf(make_box_mesh(V3(0.5, 0.5, 0.5)), voxel, 2 * voxel);
+  EXPECT_NEAR(vol.interpolate(V3()), -0.5, voxel);
+}
+TEST(BakeMesh, SurfaceLatticeProximity) {  // :172-176
+  double voxel = 0.1;
+  SdfVolume vol = bake_mesh_sdf(make_box_mesh(V3(0.5, 0.5, 0.5)), voxel, 2 * voxel);
+  EXPECT(std::abs(vol.interpolate(V3(0.5, 0.0, 0.0))) <= voxel);
+}
+TEST(BakeMesh, EmptyAndDegenerateMeshError) {  // :178-182
+  EXPECT_THROW(bake_mesh_sdf({}, 0.01, 0.01), std::invalid_argument);
+  Triangle degen{V3(0, 0, 0), V3(1, 0, 0), V3(2, 0, 0)};
+  EXPECT_THROW(bake_mesh_sdf({degen, degen}, 0.1, 0.1), std::invalid_argument);
+}
+
+// ---- test_scenario.cpp (task metrics, :24-270) -----------------------------
+namespace {
+const RegionBox kUnitRegion{V3(0, 0, 0), V3(1, 1, 1)};
+double chamfer_brute(const std::vector<V3>& a, const std::vector<V3>& b) {  // test_scenario.cpp:193-204
+  auto side = [](const std::vector<V3>& from, const std::vector<V3>& to) {
+    double sum = 0.0;
+    for (const V3& p : from) {
+      double best = std::numeric_limits<double>::infinity();
+      for (const V3& q : to) best = std::min(best, (p - q).norm());
+      sum += best;
+    }
+    return sum / static_cast<double>(from.size());
+  };
+  return side(a, b) + side(b, a);
+}
+}  // namespace
+
+TEST(Fill, AllInsideAtRestSucceeds) {  // test_scenario.cpp:27-34
+  std::vector<V3> x, v;
+  for (int i = 0; i < 10; ++i) x.push_back(V3(0.1 * i + 0.05, 0.5, 0.5)), v.push_back(V3());
+  FillResult r = metric_fill(x, v, kUnitRegion);
+  EXPECT(r.fraction == 1.0 && r.max_speed == 0.0 && r.success);
+}
+TEST(Fill, NoneInsideFails) {  // :36-41
+  FillResult r = metric_fill({V3(2, 2, 2), V3(-1, 0, 0)}, {V3(), V3()}, kUnitRegion);
+  EXPECT(r.fraction == 0.0 && !r.success);
+}
+TEST(Fill, NinetyOnePercentInsideIsSuccessAtTheBoundary) {  // :43-53
+  std::vector<V3> x, v(100);
+  for (int i = 0; i < 91; ++i) x.push_back(V3(0.5, 0.5, 0.5));
+  for (int i = 0; i < 9; ++i) x.push_back(V3(5, 5, 5));
+  FillResult r = metric_fill(x, v, kUnitRegion);
+  EXPECT(r.fraction == 0.91 && r.success);
+  x[0] = V3(5, 5, 5);
+  EXPECT(!metric_fill(x, v, kUnitRegion).success);
+}
+TEST(Fill, FastParticleBreaksSuccess) {  // :55-61
+  FillResult r = metric_fill({V3(0.5, 0.5, 0.5)}, {V3(0.06, 0, 0)}, kUnitRegion);
+  EXPECT(r.fraction == 1.0);
+  EXPECT_NEAR(r.max_speed, 0.06, 1e-15);
+  EXPECT(!r.success);
+}
+TEST(Fill, FractionInvariantUnderReordering) {  // :63-71
+  auto g = rng(7);
+  std::vector<V3> x, v;
+  for (int i = 0; i < 200; ++i) x.push_back(random_vec3(g, -0.5, 1.5)), v.push_back(V3());
+  FillResult a = metric_fill(x, v, kUnitRegion);
+  std::reverse(x.begin(), x.end());
+  FillResult b = metric_fill(x, v, kUnitRegion);
+  EXPECT(a.fraction == b.fraction && a.max_speed == b.max_speed);
+}
+TEST(Fill, EmptyInputThrows) {  // :73-75
+  EXPECT_THROW(metric_fill({}, {}, kUnitRegion), std::invalid_argument);
+}
+TEST(Heightmap, NoParticlesAllZeros) {  // :80-85
+  DepthMap m = render_heightmap({}, kUnitRegion, 4, 4);
+  EXPECT(m.samples.size() == 16u);
+  for (double s : m.samples) EXPECT(s == 0.0);
+}
+TEST(Heightmap, SingleParticleFillsExactlyItsCell) {  // :87-96
+  V3 x(0.30, 0.77, 0.42);
+  DepthMap m = render_heightmap({x}, kUnitRegion, 5, 4);
+  int ci = static_cast<int>(x.x / 0.2), cj = static_cast<int>(x.y / 0.25);
+  for (int j = 0; j < 4; ++j)
+    for (int i = 0; i < 5; ++i) EXPECT(m.at(i, j) == ((i == ci && j == cj) ? 0.42 : 0.0));
+}
+TEST(Heightmap, SameCellTakesMaxHeight) {  // :98-102
+  DepthMap m = render_heightmap({V3(0.1, 0.1, 0.3), V3(0.12, 0.11, 0.8)}, kUnitRegion, 4, 4);
+  EXPECT(m.at(0, 0) == 0.8);
+}
+TEST(Heightmap, PermutationInvariantAndMonotone) {  // :104-116
+  auto g = rng(11);
+  std::vector<V3> ps;
+  for (int i = 0; i < 300; ++i) ps.push_back(random_vec3(g, 0.0, 1.0));
+  DepthMap a = render_heightmap(ps, kUnitRegion, 6, 6);
+  std::shuffle(ps.begin(), ps.end(), g);
+  DepthMap b = render_heightmap(ps, kUnitRegion, 6, 6);
+  EXPECT(a.samples == b.samples);
+  ps.push_back(V3(0.5, 0.5, 0.99));
+  DepthMap c = render_heightmap(ps, kUnitRegion, 6, 6);
+  for (std::size_t i = 0; i < a.samples.size(); ++i) EXPECT(c.samples[i] >= b.samples[i]);
+}
+TEST(Heightmap, ParticlesOutsideRegionIgnored) {  // :118-121
+  DepthMap m = render_heightmap({V3(1.5, 0.5, 0.5)}, kUnitRegion, 4, 4);
+  for (double s : m.samples) EXPECT(s == 0.0);
+}
+TEST(Heightmap, TooCoarseResolutionThrows) {  // :123-125
+  EXPECT_THROW(render_heightmap({}, kUnitRegion, 1, 4), std::invalid_argument);
+}
+namespace {
+DepthMap map_from(std::initializer_list<double> vals, int nx, int ny, double threshold) {  // :130-138
+  DepthMap m;
+  m.nx = nx;
+  m.ny = ny;
+  m.cell = 0.01;
+  m.threshold = threshold;
+  m.samples.assign(vals);
+  return m;
+}
+}  // namespace
+TEST(WriteIou, IdenticalMapsScoreOne) {  // :140-145
+  DepthMap m = map_from({0.1, 0.0, 0.2, 0.0, 0.1, 0.2}, 3, 2, 0.05);
+  IouResult r = metric_write_iou(m, m);
+  EXPECT(r.iou == 1.0 && r.success);
+}
+TEST(WriteIou, DisjointOccupancyScoresZero) {  // :147-153
+  IouResult r = metric_write_iou(map_from({0.0, 0.1, 0.0, 0.1}, 2, 2, 0.05), map_from({0.1, 0.0, 0.1, 0.0}, 2, 2, 0.05));
+  EXPECT(r.iou == 0.0 && !r.success);
+}
+TEST(WriteIou, BothEmptyDefinedAsOne) {  // :155-159
+  DepthMap a = map_from({0.1, 0.1, 0.1, 0.1}, 2, 2, 0.05);
+  EXPECT(metric_write_iou(a, a).iou == 1.0);
+}
+TEST(WriteIou, MatchesBruteForceCountingOracle) {  // :161-180
+  auto g = rng(13);
+  for (int trial = 0; trial < 20; ++trial) {
+    DepthMap a, b;
+    a.nx = b.nx = 7;
+    a.ny = b.ny = 5;
+    a.threshold = b.threshold = 0.5;
+    for (int i = 0; i < 35; ++i) {
+      a.samples.push_back(uniform(g, 0.0, 1.0));
+      b.samples.push_back(uniform(g, 0.0, 1.0));
+    }
+    std::size_t inter = 0, uni = 0;
+    for (int i = 0; i < 35; ++i) {
+      bool oa = a.samples[i] < 0.5, ob = b.samples[i] < 0.5;
+      if (oa && ob) ++inter;
+      if (oa || ob) ++uni;
+    }
+    double expect = uni == 0 ? 1.0 : double(inter) / double(uni);
+    EXPECT(metric_write_iou(a, b).iou == expect);
+  }
+}
+TEST(WriteIou, ResolutionMismatchThrows) {  // :182-186
+  EXPECT_THROW(metric_write_iou(map_from({0, 0, 0, 0}, 2, 2, 0.5), map_from({0, 0, 0, 0, 0, 0}, 3, 2, 0.5)),
+               std::invalid_argument);
+}
+TEST(Chamfer, EqualSetsAreZero) {  // :205-210
+  auto g = rng(17);
+  std::vector<V3> a;
+  for (int i = 0; i < 50; ++i) a.push_back(random_vec3(g));
+  EXPECT(chamfer_distance(a, a) == 0.0);
+}
+TEST(Chamfer, UnitSeparationSumsToTwo) {  // :211-214
+  EXPECT(chamfer_distance({V3(0, 0, 0)}, {V3(0, 0, 1)}) == 2.0);
+}
+TEST(Chamfer, MatchesBruteForceOracle) {  // :216-224
+  auto g = rng(19);
+  std::vector<V3> a, b;
+  for (int i = 0; i < 500; ++i) {
+    a.push_back(random_vec3(g, 0.0, 0.2));
+    b.push_back(random_vec3(g, 0.05, 0.25));
+  }
+  EXPECT_NEAR(chamfer_distance(a, b), chamfer_brute(a, b), 1e-12);
+}
+TEST(Chamfer, SymmetricAndNonNegative) {  // :226-234
+  auto g = rng(23);
+  std::vector<V3> a, b;
+  for (int i = 0; i < 80; ++i) a.push_back(random_vec3(g));
+  for (int i = 0; i < 120; ++i) b.push_back(random_vec3(g));
+  double ab = chamfer_distance(a, b);
+  EXPECT_NEAR(ab, chamfer_distance(b, a), 4 * std::numeric_limits<double>::epsilon() * ab);
+  EXPECT(ab > 0.0);
+}
+TEST(Chamfer, EmptySetThrows) {  // :236-238
+  EXPECT_THROW(chamfer_distance({}, {V3()}), std::invalid_argument);
+}
+TEST(Pinch, CurrentEqualsTargetSucceeds) {  // :243-249
+  std::vector<V3> init = {V3(0, 0, 0), V3(1, 0, 0)}, target = {V3(0, 0, 1), V3(1, 0, 1)};
+  PinchResult r = metric_pinch(target, init, target);
+  EXPECT(r.ratio == 0.0 && r.success);
+}
+TEST(Pinch, CurrentEqualsInitialFails) {  // :251-257
+  std::vector<V3> init = {V3(0, 0, 0), V3(1, 0, 0)}, target = {V3(0, 0, 1), V3(1, 0, 1)};
+  PinchResult r = metric_pinch(init, init, target);
+  EXPECT(r.ratio == 1.0 && !r.success);
+}
+TEST(Pinch, HalfwayInterpolationMatchesBruteForceRatio) {  // :259-273
+  auto g = rng(29);
+  std::vector<V3> init, target, current;
+  for (int i = 0; i < 60; ++i) {
+    V3 a = random_vec3(g, 0.0, 0.1);
+    V3 b = a + V3(0.05, 0.0, 0.02);
+    init.push_back(a);
+    target.push_back(b);
+    current.push_back(0.5 * (a + b));
+  }
+  PinchResult r = metric_pinch(current, init, target);
+  double expect = chamfer_brute(current, target) / chamfer_brute(init, target);
+  EXPECT_NEAR(r.ratio, expect, 1e-12);
+  EXPECT(r.success == (r.ratio < 0.3));
 }
 
 int main(int argc, char** argv) {

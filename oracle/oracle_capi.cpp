@@ -3,6 +3,7 @@
 // so parity tests can drive both with the same descriptors. Loaded by
 // tests/ and bench.py (cpu_baseline / --impl reference) through ctypes.
 #include "msim_oracle.hpp"
+#include "msim_oracle_tasks.hpp"
 #include "../include/msim_gpu.h"
 
 #include <chrono>
@@ -420,4 +421,90 @@ double oracle_time_env_steps(oracle_world* w, int steps, int* err) {
   return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
 }
 
+// ---- mesh baking and task metrics (msim_oracle_tasks.hpp) -----------------
+namespace {
+TriangleMesh mesh_from(const double* tri, int64_t n) {
+  TriangleMesh m((size_t)n);
+  for (int64_t t = 0; t < n; ++t) m[t] = {v3(tri + 9 * t), v3(tri + 9 * t + 3), v3(tri + 9 * t + 6)};
+  return m;
+}
+std::vector<V3> pts_from(const double* p, int64_t n) {
+  std::vector<V3> v((size_t)n);
+  for (int64_t i = 0; i < n; ++i) v[i] = v3(p + 3 * i);
+  return v;
+}
+RegionBox region_from(const double* r) {
+  RegionBox b;
+  b.min = v3(r);
+  b.max = v3(r + 3);
+  return b;
+}
+}  // namespace
+
+int oracle_bake_grid(const double* tri, int64_t n, double voxel, double padding, double* origin, int32_t* dims) {
+  return guarded(nullptr, [&] {
+    V3 o;
+    int d[3];
+    bake_grid(mesh_from(tri, n), voxel, padding, o, d);
+    put(origin, o);
+    for (int k = 0; k < 3; ++k) dims[k] = d[k];
+  });
+}
+int oracle_bake_mesh_sdf(const double* tri, int64_t n, double voxel, double padding, float* samples, int64_t cap) {
+  return guarded(nullptr, [&] {
+    SdfVolume v = bake_mesh_sdf(mesh_from(tri, n), voxel, padding);
+    if ((int64_t)v.samples.size() > cap) throw std::invalid_argument("bake_mesh_sdf: samples capacity");
+    std::memcpy(samples, v.samples.data(), v.samples.size() * sizeof(float));
+  });
+}
+void oracle_make_box_mesh(const double* half, const double* center, double* tri) {
+  TriangleMesh m = make_box_mesh(v3(half), center ? v3(center) : V3::Zero());
+  for (size_t t = 0; t < m.size(); ++t) {
+    put(tri + 9 * t, m[t].a);
+    put(tri + 9 * t + 3, m[t].b);
+    put(tri + 9 * t + 6, m[t].c);
+  }
+}
+int oracle_metric_fill(int64_t n, const double* x, const double* v, const double* region, double* fraction,
+                       double* max_speed, int32_t* success) {
+  return guarded(nullptr, [&] {
+    FillResult r = metric_fill(pts_from(x, n), pts_from(v, n), region_from(region));
+    *fraction = r.fraction;
+    *max_speed = r.max_speed;
+    *success = r.success;
+  });
+}
+int oracle_render_heightmap(int64_t n, const double* x, const double* region, int nx, int ny, double* out) {
+  return guarded(nullptr, [&] {
+    DepthMap m = render_heightmap(pts_from(x, n), region_from(region), nx, ny);
+    std::memcpy(out, m.samples.data(), m.samples.size() * sizeof(double));
+  });
+}
+int oracle_metric_write_iou(int nx, int ny, double threshold, const double* a, const double* b, double* iou,
+                            int32_t* success) {
+  return guarded(nullptr, [&] {
+    DepthMap ma, mb;
+    ma.nx = mb.nx = nx;
+    ma.ny = mb.ny = ny;
+    ma.threshold = mb.threshold = threshold;
+    ma.samples.assign(a, a + (size_t)nx * ny);
+    mb.samples.assign(b, b + (size_t)nx * ny);
+    IouResult r = metric_write_iou(ma, mb);
+    *iou = r.iou;
+    *success = r.success;
+  });
+}
+int oracle_chamfer(int64_t na, const double* a, int64_t nb, const double* b, double* out) {
+  return guarded(nullptr, [&] { *out = chamfer_distance(pts_from(a, na), pts_from(b, nb)); });
+}
+int oracle_metric_pinch(int64_t nc, const double* cur, int64_t ni, const double* init, int64_t nt,
+                        const double* tgt, double* ratio, int32_t* success) {
+  return guarded(nullptr, [&] {
+    PinchResult r = metric_pinch(pts_from(cur, nc), pts_from(init, ni), pts_from(tgt, nt));
+    *ratio = r.ratio;
+    *success = r.success;
+  });
+}
+
 }  // extern "C"
+

@@ -14,9 +14,10 @@ def test_ported_reference_kats_pass():
     passed = [l for l in out.splitlines() if l.startswith("PASS")]
     # every hot-path suite of the reference is represented
     for suite in ("P2g.", "GridUpdate.", "G2p.", "Stress.", "ReturnMap.", "Substep.", "SdfEval.",
-                  "SdfGradient.", "PenaltyParticle.", "PenaltyGrid.", "EnvStep.", "Acceptance."):
+                  "SdfGradient.", "PenaltyParticle.", "PenaltyGrid.", "EnvStep.", "Acceptance.",
+                  "BakeMesh.", "Fill.", "Heightmap.", "WriteIou.", "Chamfer.", "Pinch."):
         assert any(suite in l for l in passed), suite
-    assert len(passed) >= 50
+    assert len(passed) >= 85
 
 
 def test_oracle_seeding_matches_library_seeding():
