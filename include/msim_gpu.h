@@ -256,6 +256,55 @@ int msim_gpu_kernel_stats(msim_gpu_ctx* ctx, int id, const char** name, int64_t*
 int msim_gpu_constitutive(msim_gpu_ctx* ctx, int mat, int64_t n, const double* F, double* tau,
                           double* Fp);
 
+/* ---- task metrics over every env's device state -------
+ * The reference evaluates these on the host particle vector after the
+ * episode (scenario.hpp:63-209); here one launch covers all envs and only the
+ * per-env results cross PCIe. Positions / velocities are the stored fp32
+ * values promoted to double; all particles count, lost ones included (the
+ * reference's `w.soft.particles`). Results are bit-identical to the reference
+ * formulas on those values, except chamfer means (summation order, ~1e-15). */
+typedef struct msim_region {       /* RegionBox (scenario.hpp:18-30) */
+  double min[3];
+  double max[3];
+} msim_region;
+typedef struct msim_fill_result {  /* FillResult (scenario.hpp:55-59) */
+  double fraction;
+  double max_speed;
+  int32_t success;
+  int32_t _pad;
+} msim_fill_result;
+/* metric_fill (scenario.hpp:63-75) per env; regions[n_env], out[n_env]. */
+int msim_gpu_metric_fill(msim_gpu_ctx* ctx, const msim_region* regions, msim_fill_result* out);
+/* render_heightmap (scenario.hpp:79-98) per env into maps[n_env*ny*nx]
+ * (x fastest, heights above the region floor, 0 where no particle). */
+int msim_gpu_render_heightmap(msim_gpu_ctx* ctx, const msim_region* regions, int nx, int ny, double* maps);
+/* render_heightmap + metric_write_iou (scenario.hpp:106-119) against
+ * targets[n_env*ny*nx] with the occupancy threshold; iou/success per env. */
+int msim_gpu_metric_write_iou(msim_gpu_ctx* ctx, const msim_region* regions, int nx, int ny,
+                              double threshold, const double* targets, double* iou, int32_t* success);
+/* chamfer_distance (scenario.hpp:179-190) of each env's particles against
+ * points[offsets[e]*3 .. offsets[e+1]*3); out[n_env]. */
+int msim_gpu_chamfer(msim_gpu_ctx* ctx, const double* points, const int64_t* offsets, double* out);
+/* metric_pinch (scenario.hpp:199-209) per env: current = the env's particles;
+ * initial / target point sets per env with their offsets. */
+int msim_gpu_metric_pinch(msim_gpu_ctx* ctx, const double* initial, const int64_t* initial_offsets,
+                          const double* target, const int64_t* target_offsets, double* ratio,
+                          int32_t* success);
+
+/* ---- mesh SDF baking ----------------------------------
+ * bake_mesh_sdf (sdf.hpp:277-310) on a GPU: triangles tri[n_tri*9] (a, b, c
+ * per triangle). msim_bake_grid returns the volume's origin and dims (host
+ * only, same validation and errors as the reference); msim_gpu_bake_mesh_sdf
+ * fills samples[dims product] (f32, x fastest), bit-identical to the reference
+ * algorithm in double. Errors: MSIM_ERR_INVALID (empty / degenerate mesh,
+ * voxel <= 0, capacity), MSIM_ERR_DEVICE; message via msim_gpu_create_error(). */
+int msim_bake_grid(const double* tri, int64_t n_tri, double voxel, double padding, double* origin,
+                   int32_t* dims);
+int msim_gpu_bake_mesh_sdf(int device, const double* tri, int64_t n_tri, double voxel, double padding,
+                           float* samples, int64_t samples_cap);
+/* make_box_mesh (sdf.hpp:443-455): 12 outward-wound triangles into tri[108]. */
+void msim_make_box_mesh(const double* half_extents, const double* center, double* tri);
+
 /* ---- host-side reference utilities (no device work) --------------------- */
 /* seed_particles_box (seeding.hpp:13-35) with a caller-held mt19937_64 state.
  * Returns the particle count; if x != NULL writes positions (n*3) and mass. */

@@ -73,6 +73,14 @@ _SIGS = {
     "oracle_seed_box": (C.c_int64, [_vp, _vp, _dp, _dp, C.c_int, C.c_double]),
     "oracle_lattice_count": (C.c_int64, [_dp, _dp, C.c_double]),
     "oracle_time_env_steps": (C.c_double, [_vp, C.c_int, _ip]),
+    "oracle_bake_grid": (C.c_int, [_dp, C.c_int64, C.c_double, C.c_double, _dp, _ip]),
+    "oracle_bake_mesh_sdf": (C.c_int, [_dp, C.c_int64, C.c_double, C.c_double, C.POINTER(C.c_float), C.c_int64]),
+    "oracle_make_box_mesh": (None, [_dp, _dp, _dp]),
+    "oracle_metric_fill": (C.c_int, [C.c_int64, _dp, _dp, _dp, _dp, _dp, _ip]),
+    "oracle_render_heightmap": (C.c_int, [C.c_int64, _dp, _dp, C.c_int, C.c_int, _dp]),
+    "oracle_metric_write_iou": (C.c_int, [C.c_int, C.c_int, C.c_double, _dp, _dp, _dp, _ip]),
+    "oracle_chamfer": (C.c_int, [C.c_int64, _dp, C.c_int64, _dp, _dp]),
+    "oracle_metric_pinch": (C.c_int, [C.c_int64, _dp, C.c_int64, _dp, C.c_int64, _dp, _dp, _ip]),
 }
 
 _lib = None
@@ -285,3 +293,79 @@ def run_kats() -> tuple[int, str]:
         build()
     r = subprocess.run([KAT], capture_output=True, text=True)
     return r.returncode, r.stdout
+
+
+# ---- task metrics and mesh baking (msim_oracle_tasks.hpp) -------------------
+def _arr(a):
+    a = np.ascontiguousarray(a, dtype=np.float64)
+    return a, a.ctypes.data_as(_dp)
+
+
+def bake_mesh_sdf(tri, voxel, padding):
+    """bake_mesh_sdf (sdf.hpp:277-310) -> (origin[3], dims[3], samples f32 x-fastest)."""
+    lib = load()
+    t, tp = _arr(tri)
+    n = t.size // 9
+    origin, dims = np.zeros(3), np.zeros(3, np.int32)
+    rc = lib.oracle_bake_grid(tp, n, voxel, padding, origin.ctypes.data_as(_dp), dims.ctypes.data_as(_ip))
+    if rc:
+        raise ValueError("bake_mesh_sdf: invalid mesh")
+    out = np.zeros(int(np.prod(dims)), np.float32)
+    assert lib.oracle_bake_mesh_sdf(tp, n, voxel, padding, out.ctypes.data_as(C.POINTER(C.c_float)), out.size) == 0
+    return origin, dims, out
+
+
+def make_box_mesh(half, center=(0.0, 0.0, 0.0)):
+    lib = load()
+    h, hp = _arr(half)
+    c, cp = _arr(center)
+    tri = np.zeros(108)
+    lib.oracle_make_box_mesh(hp, cp, tri.ctypes.data_as(_dp))
+    return tri
+
+
+def metric_fill(x, v, region):
+    lib = load()
+    xa, xp = _arr(x)
+    va, vp = _arr(v)
+    r, rp = _arr(region)
+    f, m, s = C.c_double(), C.c_double(), C.c_int32()
+    assert lib.oracle_metric_fill(len(xa), xp, vp, rp, C.byref(f), C.byref(m), C.byref(s)) == 0
+    return f.value, m.value, bool(s.value)
+
+
+def render_heightmap(x, region, nx, ny):
+    lib = load()
+    xa, xp = _arr(x)
+    r, rp = _arr(region)
+    out = np.zeros(nx * ny)
+    assert lib.oracle_render_heightmap(len(xa), xp, rp, nx, ny, out.ctypes.data_as(_dp)) == 0
+    return out
+
+
+def metric_write_iou(nx, ny, threshold, a, b):
+    lib = load()
+    aa, ap = _arr(a)
+    ba, bp = _arr(b)
+    iou, s = C.c_double(), C.c_int32()
+    assert lib.oracle_metric_write_iou(nx, ny, threshold, ap, bp, C.byref(iou), C.byref(s)) == 0
+    return iou.value, bool(s.value)
+
+
+def chamfer(a, b):
+    lib = load()
+    aa, ap = _arr(a)
+    ba, bp = _arr(b)
+    out = C.c_double()
+    assert lib.oracle_chamfer(len(aa), ap, len(ba), bp, C.byref(out)) == 0
+    return out.value
+
+
+def metric_pinch(cur, init, tgt):
+    lib = load()
+    c, cp = _arr(cur)
+    i, ip = _arr(init)
+    t, tp = _arr(tgt)
+    r, s = C.c_double(), C.c_int32()
+    assert lib.oracle_metric_pinch(len(c), cp, len(i), ip, len(t), tp, C.byref(r), C.byref(s)) == 0
+    return r.value, bool(s.value)

@@ -9,6 +9,6 @@ from . import abi
 abi.load()
 
 from .scenes import CONFIGS, Scene  # noqa: E402
-from .world import DeviceError, GpuWorld, SimulationDiverged  # noqa: E402
+from .world import DeviceError, GpuWorld, SimulationDiverged, bake_mesh_sdf, make_box_mesh  # noqa: E402
 
-__all__ = ["abi", "CONFIGS", "Scene", "GpuWorld", "SimulationDiverged", "DeviceError"]
+__all__ = ["abi", "CONFIGS", "Scene", "GpuWorld", "SimulationDiverged", "DeviceError", "bake_mesh_sdf", "make_box_mesh"]

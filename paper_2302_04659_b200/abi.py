@@ -107,6 +107,14 @@ class StepReport(C.Structure):
     ]
 
 
+class Region(C.Structure):  # msim_region = RegionBox (scenario.hpp:18-30)
+    _fields_ = [("min", C.c_double * 3), ("max", C.c_double * 3)]
+
+
+class FillResult(C.Structure):  # msim_fill_result = FillResult (scenario.hpp:55-59)
+    _fields_ = [("fraction", C.c_double), ("max_speed", C.c_double), ("success", C.c_int32), ("_pad", C.c_int32)]
+
+
 # Every symbol include/msim_gpu.h declares (checked by tests/test_abi.py).
 EXPORTED = [
     "msim_gpu_create", "msim_gpu_destroy", "msim_gpu_last_error", "msim_gpu_create_error",
@@ -123,6 +131,8 @@ EXPORTED = [
     "msim_gpu_read_all_wrenches", "msim_gpu_stream", "msim_gpu_launches", "msim_gpu_set_kernel_timing",
     "msim_gpu_kernel_count", "msim_gpu_kernel_stats",
     "msim_seed_box_count", "msim_seed_box",
+    "msim_gpu_metric_fill", "msim_gpu_render_heightmap", "msim_gpu_metric_write_iou", "msim_gpu_chamfer",
+    "msim_gpu_metric_pinch", "msim_bake_grid", "msim_gpu_bake_mesh_sdf", "msim_make_box_mesh",
 ]
 
 _dp = C.POINTER(C.c_double)
@@ -177,6 +187,14 @@ _SIGS = {
     "msim_gpu_kernel_count": (C.c_int, []),
     "msim_gpu_kernel_stats": (C.c_int, [_vp, C.c_int, C.POINTER(C.c_char_p), _lp, _dp]),
     "msim_seed_box": (C.c_int64, [_vp, _dp, _dp, C.c_double, C.c_double, _dp, _dp]),
+    "msim_gpu_metric_fill": (C.c_int, [_vp, C.POINTER(Region), C.POINTER(FillResult)]),
+    "msim_gpu_render_heightmap": (C.c_int, [_vp, C.POINTER(Region), C.c_int, C.c_int, _dp]),
+    "msim_gpu_metric_write_iou": (C.c_int, [_vp, C.POINTER(Region), C.c_int, C.c_int, C.c_double, _dp, _dp, _ip]),
+    "msim_gpu_chamfer": (C.c_int, [_vp, _dp, _lp, _dp]),
+    "msim_gpu_metric_pinch": (C.c_int, [_vp, _dp, _lp, _dp, _lp, _dp, _ip]),
+    "msim_bake_grid": (C.c_int, [_dp, C.c_int64, C.c_double, C.c_double, _dp, _ip]),
+    "msim_gpu_bake_mesh_sdf": (C.c_int, [C.c_int, _dp, C.c_int64, C.c_double, C.c_double, C.POINTER(C.c_float), C.c_int64]),
+    "msim_make_box_mesh": (None, [_dp, _dp, _dp]),
 }
 
 _lib = None

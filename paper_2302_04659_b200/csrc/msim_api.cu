@@ -1127,6 +1127,301 @@ int msim_gpu_constitutive(msim_gpu_ctx* c, int mat, int64_t n, const double* F, 
 }
 
 
+// ---- task metrics (scenario.hpp:63-209) -----------------------------------
+namespace {
+bool region_ok(const msim_region& r) {  // RegionBox::validate (scenario.hpp:26-29)
+  return std::min({r.max[0] - r.min[0], r.max[1] - r.min[1], r.max[2] - r.min[2]}) > 0.0;
+}
+// regions of all envs to the device (6 doubles per env)
+int upload_regions(msim_gpu_ctx* c, const msim_region* regions, DevBuf& buf) {
+  if (!regions) return fail(c, MSIM_ERR_INVALID, "metric: regions required");
+  for (int e = 0; e < c->n_env; ++e)
+    if (!region_ok(regions[e])) return fail(c, MSIM_ERR_INVALID, "RegionBox: extents must be positive");
+  std::vector<double> h(6 * (size_t)c->n_env);
+  for (int e = 0; e < c->n_env; ++e)
+    for (int k = 0; k < 3; ++k) {
+      h[6 * e + k] = regions[e].min[k];
+      h[6 * e + 3 + k] = regions[e].max[k];
+    }
+  CK(buf.ensure(sizeof(double) * h.size()));
+  CK(cudaMemcpyAsync(buf.p, h.data(), sizeof(double) * h.size(), cudaMemcpyHostToDevice, c->stream));
+  return MSIM_OK;
+}
+int heightmaps(msim_gpu_ctx* c, const msim_region* regions, int nx, int ny, DevBuf& maps, DevBuf& reg) {
+  int rc = upload_regions(c, regions, reg);
+  if (rc) return rc;
+  if (nx < 2 || ny < 2) return fail(c, MSIM_ERR_INVALID, "render_heightmap: resolution must be >= 2x2");
+  const size_t cells = (size_t)nx * ny * c->n_env;
+  CK(maps.ensure(sizeof(double) * cells));
+  CK(cudaMemsetAsync(maps.p, 0, sizeof(double) * cells, c->stream));  // +0.0
+  launch_heightmap(params(c), reg.as<double>(), nx, ny, maps.as<unsigned long long>(), c->stream);
+  CK(cudaGetLastError());
+  return MSIM_OK;
+}
+// per-env chamfer of device point sets A (offsets offA) and B (offB); out[n_env]
+void chamfer_sets(msim_gpu_ctx* c, const double* A, const long long* offA_d, const std::vector<long long>& offA,
+                  const double* B, const long long* offB_d, const std::vector<long long>& offB, double* out) {
+  const int ne = c->n_env;
+  long long maxa = 0, maxb = 0;
+  for (int e = 0; e < ne; ++e) {
+    maxa = std::max(maxa, offA[e + 1] - offA[e]);
+    maxb = std::max(maxb, offB[e + 1] - offB[e]);
+  }
+  DevBuf mind, means;
+  CK(mind.ensure(sizeof(double) * (size_t)std::max(offA[ne], offB[ne]) + 16));
+  CK(means.ensure(sizeof(double) * 2 * ne));
+  double* mab = means.as<double>();
+  double* mba = mab + ne;
+  launch_chamfer_side(A, offA_d, maxa, B, offB_d, ne, mind.as<double>(), mab, c->stream);
+  launch_chamfer_side(B, offB_d, maxb, A, offA_d, ne, mind.as<double>(), mba, c->stream);
+  CK(cudaGetLastError());
+  std::vector<double> h(2 * (size_t)ne);
+  CK(cudaMemcpyAsync(h.data(), means.p, sizeof(double) * 2 * ne, cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  for (int e = 0; e < ne; ++e) out[e] = h[e] + h[ne + e];  // ab / |a| + ba / |b|
+}
+// host point sets (per-env offsets) to the device; checks non-empty sets
+int upload_points(msim_gpu_ctx* c, const double* pts, const int64_t* off, DevBuf& buf, DevBuf& off_d,
+                  std::vector<long long>& off_h) {
+  if (!pts || !off) return fail(c, MSIM_ERR_INVALID, "chamfer_distance: point sets required");
+  off_h.assign(off, off + c->n_env + 1);
+  for (int e = 0; e < c->n_env; ++e)
+    if (off_h[e + 1] <= off_h[e]) return fail(c, MSIM_ERR_INVALID, "chamfer_distance: point sets must be non-empty");
+  const long long base = off_h[0];
+  for (auto& o : off_h) o -= base;
+  CK(buf.ensure(sizeof(double) * 3 * (size_t)off_h[c->n_env] + 16));
+  CK(off_d.ensure(sizeof(long long) * (c->n_env + 1)));
+  CK(cudaMemcpyAsync(buf.p, pts + 3 * base, sizeof(double) * 3 * off_h[c->n_env], cudaMemcpyHostToDevice, c->stream));
+  CK(cudaMemcpyAsync(off_d.p, off_h.data(), sizeof(long long) * (c->n_env + 1), cudaMemcpyHostToDevice, c->stream));
+  return MSIM_OK;
+}
+int particle_points(msim_gpu_ctx* c, DevBuf& pos) {
+  for (int e = 0; e < c->n_env; ++e)
+    if (c->env_off_h[e + 1] <= c->env_off_h[e])
+      return fail(c, MSIM_ERR_INVALID, "chamfer_distance: point sets must be non-empty");
+  CK(pos.ensure(sizeof(double) * 3 * (size_t)std::max<long long>(c->n, 1)));
+  launch_positions(params(c), pos.as<double>(), c->stream);
+  CK(cudaGetLastError());
+  return MSIM_OK;
+}
+}  // namespace
+
+int msim_gpu_metric_fill(msim_gpu_ctx* c, const msim_region* regions, msim_fill_result* out) {
+  return guarded(c, [&]() -> int {
+    if (!out) return fail(c, MSIM_ERR_INVALID, "metric_fill: out required");
+    for (int e = 0; e < c->n_env; ++e)
+      if (c->env_off_h.empty() || c->env_off_h[e + 1] == c->env_off_h[e])
+        return fail(c, MSIM_ERR_INVALID, "metric_fill: no particles");
+    set_device(c);
+    DevBuf reg, acc;
+    int rc = upload_regions(c, regions, reg);
+    if (rc) return rc;
+    CK(acc.ensure(sizeof(unsigned long long) * 2 * c->n_env));
+    CK(cudaMemsetAsync(acc.p, 0, sizeof(unsigned long long) * 2 * c->n_env, c->stream));
+    unsigned long long* inside = acc.as<unsigned long long>();
+    launch_fill(params(c), reg.as<double>(), inside, inside + c->n_env, c->stream);
+    CK(cudaGetLastError());
+    std::vector<unsigned long long> h(2 * (size_t)c->n_env);
+    CK(cudaMemcpyAsync(h.data(), acc.p, sizeof(unsigned long long) * h.size(), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    for (int e = 0; e < c->n_env; ++e) {
+      const double n = (double)(c->env_off_h[e + 1] - c->env_off_h[e]);
+      out[e].fraction = (double)h[e] / n;
+      std::memcpy(&out[e].max_speed, &h[c->n_env + e], sizeof(double));
+      out[e].success = out[e].fraction > 0.9 && out[e].max_speed < 0.05;
+      out[e]._pad = 0;
+    }
+    return MSIM_OK;
+  });
+}
+
+int msim_gpu_render_heightmap(msim_gpu_ctx* c, const msim_region* regions, int nx, int ny, double* maps) {
+  return guarded(c, [&]() -> int {
+    if (!maps) return fail(c, MSIM_ERR_INVALID, "render_heightmap: maps required");
+    set_device(c);
+    DevBuf m, reg;
+    int rc = heightmaps(c, regions, nx, ny, m, reg);
+    if (rc) return rc;
+    CK(cudaMemcpyAsync(maps, m.p, sizeof(double) * (size_t)nx * ny * c->n_env, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    return MSIM_OK;
+  });
+}
+
+int msim_gpu_metric_write_iou(msim_gpu_ctx* c, const msim_region* regions, int nx, int ny, double threshold,
+                              const double* targets, double* iou, int32_t* success) {
+  return guarded(c, [&]() -> int {
+    if (!targets || !iou || !success) return fail(c, MSIM_ERR_INVALID, "metric_write_iou: null argument");
+    set_device(c);
+    DevBuf m, reg, tg, res;
+    int rc = heightmaps(c, regions, nx, ny, m, reg);
+    if (rc) return rc;
+    const size_t cells = (size_t)nx * ny;
+    CK(tg.ensure(sizeof(double) * cells * c->n_env));
+    CK(cudaMemcpyAsync(tg.p, targets, sizeof(double) * cells * c->n_env, cudaMemcpyHostToDevice, c->stream));
+    CK(res.ensure((sizeof(double) + sizeof(int)) * c->n_env));
+    double* di = res.as<double>();
+    int* ds = reinterpret_cast<int*>(di + c->n_env);
+    launch_iou(m.as<double>(), tg.as<double>(), c->n_env, (int)cells, threshold, di, ds, c->stream);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(iou, di, sizeof(double) * c->n_env, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(success, ds, sizeof(int) * c->n_env, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    return MSIM_OK;
+  });
+}
+
+int msim_gpu_chamfer(msim_gpu_ctx* c, const double* points, const int64_t* offsets, double* out) {
+  return guarded(c, [&]() -> int {
+    if (!out) return fail(c, MSIM_ERR_INVALID, "chamfer_distance: out required");
+    set_device(c);
+    DevBuf pos, pts, off_d;
+    std::vector<long long> off_h;
+    int rc = particle_points(c, pos);
+    if (!rc) rc = upload_points(c, points, offsets, pts, off_d, off_h);
+    if (rc) return rc;
+    chamfer_sets(c, pos.as<double>(), c->env_off_d.as<long long>(), c->env_off_h, pts.as<double>(),
+                 off_d.as<long long>(), off_h, out);
+    return MSIM_OK;
+  });
+}
+
+int msim_gpu_metric_pinch(msim_gpu_ctx* c, const double* initial, const int64_t* initial_offsets,
+                          const double* target, const int64_t* target_offsets, double* ratio, int32_t* success) {
+  return guarded(c, [&]() -> int {
+    if (!ratio || !success) return fail(c, MSIM_ERR_INVALID, "metric_pinch: null argument");
+    set_device(c);
+    DevBuf pos, ini, ini_off, tgt, tgt_off;
+    std::vector<long long> ini_h, tgt_h;
+    int rc = upload_points(c, initial, initial_offsets, ini, ini_off, ini_h);
+    if (!rc) rc = upload_points(c, target, target_offsets, tgt, tgt_off, tgt_h);
+    if (!rc) rc = particle_points(c, pos);
+    if (rc) return rc;
+    std::vector<double> t(c->n_env), d(c->n_env);
+    chamfer_sets(c, ini.as<double>(), ini_off.as<long long>(), ini_h, tgt.as<double>(), tgt_off.as<long long>(),
+                 tgt_h, t.data());
+    chamfer_sets(c, pos.as<double>(), c->env_off_d.as<long long>(), c->env_off_h, tgt.as<double>(),
+                 tgt_off.as<long long>(), tgt_h, d.data());
+    for (int e = 0; e < c->n_env; ++e) {  // scenario.hpp:205-207
+      ratio[e] = t[e] > 0.0 ? d[e] / t[e] : (d[e] == 0.0 ? 0.0 : std::numeric_limits<double>::infinity());
+      success[e] = d[e] < 0.3 * t[e];
+    }
+    return MSIM_OK;
+  });
+}
+
+// ---- mesh SDF baking (sdf.hpp:277-310) -------------------------------------
+namespace {
+struct hv3 {
+  double x, y, z;
+};
+hv3 hsub(hv3 a, hv3 b) { return {a.x - b.x, a.y - b.y, a.z - b.z}; }
+hv3 hcross(hv3 a, hv3 b) { return {a.y * b.z - a.z * b.y, a.z * b.x - a.x * b.z, a.x * b.y - a.y * b.x}; }
+double hnorm(hv3 a) { return std::sqrt(a.x * a.x + a.y * a.y + a.z * a.z); }
+hv3 tri_v(const double* tri, int64_t t, int k) { return {tri[9 * t + 3 * k], tri[9 * t + 3 * k + 1], tri[9 * t + 3 * k + 2]}; }
+
+// the grid of bake_mesh_sdf (sdf.hpp:277-296) with the reference's checks
+bool bake_grid_impl(const double* tri, int64_t n, double voxel, double padding, double* origin, int* dims,
+                    std::string& err) {
+  if (!tri || n <= 0) {
+    err = "bake_mesh_sdf: empty mesh";
+    return false;
+  }
+  if (voxel <= 0.0) {
+    err = "bake_mesh_sdf: voxel size must be > 0";
+    return false;
+  }
+  bool degenerate = true;
+  double lo[3] = {tri[0], tri[1], tri[2]}, hi[3] = {tri[0], tri[1], tri[2]};
+  for (int64_t t = 0; t < n; ++t) {
+    for (int v = 0; v < 3; ++v)
+      for (int k = 0; k < 3; ++k) {
+        lo[k] = std::min(lo[k], tri[9 * t + 3 * v + k]);
+        hi[k] = std::max(hi[k], tri[9 * t + 3 * v + k]);
+      }
+    const hv3 a = tri_v(tri, t, 0), b = tri_v(tri, t, 1), c = tri_v(tri, t, 2);
+    if (hnorm(hcross(hsub(b, a), hsub(c, a))) > 1e-14) degenerate = false;
+  }
+  if (degenerate) {
+    err = "bake_mesh_sdf: mesh has only zero-area triangles";
+    return false;
+  }
+  for (int k = 0; k < 3; ++k) {
+    origin[k] = lo[k] - padding;
+    const double span = hi[k] - lo[k] + 2.0 * padding;
+    dims[k] = std::max(2, static_cast<int>(std::ceil(span / voxel)) + 1);
+  }
+  return true;
+}
+}  // namespace
+
+int msim_bake_grid(const double* tri, int64_t n_tri, double voxel, double padding, double* origin, int32_t* dims) {
+  g_create_error.clear();
+  int d[3];
+  double o[3];
+  if (!bake_grid_impl(tri, n_tri, voxel, padding, o, d, g_create_error)) return MSIM_ERR_INVALID;
+  for (int k = 0; k < 3; ++k) {
+    if (origin) origin[k] = o[k];
+    if (dims) dims[k] = d[k];
+  }
+  return MSIM_OK;
+}
+
+int msim_gpu_bake_mesh_sdf(int device, const double* tri, int64_t n_tri, double voxel, double padding,
+                           float* samples, int64_t samples_cap) {
+  g_create_error.clear();
+  int d[3];
+  double o[3];
+  if (!bake_grid_impl(tri, n_tri, voxel, padding, o, d, g_create_error)) return MSIM_ERR_INVALID;
+  const long long nvox = (long long)d[0] * d[1] * d[2];
+  if (!samples || samples_cap < nvox) {
+    g_create_error = "bake_mesh_sdf: samples capacity below dims product";
+    return MSIM_ERR_INVALID;
+  }
+  // the three parity rays of sdf.hpp:258-262, normalized as Vec3::normalized()
+  const double raw[9] = {1.0, 0.0, 0.0, 1.0, 0.137, 0.071, 1.0, -0.083, 0.143};
+  double dirs[9];
+  for (int r = 0; r < 3; ++r) {
+    const double nn = hnorm({raw[3 * r], raw[3 * r + 1], raw[3 * r + 2]});
+    for (int k = 0; k < 3; ++k) dirs[3 * r + k] = raw[3 * r + k] / nn;
+  }
+  try {
+    CK(cudaSetDevice(device));
+    cudaStream_t s;
+    CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    DevBuf tri_d, out_d;
+    CK(tri_d.ensure(sizeof(double) * 9 * n_tri));
+    CK(out_d.ensure(sizeof(float) * nvox));
+    CK(cudaMemcpyAsync(tri_d.p, tri, sizeof(double) * 9 * n_tri, cudaMemcpyHostToDevice, s));
+    launch_bake(tri_d.as<double>(), n_tri, o, voxel, d, dirs, out_d.as<float>(), s);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(samples, out_d.p, sizeof(float) * nvox, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    CK(cudaStreamDestroy(s));
+  } catch (const CudaError& e) {
+    g_create_error = std::string("CUDA error ") + cudaGetErrorString(e.e) + " at " + e.what;
+    return MSIM_ERR_DEVICE;
+  }
+  return MSIM_OK;
+}
+
+// make_box_mesh (sdf.hpp:443-455)
+void msim_make_box_mesh(const double* h, const double* center, double* tri) {
+  const double c0[3] = {0.0, 0.0, 0.0};
+  const double* c = center ? center : c0;
+  double v[8][3];
+  for (int i = 0; i < 8; ++i) {
+    v[i][0] = c[0] + ((i & 1) ? h[0] : -h[0]);
+    v[i][1] = c[1] + ((i & 2) ? h[1] : -h[1]);
+    v[i][2] = c[2] + ((i & 4) ? h[2] : -h[2]);
+  }
+  static const int f[12][3] = {{0, 2, 1}, {1, 2, 3}, {4, 5, 6}, {5, 7, 6}, {0, 1, 4}, {1, 5, 4},
+                               {2, 6, 3}, {3, 6, 7}, {0, 4, 2}, {2, 4, 6}, {1, 3, 5}, {3, 7, 5}};
+  for (int t = 0; t < 12; ++t)
+    for (int k = 0; k < 3; ++k)
+      for (int a = 0; a < 3; ++a) tri[9 * t + 3 * k + a] = v[f[t][k]][a];
+}
+
 void* msim_gpu_stream(msim_gpu_ctx* c) { return c ? (void*)c->stream : nullptr; }
 
 int64_t msim_gpu_launches(const msim_gpu_ctx* c) { return c ? c->timer.launches : -1; }

@@ -288,4 +288,17 @@ void launch_iteration_end(const SimParams& P, cudaStream_t s);
 // Dynamic shared memory opt-in for the particle kernel (call once per device).
 void configure_kernels();
 
+// msim_tasks.cu (compiled with --fmad=false): mesh SDF bake and task metrics
+void launch_bake(const double* tri, long long n_tri, const double* origin, double voxel, const int* dims,
+                 const double* dirs, float* out, cudaStream_t s);
+void launch_fill(const SimParams& P, const double* regions, unsigned long long* inside, unsigned long long* vmax_bits,
+                 cudaStream_t s);
+void launch_heightmap(const SimParams& P, const double* regions, int nx, int ny, unsigned long long* maps,
+                      cudaStream_t s);
+void launch_iou(const double* maps, const double* targets, int n_env, int cells, double threshold, double* iou,
+                int* success, cudaStream_t s);
+void launch_positions(const SimParams& P, double* pos, cudaStream_t s);
+void launch_chamfer_side(const double* A, const long long* offA, long long max_na, const double* B,
+                         const long long* offB, int n_env, double* mind, double* mean_out, cudaStream_t s);
+
 }  // namespace msim_impl

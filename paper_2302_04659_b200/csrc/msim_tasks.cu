@@ -1,0 +1,287 @@
+// Device side of the consumers of the soft-body state that SURVEY.md §8(f)
+// ranks next after the substep (reference paths relative to
+// /root/reference/proj/include/msim/):
+//   * mesh SDF baking, bake_mesh_sdf (sdf.hpp:203-310): one thread per voxel,
+//     triangles streamed through shared memory, exact point-triangle distance
+//     and the three-ray parity vote in fp64;
+//   * batched task metrics over every env's live particle state:
+//     metric_fill, render_heightmap, metric_write_iou, chamfer_distance /
+//     metric_pinch (scenario.hpp:63-209).
+// This file is compiled with --fmad=false: every fp64 expression below keeps
+// the reference's operation order with one rounding per operation, so baked
+// samples, heights, speeds and nearest distances are bit-identical to the
+// double-precision restatement fed the same inputs.
+#include <cfloat>
+#include <cstdint>
+
+#include "msim_internal.h"
+
+namespace msim_impl {
+namespace {
+
+struct d3 {
+  double x, y, z;
+};
+__device__ __forceinline__ d3 operator+(d3 a, d3 b) { return {a.x + b.x, a.y + b.y, a.z + b.z}; }
+__device__ __forceinline__ d3 operator-(d3 a, d3 b) { return {a.x - b.x, a.y - b.y, a.z - b.z}; }
+__device__ __forceinline__ d3 operator*(d3 a, double s) { return {a.x * s, a.y * s, a.z * s}; }
+__device__ __forceinline__ double dot(d3 a, d3 b) { return a.x * b.x + a.y * b.y + a.z * b.z; }
+__device__ __forceinline__ d3 cross(d3 a, d3 b) {
+  return {a.y * b.z - a.z * b.y, a.z * b.x - a.x * b.z, a.x * b.y - a.y * b.x};
+}
+__device__ __forceinline__ double norm(d3 a) { return sqrt(a.x * a.x + a.y * a.y + a.z * a.z); }
+
+// point_triangle_distance (sdf.hpp:214-237), same branch structure and order
+__device__ double point_triangle_distance(d3 p, d3 a, d3 b, d3 c) {
+  d3 ab = b - a, ac = c - a, ap = p - a;
+  double d1 = dot(ab, ap), d2 = dot(ac, ap);
+  if (d1 <= 0 && d2 <= 0) return norm(p - a);
+  d3 bp = p - b;
+  double d3_ = dot(ab, bp), d4 = dot(ac, bp);
+  if (d3_ >= 0 && d4 <= d3_) return norm(p - b);
+  double vc = d1 * d4 - d3_ * d2;
+  if (vc <= 0 && d1 >= 0 && d3_ <= 0) return norm(p - (a + ab * (d1 / (d1 - d3_))));
+  d3 cp = p - c;
+  double d5 = dot(ab, cp), d6 = dot(ac, cp);
+  if (d6 >= 0 && d5 <= d6) return norm(p - c);
+  double vb = d5 * d2 - d1 * d6;
+  if (vb <= 0 && d2 >= 0 && d6 <= 0) return norm(p - (a + ac * (d2 / (d2 - d6))));
+  double va = d3_ * d6 - d5 * d4;
+  if (va <= 0 && (d4 - d3_) >= 0 && (d5 - d6) >= 0) {
+    double w = (d4 - d3_) / ((d4 - d3_) + (d5 - d6));
+    return norm(p - (b + (c - b) * w));
+  }
+  double denom = 1.0 / (va + vb + vc);
+  d3 closest = a + ab * (vb * denom) + ac * (vc * denom);
+  return norm(p - closest);
+}
+
+// ray_hits_triangle (sdf.hpp:239-254), Moller-Trumbore
+__device__ bool ray_hits_triangle(d3 orig, d3 dir, d3 a, d3 b, d3 c) {
+  d3 e1 = b - a, e2 = c - a;
+  d3 pv = cross(dir, e2);
+  double det = dot(e1, pv);
+  if (fabs(det) < 1e-14) return false;
+  double inv = 1.0 / det;
+  d3 tv = orig - a;
+  double u = dot(tv, pv) * inv;
+  if (u < 0.0 || u > 1.0) return false;
+  d3 qv = cross(tv, e1);
+  double v = dot(dir, qv) * inv;
+  if (v < 0.0 || u + v > 1.0) return false;
+  double dist = dot(e2, qv) * inv;
+  return dist > 0.0;
+}
+
+constexpr int kBakeT = 128;
+
+// One thread per voxel (x-fastest, sdf.hpp:297-308); the mesh is streamed in
+// chunks of kBakeT triangles through shared memory, each chunk read by every
+// voxel of the block. Distance min and the three ray parities are one pass.
+__global__ void __launch_bounds__(kBakeT) k_bake(const double* __restrict__ tri, long long n_tri, d3 origin,
+                                                 double voxel, int dx, int dy, int dz, d3 r0, d3 r1, d3 r2,
+                                                 float* __restrict__ out) {
+  __shared__ double st[kBakeT * 9];
+  const long long nvox = (long long)dx * dy * dz;
+  const long long idx = (long long)blockIdx.x * kBakeT + threadIdx.x;
+  const bool valid = idx < nvox;
+  const int i = (int)(idx % dx), j = (int)((idx / dx) % dy), k = (int)(idx / ((long long)dx * dy));
+  const d3 p = origin + d3{voxel * i, voxel * j, voxel * k};  // origin + voxel * (i, j, k)
+  double d = DBL_MAX;
+  int c0 = 0, c1 = 0, c2 = 0;
+  for (long long base = 0; base < n_tri; base += kBakeT) {
+    const int cnt = (int)min((long long)kBakeT, n_tri - base);
+    __syncthreads();
+    for (int q = threadIdx.x; q < cnt * 9; q += kBakeT) st[q] = tri[base * 9 + q];
+    __syncthreads();
+    if (!valid) continue;
+    for (int t = 0; t < cnt; ++t) {
+      const double* s = st + 9 * t;
+      const d3 a = {s[0], s[1], s[2]}, b = {s[3], s[4], s[5]}, c = {s[6], s[7], s[8]};
+      const double e = point_triangle_distance(p, a, b, c);
+      d = (e < d) ? e : d;  // std::min(d, e)
+      c0 += ray_hits_triangle(p, r0, a, b, c);
+      c1 += ray_hits_triangle(p, r1, a, b, c);
+      c2 += ray_hits_triangle(p, r2, a, b, c);
+    }
+  }
+  if (!valid) return;
+  const int votes = (c0 & 1) + (c1 & 1) + (c2 & 1);
+  out[idx] = (float)(votes >= 2 ? -d : d);
+}
+
+// ---- task metrics --------------------------------------------------------
+
+__device__ __forceinline__ bool region_contains(const double* r, double x, double y, double z) {
+  return x >= r[0] && y >= r[1] && z >= r[2] && x <= r[3] && y <= r[4] && z <= r[5];
+}
+
+// metric_fill (scenario.hpp:63-75): per env count inside + max |v| (double of the stored fp32)
+__global__ void k_fill(SimParams P, const double* __restrict__ regions, unsigned long long* inside,
+                       unsigned long long* vmax_bits) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= P.n) return;
+  const Particles& q = P.cur;
+  const int env = (q.meta[i] >> 8) & kEnvMask;
+  const double x = q.x[0][i], y = q.x[1][i], z = q.x[2][i];
+  const double vx = q.v[0][i], vy = q.v[1][i], vz = q.v[2][i];
+  const double sp = sqrt(vx * vx + vy * vy + vz * vz);
+  if (region_contains(regions + 6 * env, x, y, z)) atomicAdd(inside + env, 1ull);
+  atomicMax(vmax_bits + env, (unsigned long long)__double_as_longlong(sp));  // sp >= 0: bit order = value order
+}
+
+// render_heightmap (scenario.hpp:79-98): per env nx*ny max heights above the region floor
+__global__ void k_heightmap(SimParams P, const double* __restrict__ regions, int nx, int ny,
+                            unsigned long long* maps) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= P.n) return;
+  const Particles& q = P.cur;
+  const int env = (q.meta[i] >> 8) & kEnvMask;
+  const double* r = regions + 6 * env;
+  const double x = q.x[0][i], y = q.x[1][i], z = q.x[2][i];
+  if (!region_contains(r, x, y, z)) return;
+  const double cell = (r[3] - r[0]) / nx, cy = (r[4] - r[1]) / ny;
+  const int ci = min(nx - 1, (int)((x - r[0]) / cell));
+  const int cj = min(ny - 1, (int)((y - r[1]) / cy));
+  const double hgt = z - r[2];  // >= 0 (contained): bit order = value order
+  atomicMax(maps + (long long)env * nx * ny + (long long)cj * nx + ci, (unsigned long long)__double_as_longlong(hgt));
+}
+
+// metric_write_iou (scenario.hpp:106-119), one block per env
+__global__ void k_iou(const double* __restrict__ maps, const double* __restrict__ targets, int cells,
+                      double threshold, double* iou, int* success) {
+  const int env = blockIdx.x;
+  const double* a = maps + (long long)env * cells;
+  const double* b = targets + (long long)env * cells;
+  unsigned inter = 0, uni = 0;
+  for (int c = threadIdx.x; c < cells; c += blockDim.x) {
+    const bool oa = a[c] < threshold, ob = b[c] < threshold;
+    inter += oa && ob;
+    uni += oa || ob;
+  }
+  __shared__ unsigned si[32], su[32];
+  for (int o = 16; o > 0; o >>= 1) {
+    inter += __shfl_xor_sync(0xffffffffu, inter, o);
+    uni += __shfl_xor_sync(0xffffffffu, uni, o);
+  }
+  const int w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  if ((threadIdx.x & 31) == 0) {
+    si[w] = inter;
+    su[w] = uni;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned ti = 0, tu = 0;
+    for (int k = 0; k < nw; ++k) {
+      ti += si[k];
+      tu += su[k];
+    }
+    const double r = tu == 0 ? 1.0 : (double)ti / (double)tu;
+    iou[env] = r;
+    success[env] = r > 0.8;
+  }
+}
+
+// particle positions of every env in upload (pid) order, fp32 -> double
+__global__ void k_positions(SimParams P, double* pos) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= P.n) return;
+  const long long j = P.cur.pid[i];
+  pos[3 * j + 0] = P.cur.x[0][i];
+  pos[3 * j + 1] = P.cur.x[1][i];
+  pos[3 * j + 2] = P.cur.x[2][i];
+}
+
+constexpr int kNnT = 128;
+
+// Nearest distance from every point of set A to set B, per env: blockIdx.y =
+// env, one query per thread, B streamed through shared memory. The minimum of
+// squared norms then one sqrt: sqrt is monotone and correctly rounded, so this
+// equals the minimum of the reference's per-pair norm() (scenario.hpp:168).
+__global__ void __launch_bounds__(kNnT) k_nearest(const double* __restrict__ A, const long long* __restrict__ offA,
+                                                  const double* __restrict__ B, const long long* __restrict__ offB,
+                                                  double* __restrict__ mind) {
+  __shared__ double sb[kNnT * 3];
+  const int env = blockIdx.y;
+  const long long a0 = offA[env], na = offA[env + 1] - a0;
+  const long long b0 = offB[env], nb = offB[env + 1] - b0;
+  const long long qi = (long long)blockIdx.x * kNnT + threadIdx.x;
+  if ((long long)blockIdx.x * kNnT >= na) return;  // block-uniform
+  const bool valid = qi < na;
+  double qx = 0, qy = 0, qz = 0;
+  if (valid) {
+    qx = A[3 * (a0 + qi)];
+    qy = A[3 * (a0 + qi) + 1];
+    qz = A[3 * (a0 + qi) + 2];
+  }
+  double best = __longlong_as_double(0x7ff0000000000000ll);  // +inf
+  for (long long base = 0; base < nb; base += kNnT) {
+    const int cnt = (int)min((long long)kNnT, nb - base);
+    __syncthreads();
+    for (int q = threadIdx.x; q < cnt * 3; q += kNnT) sb[q] = B[3 * (b0 + base) + q];
+    __syncthreads();
+    for (int t = 0; t < cnt; ++t) {
+      const double dx = sb[3 * t] - qx, dy = sb[3 * t + 1] - qy, dz = sb[3 * t + 2] - qz;
+      const double d2 = dx * dx + dy * dy + dz * dz;
+      best = d2 < best ? d2 : best;
+    }
+  }
+  if (valid) mind[a0 + qi] = sqrt(best);
+}
+
+// mean of a segmented array, one block per segment, fixed reduction order
+__global__ void k_segment_mean(const double* __restrict__ v, const long long* __restrict__ off, double* out) {
+  const int env = blockIdx.x;
+  const long long s = off[env], n = off[env + 1] - s;
+  double acc = 0.0;
+  for (long long k = threadIdx.x; k < n; k += blockDim.x) acc += v[s + k];
+  __shared__ double red[256];
+  red[threadIdx.x] = acc;
+  __syncthreads();
+  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+    if ((int)threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) out[env] = n > 0 ? red[0] / (double)n : 0.0;
+}
+
+inline unsigned nblk(long long n, int t = 256) { return (unsigned)((n + t - 1) / t); }
+
+}  // namespace
+
+void launch_bake(const double* tri, long long n_tri, const double* origin, double voxel, const int* dims,
+                 const double* dirs, float* out, cudaStream_t s) {
+  const long long nvox = (long long)dims[0] * dims[1] * dims[2];
+  k_bake<<<nblk(nvox, kBakeT), kBakeT, 0, s>>>(tri, n_tri, d3{origin[0], origin[1], origin[2]}, voxel, dims[0],
+                                                 dims[1], dims[2], d3{dirs[0], dirs[1], dirs[2]},
+                                                 d3{dirs[3], dirs[4], dirs[5]}, d3{dirs[6], dirs[7], dirs[8]}, out);
+}
+
+void launch_fill(const SimParams& P, const double* regions, unsigned long long* inside, unsigned long long* vmax_bits,
+                 cudaStream_t s) {
+  if (P.n > 0) k_fill<<<nblk(P.n), 256, 0, s>>>(P, regions, inside, vmax_bits);
+}
+
+void launch_heightmap(const SimParams& P, const double* regions, int nx, int ny, unsigned long long* maps,
+                      cudaStream_t s) {
+  if (P.n > 0) k_heightmap<<<nblk(P.n), 256, 0, s>>>(P, regions, nx, ny, maps);
+}
+
+void launch_iou(const double* maps, const double* targets, int n_env, int cells, double threshold, double* iou,
+                int* success, cudaStream_t s) {
+  if (n_env > 0) k_iou<<<n_env, 256, 0, s>>>(maps, targets, cells, threshold, iou, success);
+}
+
+void launch_positions(const SimParams& P, double* pos, cudaStream_t s) {
+  if (P.n > 0) k_positions<<<nblk(P.n), 256, 0, s>>>(P, pos);
+}
+
+void launch_chamfer_side(const double* A, const long long* offA, long long max_na, const double* B,
+                         const long long* offB, int n_env, double* mind, double* mean_out, cudaStream_t s) {
+  if (n_env <= 0 || max_na <= 0) return;
+  dim3 grid(nblk(max_na, kNnT), n_env);
+  k_nearest<<<grid, kNnT, 0, s>>>(A, offA, B, offB, mind);
+  k_segment_mean<<<n_env, 256, 0, s>>>(mind, offA, mean_out);
+}
+
+}  // namespace msim_impl

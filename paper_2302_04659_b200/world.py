@@ -221,6 +221,69 @@ class GpuWorld:
                                                                   abi.dptr(Fp)))
         return tau, Fp
 
+    # ---- task metrics over every env (scenario.hpp:63-209) -------------------
+    def _regions(self, regions):
+        regions = np.asarray(regions, dtype=np.float64).reshape(-1, 6)
+        if regions.shape[0] == 1 and self.n_env > 1:
+            regions = np.repeat(regions, self.n_env, axis=0)
+        arr = (abi.Region * self.n_env)()
+        for e in range(self.n_env):
+            arr[e].min[:] = regions[e, :3]
+            arr[e].max[:] = regions[e, 3:]
+        return arr
+
+    def metric_fill(self, regions):
+        """metric_fill per env -> list of (fraction, max_speed, success); regions (n_env|1, 6) = min xyz, max xyz."""
+        out = (abi.FillResult * self.n_env)()
+        _check(self.lib, self.ctx, self.lib.msim_gpu_metric_fill(self.ctx, self._regions(regions), out))
+        return [(r.fraction, r.max_speed, bool(r.success)) for r in out]
+
+    def render_heightmap(self, regions, nx: int, ny: int):
+        """render_heightmap per env -> (n_env, ny, nx) heights above each region floor."""
+        maps = np.zeros((self.n_env, ny, nx))
+        _check(self.lib, self.ctx, self.lib.msim_gpu_render_heightmap(self.ctx, self._regions(regions), nx, ny,
+                                                                      abi.dptr(maps)))
+        return maps
+
+    def metric_write_iou(self, regions, targets, threshold: float):
+        """metric_write_iou of each env's heightmap vs targets (n_env, ny, nx) -> (iou[n_env], success[n_env])."""
+        t = np.ascontiguousarray(np.asarray(targets, dtype=np.float64))
+        ny, nx = t.shape[-2], t.shape[-1]
+        t = np.ascontiguousarray(np.broadcast_to(t, (self.n_env, ny, nx)))
+        iou = np.zeros(self.n_env)
+        ok = np.zeros(self.n_env, np.int32)
+        _check(self.lib, self.ctx, self.lib.msim_gpu_metric_write_iou(
+            self.ctx, self._regions(regions), nx, ny, threshold, abi.dptr(t), abi.dptr(iou),
+            ok.ctypes.data_as(C.POINTER(C.c_int32))))
+        return iou, ok.astype(bool)
+
+    @staticmethod
+    def _point_sets(sets):
+        pts = np.ascontiguousarray(np.concatenate([np.asarray(p, np.float64).reshape(-1, 3) for p in sets]))
+        off = np.zeros(len(sets) + 1, np.int64)
+        off[1:] = np.cumsum([np.asarray(p).reshape(-1, 3).shape[0] for p in sets])
+        return pts, off
+
+    def chamfer(self, targets):
+        """chamfer_distance(particles of env e, targets[e]) for every env."""
+        pts, off = self._point_sets(targets)
+        out = np.zeros(self.n_env)
+        _check(self.lib, self.ctx, self.lib.msim_gpu_chamfer(self.ctx, abi.dptr(pts), off.ctypes.data_as(
+            C.POINTER(C.c_int64)), abi.dptr(out)))
+        return out
+
+    def metric_pinch(self, initial, targets):
+        """metric_pinch(current = env particles, initial[e], targets[e]) -> (ratio[n_env], success[n_env])."""
+        ip, io = self._point_sets(initial)
+        tp, to = self._point_sets(targets)
+        ratio = np.zeros(self.n_env)
+        ok = np.zeros(self.n_env, np.int32)
+        lp = C.POINTER(C.c_int64)
+        _check(self.lib, self.ctx, self.lib.msim_gpu_metric_pinch(
+            self.ctx, abi.dptr(ip), io.ctypes.data_as(lp), abi.dptr(tp), to.ctypes.data_as(lp), abi.dptr(ratio),
+            ok.ctypes.data_as(C.POINTER(C.c_int32))))
+        return ratio, ok.astype(bool)
+
     def close(self):
         if getattr(self, "ctx", None):
             self.lib.msim_gpu_destroy(self.ctx)
@@ -231,3 +294,28 @@ class GpuWorld:
             self.close()
         except Exception:
             pass
+
+
+def bake_mesh_sdf(triangles, voxel: float, padding: float, device: int = 0):
+    """bake_mesh_sdf (sdf.hpp:277-310) on the GPU -> (origin[3], dims[3], samples f32 x-fastest).
+    triangles: (n, 3, 3) or flat (a, b, c per triangle)."""
+    lib = abi.load()
+    tri = np.ascontiguousarray(np.asarray(triangles, dtype=np.float64).reshape(-1))
+    n = tri.size // 9
+    origin, dims = np.zeros(3), np.zeros(3, np.int32)
+    ip = C.POINTER(C.c_int32)
+    _check(lib, None, lib.msim_bake_grid(abi.dptr(tri), n, voxel, padding, abi.dptr(origin), dims.ctypes.data_as(ip)))
+    out = np.zeros(int(np.prod(dims)), np.float32)
+    _check(lib, None, lib.msim_gpu_bake_mesh_sdf(device, abi.dptr(tri), n, voxel, padding,
+                                                 out.ctypes.data_as(C.POINTER(C.c_float)), out.size))
+    return origin, dims, out
+
+
+def make_box_mesh(half_extents, center=(0.0, 0.0, 0.0)):
+    """make_box_mesh (sdf.hpp:443-455) -> (12, 3, 3) triangles."""
+    lib = abi.load()
+    h = np.ascontiguousarray(np.asarray(half_extents, np.float64))
+    c = np.ascontiguousarray(np.asarray(center, np.float64))
+    tri = np.zeros(108)
+    lib.msim_make_box_mesh(abi.dptr(h), abi.dptr(c), abi.dptr(tri))
+    return tri.reshape(12, 3, 3)
