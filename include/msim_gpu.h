@@ -291,6 +291,20 @@ int msim_gpu_metric_pinch(msim_gpu_ctx* ctx, const double* initial, const int64_
                           const double* target, const int64_t* target_offsets, double* ratio,
                           int32_t* success);
 
+/* ---- on-device seeding for batched env resets --------
+ * seed_particles_box (seeding.hpp:13-35) run on the device for n envs at once:
+ * env envs[i] is refilled from a fresh std::mt19937_64(seeds[i]) over the box
+ * boxes[i*6 .. +6) = (min xyz, max xyz) with the jittered lattice of spacing
+ * cbrt(particle_volume); its particles (upload order) get those positions,
+ * v = 0, F = I, C = 0, mass = density(material) * particle_volume, volume0 =
+ * particle_volume and the material; lost flags, the lost count and a latched
+ * error are cleared. Every box must give the same lattice shape and its count
+ * must equal the env's particle count (MSIM_ERR_INVALID otherwise). Positions
+ * equal msim_seed_box's (the reference's draws, GCC argument order) rounded
+ * to fp32. Bodies are reset by the caller (msim_gpu_sync_bodies). */
+int msim_gpu_seed_envs(msim_gpu_ctx* ctx, int n, const int32_t* envs, const uint64_t* seeds, const double* boxes,
+                       int32_t material, double particle_volume);
+
 /* ---- mesh SDF baking ----------------------------------
  * bake_mesh_sdf (sdf.hpp:277-310) on a GPU: triangles tri[n_tri*9] (a, b, c
  * per triangle). msim_bake_grid returns the volume's origin and dims (host

@@ -1310,6 +1310,67 @@ int msim_gpu_metric_pinch(msim_gpu_ctx* c, const double* initial, const int64_t*
   });
 }
 
+// ---- on-device seeding for batched env resets (seeding.hpp:13-35) ----------
+int msim_gpu_seed_envs(msim_gpu_ctx* c, int n, const int32_t* envs, const uint64_t* seeds, const double* boxes,
+                       int32_t material, double particle_volume) {
+  return guarded(c, [&]() -> int {
+    if (n < 0 || (n > 0 && (!envs || !seeds || !boxes))) return fail(c, MSIM_ERR_INVALID, "seed_envs: null argument");
+    if (material < 0 || material >= (int)c->mats_h.size()) return fail(c, MSIM_ERR_INVALID, "seed_envs: material out of range");
+    if (!(particle_volume > 0.0)) return fail(c, MSIM_ERR_INVALID, "seed_envs: particle volume must be > 0");
+    if (n == 0) return MSIM_OK;
+    // the lattice (seeding.hpp:17-23) in host double, like msim_seed_box
+    const double spacing = std::cbrt(particle_volume);
+    int cnt[3] = {0, 0, 0};
+    std::vector<unsigned char> flag(c->n_env, 0);
+    for (int r = 0; r < n; ++r) {
+      const int e = envs[r];
+      if (e < 0 || e >= c->n_env) return fail(c, MSIM_ERR_INVALID, "seed_envs: env out of range");
+      if (flag[e]) return fail(c, MSIM_ERR_INVALID, "seed_envs: env listed twice");
+      flag[e] = 1;
+      long long total = 1;
+      for (int a = 0; a < 3; ++a) {
+        const int k = std::max(1, (int)std::floor((boxes[6 * r + 3 + a] - boxes[6 * r + a]) / spacing));
+        if (r == 0) cnt[a] = k;
+        else if (k != cnt[a]) return fail(c, MSIM_ERR_INVALID, "seed_envs: boxes must give the same lattice shape");
+        total *= k;
+      }
+      if (total != c->env_off_h[e + 1] - c->env_off_h[e])
+        return fail(c, MSIM_ERR_INVALID, "seed_envs: lattice count differs from the env's particle count");
+    }
+    set_device(c);
+    cudaStream_t s = c->stream;
+    DevBuf d_env, d_seed, d_box, d_flag, d_pos;
+    CK(d_env.ensure(sizeof(int) * n));
+    CK(d_seed.ensure(sizeof(unsigned long long) * n));
+    CK(d_box.ensure(sizeof(double) * 6 * n));
+    CK(d_flag.ensure(c->n_env));
+    CK(d_pos.ensure(sizeof(double) * 3 * (size_t)std::max<long long>(c->n, 1)));
+    CK(cudaMemcpyAsync(d_env.p, envs, sizeof(int) * n, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(d_seed.p, seeds, sizeof(unsigned long long) * n, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(d_box.p, boxes, sizeof(double) * 6 * n, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(d_flag.p, flag.data(), c->n_env, cudaMemcpyHostToDevice, s));
+    const double density = c->mats_h[material].density;
+    launch_seed(params(c), n, d_env.as<int>(), d_seed.as<unsigned long long>(), d_box.as<double>(),
+                c->env_off_d.as<long long>(), spacing, cnt[0], cnt[1], d_pos.as<double>(),
+                d_flag.as<unsigned char>(), (float)(density * particle_volume), (float)particle_volume,
+                (unsigned)material, s);
+    CK(cudaGetLastError());
+    std::vector<long long> lost(c->n_env);
+    std::vector<int> code(c->n_env);
+    CK(cudaMemcpyAsync(lost.data(), c->lost_d.p, sizeof(long long) * c->n_env, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(code.data(), c->err_code_d.p, sizeof(int) * c->n_env, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    for (int e = 0; e < c->n_env; ++e)
+      if (flag[e]) lost[e] = 0, code[e] = 0;  // a fresh world: no lost particles, no latched error
+    CK(cudaMemcpyAsync(c->lost_d.p, lost.data(), sizeof(long long) * c->n_env, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(c->err_code_d.p, code.data(), sizeof(int) * c->n_env, cudaMemcpyHostToDevice, s));
+    CK(cudaStreamSynchronize(s));
+    c->vmax_valid = false;
+    c->perm_valid = false;
+    return MSIM_OK;
+  });
+}
+
 // ---- mesh SDF baking (sdf.hpp:277-310) -------------------------------------
 namespace {
 struct hv3 {

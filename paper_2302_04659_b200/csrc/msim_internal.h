@@ -298,6 +298,9 @@ void launch_heightmap(const SimParams& P, const double* regions, int nx, int ny,
 void launch_iou(const double* maps, const double* targets, int n_env, int cells, double threshold, double* iou,
                 int* success, cudaStream_t s);
 void launch_positions(const SimParams& P, double* pos, cudaStream_t s);
+void launch_seed(const SimParams& P, int n_reset, const int* envs, const unsigned long long* seeds,
+                 const double* boxes, const long long* env_off, double spacing, int cx, int cy, double* pos,
+                 const unsigned char* env_reset, float mass, float vol0, unsigned material, cudaStream_t s);
 void launch_chamfer_side(const double* A, const long long* offA, long long max_na, const double* B,
                          const long long* offB, int n_env, double* mind, double* mean_out, cudaStream_t s);
 

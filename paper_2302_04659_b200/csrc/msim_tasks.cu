@@ -245,6 +245,99 @@ __global__ void k_segment_mean(const double* __restrict__ v, const long long* __
   if (threadIdx.x == 0) out[env] = n > 0 ? red[0] / (double)n : 0.0;
 }
 
+// ---- on-device seeding (seeding.hpp:13-35) --------------------------------
+// std::mt19937_64 (libstdc++ parameters) with the 312-word twist split in the
+// three dependency phases of _M_gen_rand, each read-all-then-write across the
+// block, and libstdc++'s uniform_real_distribution<double>:
+// (double(x) / 2^64, clamped below 1) * (b - a) + a.
+constexpr int kMtN = 312, kMtM = 156;
+constexpr unsigned long long kMtA = 0xb5026f5aa96619e9ull, kMtUpper = ~0ull << 31, kMtLower = ~kMtUpper;
+
+__device__ __forceinline__ unsigned long long mt_mix(unsigned long long hi, unsigned long long lo) {
+  const unsigned long long y = (hi & kMtUpper) | (lo & kMtLower);
+  return (y >> 1) ^ ((y & 1ull) ? kMtA : 0ull);
+}
+__device__ __forceinline__ unsigned long long mt_temper(unsigned long long z) {
+  z ^= (z >> 29) & 0x5555555555555555ull;
+  z ^= (z << 17) & 0x71d67fffeda60000ull;
+  z ^= (z << 37) & 0xfff7eee000000000ull;
+  z ^= z >> 43;
+  return z;
+}
+
+// One CTA per env being reset: its particles (upload order) get the jittered
+// lattice positions of box [lo, hi] drawn from mt19937_64(seed), written to
+// pos[3 * pid] in double. Draw d belongs to particle d / 3, component 2 - d % 3
+// (GCC evaluates Vec3(jitter, jitter, jitter) right to left).
+__global__ void __launch_bounds__(kMtN) k_seed_lattice(const int* envs, const unsigned long long* seeds,
+                                                        const double* boxes, const long long* env_off,
+                                                        double spacing, int cx, int cy, double* pos) {
+  __shared__ unsigned long long mt[kMtN];
+  __shared__ double jit[kMtN];
+  const int r = blockIdx.x, t = threadIdx.x;
+  const int env = envs[r];
+  const double* box = boxes + 6 * r;
+  const long long first = env_off[env], n = env_off[env + 1] - first;
+  if (t == 0) {  // std::mersenne_twister_engine::seed (sequential recurrence)
+    mt[0] = seeds[r];
+    for (int i = 1; i < kMtN; ++i) mt[i] = 6364136223846793005ull * (mt[i - 1] ^ (mt[i - 1] >> 62)) + (unsigned long long)i;
+  }
+  const double a = -0.25 * spacing, b = 0.25 * spacing;
+  const long long draws = 3 * n;
+  for (long long d0 = 0; d0 < draws; d0 += kMtN) {
+    __syncthreads();
+    unsigned long long v = 0;  // phase 1: k < n - m, old words only
+    if (t < kMtN - kMtM) v = mt[t + kMtM] ^ mt_mix(mt[t], mt[t + 1]);
+    __syncthreads();
+    if (t < kMtN - kMtM) mt[t] = v;
+    __syncthreads();
+    if (t >= kMtN - kMtM && t < kMtN - 1) v = mt[t - (kMtN - kMtM)] ^ mt_mix(mt[t], mt[t + 1]);  // phase 2
+    __syncthreads();
+    if (t >= kMtN - kMtM && t < kMtN - 1) mt[t] = v;
+    __syncthreads();
+    if (t == kMtN - 1) mt[t] = mt[kMtM - 1] ^ mt_mix(mt[kMtN - 1], mt[0]);  // phase 3
+    __syncthreads();
+    double c = (double)mt_temper(mt[t]) / 18446744073709551616.0;  // generate_canonical<double, 53>
+    if (c >= 1.0) c = __longlong_as_double(0x3fefffffffffffffll);   // nextafter(1, 0)
+    jit[t] = c * (b - a) + a;
+    const long long d = d0 + t;
+    if (d < draws) {
+      const long long p = d / 3;
+      const int comp = 2 - (int)(d % 3);
+      const long long idx = comp == 0 ? p % cx : (comp == 1 ? (p / cx) % cy : p / ((long long)cx * cy));
+      double q = box[comp] + spacing * ((double)idx + 0.5);
+      q += jit[t];
+      q = q < box[comp] ? box[comp] : q;              // cwiseMax(box_min)
+      q = box[3 + comp] < q ? box[3 + comp] : q;      // cwiseMin(box_max)
+      pos[3 * (first + p) + comp] = q;
+    }
+  }
+}
+
+// the reset envs' particle state from the seeded positions (flag per env)
+__global__ void k_seed_apply(SimParams P, const unsigned char* env_reset, const double* pos, float mass, float vol0,
+                             unsigned material) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= P.n) return;
+  Particles& q = P.cur;
+  const unsigned env = (q.meta[i] >> 8) & kEnvMask;
+  if (!env_reset[env]) return;
+  const long long j = q.pid[i];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    q.x[a][i] = (float)pos[3 * j + a];
+    q.v[a][i] = 0.0f;
+  }
+#pragma unroll
+  for (int k = 0; k < 9; ++k) {
+    q.C[k][i] = 0.0f;
+    q.G[k][i] = 0.0f;
+  }
+  q.mass[i] = mass;
+  q.vol0[i] = vol0;
+  q.meta[i] = (env << 8) | (material & 0xFFu);  // lost flag cleared
+}
+
 inline unsigned nblk(long long n, int t = 256) { return (unsigned)((n + t - 1) / t); }
 
 }  // namespace
@@ -255,6 +348,14 @@ void launch_bake(const double* tri, long long n_tri, const double* origin, doubl
   k_bake<<<nblk(nvox, kBakeT), kBakeT, 0, s>>>(tri, n_tri, d3{origin[0], origin[1], origin[2]}, voxel, dims[0],
                                                  dims[1], dims[2], d3{dirs[0], dirs[1], dirs[2]},
                                                  d3{dirs[3], dirs[4], dirs[5]}, d3{dirs[6], dirs[7], dirs[8]}, out);
+}
+
+void launch_seed(const SimParams& P, int n_reset, const int* envs, const unsigned long long* seeds,
+                 const double* boxes, const long long* env_off, double spacing, int cx, int cy, double* pos,
+                 const unsigned char* env_reset, float mass, float vol0, unsigned material, cudaStream_t s) {
+  if (n_reset <= 0) return;
+  k_seed_lattice<<<n_reset, kMtN, 0, s>>>(envs, seeds, boxes, env_off, spacing, cx, cy, pos);
+  if (P.n > 0) k_seed_apply<<<nblk(P.n), 256, 0, s>>>(P, env_reset, pos, mass, vol0, material);
 }
 
 void launch_fill(const SimParams& P, const double* regions, unsigned long long* inside, unsigned long long* vmax_bits,

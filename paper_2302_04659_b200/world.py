@@ -221,6 +221,18 @@ class GpuWorld:
                                                                   abi.dptr(Fp)))
         return tau, Fp
 
+    def seed_envs(self, envs, seeds, boxes, material: int = 0, particle_volume: float | None = None):
+        """Batched env reset on the device: seed_particles_box (seeding.hpp:13-35) with
+        mt19937_64(seeds[i]) into boxes[i] = (min xyz, max xyz) for envs[i]."""
+        envs = np.ascontiguousarray(np.asarray(envs, np.int32))
+        seeds = np.ascontiguousarray(np.asarray(seeds, np.uint64))
+        boxes = np.ascontiguousarray(np.asarray(boxes, np.float64).reshape(-1, 6))
+        if particle_volume is None:
+            particle_volume = float(self.scene.envs[int(envs[0])].vol0[0])
+        _check(self.lib, self.ctx, self.lib.msim_gpu_seed_envs(
+            self.ctx, len(envs), envs.ctypes.data_as(C.POINTER(C.c_int32)), seeds.ctypes.data_as(C.POINTER(C.c_uint64)),
+            abi.dptr(boxes), material, particle_volume))
+
     # ---- task metrics over every env (scenario.hpp:63-209) -------------------
     def _regions(self, regions):
         regions = np.asarray(regions, dtype=np.float64).reshape(-1, 6)

@@ -6,7 +6,7 @@ relative (summation order only)."""
 import numpy as np
 import pytest
 
-from gpu_helpers import rel  # noqa: F401  (shared helpers import path)
+from gpu_helpers import rel
 from oracle import oracle_py
 from paper_2302_04659_b200 import GpuWorld, bake_mesh_sdf, make_box_mesh
 from paper_2302_04659_b200.scenes import V0_SOFT, Scene, block_env
@@ -113,3 +113,50 @@ def test_metric_errors_match_reference(stepped):
         gw.render_heightmap(REGIONS, 1, 4)
     with pytest.raises(ValueError, match="non-empty"):
         gw.chamfer([np.zeros((0, 3))] * 3)
+
+
+def test_seed_envs_matches_host_seeder_and_steps_like_oracle():
+    """§8f #4: batched reset by on-device seeding (mt19937_64 + the reference's
+    jittered lattice): positions equal the host seeder's rounded to fp32, the
+    rest of the state is fresh, untouched envs keep theirs, and the reset world
+    then steps like the oracle fed the same state."""
+    from oracle.oracle_py import OracleWorld
+    from paper_2302_04659_b200.scenes import EnvSpec, Rng, lattice_span, seed_box
+
+    counts = (10, 9, 6)
+    los = [(0.10, 0.10, 0.03), (0.12, 0.08, 0.05), (0.02, 0.10, 0.03)]
+    envs = [block_env(los[e], counts, 0, (1000.0, 1e4, 0.3, 2e3), V0_SOFT, seed=40 + e, vel_seed=50 + e)
+            for e in range(3)]
+    envs[2].x[:4, 0] = -0.05  # lost before the reset
+    scene = Scene(name="reset", dims=(32, 32, 32), h=0.01, dt=2e-4, envs=envs, n_rigid=3,
+                  lost_fraction_threshold=1.0)
+    gw = GpuWorld(scene)
+    gw.env_step()
+    assert gw.lost_count(2) > 0
+    before1 = gw.particles(1)
+    new_lo = [(0.11, 0.12, 0.04), None, (0.15, 0.09, 0.06)]
+    boxes = [list(new_lo[e]) + [new_lo[e][a] + lattice_span(counts[a], V0_SOFT) for a in range(3)] for e in (0, 2)]
+    seeds = [9001, 123456789012345]
+    gw.seed_envs([0, 2], seeds, boxes)
+    assert gw.lost_count(2) == 0
+    for r, e in enumerate((0, 2)):
+        x_host, m_host = seed_box(Rng(seeds[r]), boxes[r][:3], boxes[r][3:], 1000.0, V0_SOFT)
+        p = gw.particles(e)
+        assert np.array_equal(p["x"], x_host.astype(np.float32).astype(np.float64)), e
+        assert not p["v"].any() and not p["C"].any() and not p["lost"].any()
+        assert np.array_equal(p["F"], np.broadcast_to(np.eye(3), p["F"].shape))
+    after1 = gw.particles(1)
+    for k in ("x", "v", "F", "C"):
+        assert np.array_equal(before1[k], after1[k])
+    # the reset env steps like the oracle started from the same (fp32-rounded) state
+    p0 = gw.particles(0)
+    env0 = EnvSpec(x=p0["x"], mass=np.full(len(p0["x"]), np.float32(1000.0 * V0_SOFT), np.float64),
+                   vol0=np.full(len(p0["x"]), np.float32(V0_SOFT), np.float64),
+                   material=np.zeros(len(p0["x"]), np.int32))
+    ow = OracleWorld(Scene(name="reset0", dims=(32, 32, 32), h=0.01, dt=2e-4, envs=[env0], n_rigid=3,
+                           lost_fraction_threshold=1.0))
+    gw.env_step()
+    ow.env_step()
+    pg, po = gw.particles(0), ow.particles()
+    assert np.linalg.norm(pg["x"] - po["x"]) / np.linalg.norm(po["x"]) < 1e-4
+    assert rel(pg["v"], po["v"]) < 1e-4
