@@ -119,6 +119,7 @@ struct msim_gpu_ctx {
 
   double time = 0.0;
   KernelTimer timer;
+  DevBuf tbuf[10];  // task-metric / seeding scratch, kept across calls (no per-call cudaMalloc)
 };
 
 namespace {
@@ -1167,7 +1168,8 @@ void chamfer_sets(msim_gpu_ctx* c, const double* A, const long long* offA_d, con
     maxa = std::max(maxa, offA[e + 1] - offA[e]);
     maxb = std::max(maxb, offB[e + 1] - offB[e]);
   }
-  DevBuf mind, means;
+  DevBuf& mind = c->tbuf[9];
+  DevBuf& means = c->tbuf[1];
   CK(mind.ensure(sizeof(double) * (size_t)std::max(offA[ne], offB[ne]) + 16));
   CK(means.ensure(sizeof(double) * 2 * ne));
   double* mab = means.as<double>();
@@ -1213,7 +1215,8 @@ int msim_gpu_metric_fill(msim_gpu_ctx* c, const msim_region* regions, msim_fill_
       if (c->env_off_h.empty() || c->env_off_h[e + 1] == c->env_off_h[e])
         return fail(c, MSIM_ERR_INVALID, "metric_fill: no particles");
     set_device(c);
-    DevBuf reg, acc;
+    DevBuf& reg = c->tbuf[0];
+    DevBuf& acc = c->tbuf[1];
     int rc = upload_regions(c, regions, reg);
     if (rc) return rc;
     CK(acc.ensure(sizeof(unsigned long long) * 2 * c->n_env));
@@ -1239,7 +1242,8 @@ int msim_gpu_render_heightmap(msim_gpu_ctx* c, const msim_region* regions, int n
   return guarded(c, [&]() -> int {
     if (!maps) return fail(c, MSIM_ERR_INVALID, "render_heightmap: maps required");
     set_device(c);
-    DevBuf m, reg;
+    DevBuf& m = c->tbuf[2];
+    DevBuf& reg = c->tbuf[0];
     int rc = heightmaps(c, regions, nx, ny, m, reg);
     if (rc) return rc;
     CK(cudaMemcpyAsync(maps, m.p, sizeof(double) * (size_t)nx * ny * c->n_env, cudaMemcpyDeviceToHost, c->stream));
@@ -1253,7 +1257,10 @@ int msim_gpu_metric_write_iou(msim_gpu_ctx* c, const msim_region* regions, int n
   return guarded(c, [&]() -> int {
     if (!targets || !iou || !success) return fail(c, MSIM_ERR_INVALID, "metric_write_iou: null argument");
     set_device(c);
-    DevBuf m, reg, tg, res;
+    DevBuf& m = c->tbuf[2];
+    DevBuf& reg = c->tbuf[0];
+    DevBuf& tg = c->tbuf[3];
+    DevBuf& res = c->tbuf[1];
     int rc = heightmaps(c, regions, nx, ny, m, reg);
     if (rc) return rc;
     const size_t cells = (size_t)nx * ny;
@@ -1275,7 +1282,9 @@ int msim_gpu_chamfer(msim_gpu_ctx* c, const double* points, const int64_t* offse
   return guarded(c, [&]() -> int {
     if (!out) return fail(c, MSIM_ERR_INVALID, "chamfer_distance: out required");
     set_device(c);
-    DevBuf pos, pts, off_d;
+    DevBuf& pos = c->tbuf[4];
+    DevBuf& pts = c->tbuf[5];
+    DevBuf& off_d = c->tbuf[6];
     std::vector<long long> off_h;
     int rc = particle_points(c, pos);
     if (!rc) rc = upload_points(c, points, offsets, pts, off_d, off_h);
@@ -1291,7 +1300,11 @@ int msim_gpu_metric_pinch(msim_gpu_ctx* c, const double* initial, const int64_t*
   return guarded(c, [&]() -> int {
     if (!ratio || !success) return fail(c, MSIM_ERR_INVALID, "metric_pinch: null argument");
     set_device(c);
-    DevBuf pos, ini, ini_off, tgt, tgt_off;
+    DevBuf& pos = c->tbuf[4];
+    DevBuf& ini = c->tbuf[5];
+    DevBuf& ini_off = c->tbuf[6];
+    DevBuf& tgt = c->tbuf[7];
+    DevBuf& tgt_off = c->tbuf[8];
     std::vector<long long> ini_h, tgt_h;
     int rc = upload_points(c, initial, initial_offsets, ini, ini_off, ini_h);
     if (!rc) rc = upload_points(c, target, target_offsets, tgt, tgt_off, tgt_h);
@@ -1339,7 +1352,11 @@ int msim_gpu_seed_envs(msim_gpu_ctx* c, int n, const int32_t* envs, const uint64
     }
     set_device(c);
     cudaStream_t s = c->stream;
-    DevBuf d_env, d_seed, d_box, d_flag, d_pos;
+    DevBuf& d_env = c->tbuf[0];
+    DevBuf& d_seed = c->tbuf[1];
+    DevBuf& d_box = c->tbuf[2];
+    DevBuf& d_flag = c->tbuf[3];
+    DevBuf& d_pos = c->tbuf[4];
     CK(d_env.ensure(sizeof(int) * n));
     CK(d_seed.ensure(sizeof(unsigned long long) * n));
     CK(d_box.ensure(sizeof(double) * 6 * n));

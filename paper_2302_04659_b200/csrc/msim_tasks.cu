@@ -116,35 +116,66 @@ __device__ __forceinline__ bool region_contains(const double* r, double x, doubl
   return x >= r[0] && y >= r[1] && z >= r[2] && x <= r[3] && y <= r[4] && z <= r[5];
 }
 
-// metric_fill (scenario.hpp:63-75): per env count inside + max |v| (double of the stored fp32)
+// max of a nonnegative double's bits over the lanes of `grp` (two 32-bit
+// warp reductions: high word, then low word among the lanes holding that high)
+__device__ __forceinline__ unsigned long long group_max_bits(unsigned grp, unsigned long long bits) {
+  const unsigned hi = (unsigned)(bits >> 32);
+  const unsigned mhi = __reduce_max_sync(grp, hi);
+  const unsigned mlo = __reduce_max_sync(grp, hi == mhi ? (unsigned)bits : 0u);
+  return ((unsigned long long)mhi << 32) | mlo;
+}
+
+// metric_fill (scenario.hpp:63-75): per env count inside + max |v| (double of
+// the stored fp32). Particles are stored env-major, so lanes are grouped by env
+// (match_any) and each group issues one atomic per counter.
 __global__ void k_fill(SimParams P, const double* __restrict__ regions, unsigned long long* inside,
                        unsigned long long* vmax_bits) {
   const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (i >= P.n) return;
-  const Particles& q = P.cur;
-  const int env = (q.meta[i] >> 8) & kEnvMask;
-  const double x = q.x[0][i], y = q.x[1][i], z = q.x[2][i];
-  const double vx = q.v[0][i], vy = q.v[1][i], vz = q.v[2][i];
-  const double sp = sqrt(vx * vx + vy * vy + vz * vz);
-  if (region_contains(regions + 6 * env, x, y, z)) atomicAdd(inside + env, 1ull);
-  atomicMax(vmax_bits + env, (unsigned long long)__double_as_longlong(sp));  // sp >= 0: bit order = value order
+  const bool valid = i < P.n;
+  int env = -1;
+  bool in = false;
+  unsigned long long bits = 0;
+  if (valid) {
+    const Particles& q = P.cur;
+    env = (q.meta[i] >> 8) & kEnvMask;
+    const double x = q.x[0][i], y = q.x[1][i], z = q.x[2][i];
+    const double vx = q.v[0][i], vy = q.v[1][i], vz = q.v[2][i];
+    const double sp = sqrt(vx * vx + vy * vy + vz * vz);
+    in = region_contains(regions + 6 * env, x, y, z);
+    bits = (unsigned long long)__double_as_longlong(sp);  // sp >= 0: bit order = value order
+  }
+  const unsigned grp = __match_any_sync(0xffffffffu, env);
+  const unsigned cnt = __popc(__ballot_sync(0xffffffffu, in) & grp);
+  bits = group_max_bits(grp, bits);
+  if (valid && (int)(threadIdx.x & 31) == __ffs(grp) - 1) {
+    if (cnt) atomicAdd(inside + env, (unsigned long long)cnt);
+    atomicMax(vmax_bits + env, bits);
+  }
 }
 
-// render_heightmap (scenario.hpp:79-98): per env nx*ny max heights above the region floor
+// render_heightmap (scenario.hpp:79-98): per env nx*ny max heights above the
+// region floor; lanes landing in the same cell combine before the atomic.
 __global__ void k_heightmap(SimParams P, const double* __restrict__ regions, int nx, int ny,
                             unsigned long long* maps) {
   const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (i >= P.n) return;
-  const Particles& q = P.cur;
-  const int env = (q.meta[i] >> 8) & kEnvMask;
-  const double* r = regions + 6 * env;
-  const double x = q.x[0][i], y = q.x[1][i], z = q.x[2][i];
-  if (!region_contains(r, x, y, z)) return;
-  const double cell = (r[3] - r[0]) / nx, cy = (r[4] - r[1]) / ny;
-  const int ci = min(nx - 1, (int)((x - r[0]) / cell));
-  const int cj = min(ny - 1, (int)((y - r[1]) / cy));
-  const double hgt = z - r[2];  // >= 0 (contained): bit order = value order
-  atomicMax(maps + (long long)env * nx * ny + (long long)cj * nx + ci, (unsigned long long)__double_as_longlong(hgt));
+  long long slot = -1;
+  unsigned long long bits = 0;
+  if (i < P.n) {
+    const Particles& q = P.cur;
+    const int env = (q.meta[i] >> 8) & kEnvMask;
+    const double* r = regions + 6 * env;
+    const double x = q.x[0][i], y = q.x[1][i], z = q.x[2][i];
+    if (region_contains(r, x, y, z)) {
+      const double cell = (r[3] - r[0]) / nx, cy = (r[4] - r[1]) / ny;
+      const int ci = min(nx - 1, (int)((x - r[0]) / cell));
+      const int cj = min(ny - 1, (int)((y - r[1]) / cy));
+      slot = (long long)env * nx * ny + (long long)cj * nx + ci;
+      bits = (unsigned long long)__double_as_longlong(z - r[2]);  // >= 0 (contained)
+    }
+  }
+  const unsigned grp = __match_any_sync(0xffffffffu, slot);
+  bits = group_max_bits(grp, bits);
+  if (slot >= 0 && (int)(threadIdx.x & 31) == __ffs(grp) - 1) atomicMax(maps + slot, bits);
 }
 
 // metric_write_iou (scenario.hpp:106-119), one block per env
@@ -192,10 +223,11 @@ __global__ void k_positions(SimParams P, double* pos) {
   pos[3 * j + 2] = P.cur.x[2][i];
 }
 
-constexpr int kNnT = 128;
+constexpr int kNnT = 128, kNnQ = 4;
 
 // Nearest distance from every point of set A to set B, per env: blockIdx.y =
-// env, one query per thread, B streamed through shared memory. The minimum of
+// env, kNnQ queries per thread (each B point read from shared memory once per
+// kNnQ distance evaluations), B streamed through shared memory. The minimum of
 // squared norms then one sqrt: sqrt is monotone and correctly rounded, so this
 // equals the minimum of the reference's per-pair norm() (scenario.hpp:168).
 __global__ void __launch_bounds__(kNnT) k_nearest(const double* __restrict__ A, const long long* __restrict__ offA,
@@ -205,28 +237,38 @@ __global__ void __launch_bounds__(kNnT) k_nearest(const double* __restrict__ A, 
   const int env = blockIdx.y;
   const long long a0 = offA[env], na = offA[env + 1] - a0;
   const long long b0 = offB[env], nb = offB[env + 1] - b0;
-  const long long qi = (long long)blockIdx.x * kNnT + threadIdx.x;
-  if ((long long)blockIdx.x * kNnT >= na) return;  // block-uniform
-  const bool valid = qi < na;
-  double qx = 0, qy = 0, qz = 0;
-  if (valid) {
-    qx = A[3 * (a0 + qi)];
-    qy = A[3 * (a0 + qi) + 1];
-    qz = A[3 * (a0 + qi) + 2];
+  const long long q0 = (long long)blockIdx.x * kNnT * kNnQ;
+  if (q0 >= na) return;  // block-uniform
+  double qx[kNnQ], qy[kNnQ], qz[kNnQ], best[kNnQ];
+#pragma unroll
+  for (int k = 0; k < kNnQ; ++k) {
+    const long long qi = q0 + k * kNnT + threadIdx.x;
+    const long long src = a0 + (qi < na ? qi : 0);
+    qx[k] = A[3 * src];
+    qy[k] = A[3 * src + 1];
+    qz[k] = A[3 * src + 2];
+    best[k] = __longlong_as_double(0x7ff0000000000000ll);  // +inf
   }
-  double best = __longlong_as_double(0x7ff0000000000000ll);  // +inf
   for (long long base = 0; base < nb; base += kNnT) {
     const int cnt = (int)min((long long)kNnT, nb - base);
     __syncthreads();
     for (int q = threadIdx.x; q < cnt * 3; q += kNnT) sb[q] = B[3 * (b0 + base) + q];
     __syncthreads();
     for (int t = 0; t < cnt; ++t) {
-      const double dx = sb[3 * t] - qx, dy = sb[3 * t + 1] - qy, dz = sb[3 * t + 2] - qz;
-      const double d2 = dx * dx + dy * dy + dz * dz;
-      best = d2 < best ? d2 : best;
+      const double bx = sb[3 * t], by = sb[3 * t + 1], bz = sb[3 * t + 2];
+#pragma unroll
+      for (int k = 0; k < kNnQ; ++k) {
+        const double dx = bx - qx[k], dy = by - qy[k], dz = bz - qz[k];
+        const double d2 = dx * dx + dy * dy + dz * dz;
+        best[k] = d2 < best[k] ? d2 : best[k];
+      }
     }
   }
-  if (valid) mind[a0 + qi] = sqrt(best);
+#pragma unroll
+  for (int k = 0; k < kNnQ; ++k) {
+    const long long qi = q0 + k * kNnT + threadIdx.x;
+    if (qi < na) mind[a0 + qi] = sqrt(best[k]);
+  }
 }
 
 // mean of a segmented array, one block per segment, fixed reduction order
@@ -380,7 +422,7 @@ void launch_positions(const SimParams& P, double* pos, cudaStream_t s) {
 void launch_chamfer_side(const double* A, const long long* offA, long long max_na, const double* B,
                          const long long* offB, int n_env, double* mind, double* mean_out, cudaStream_t s) {
   if (n_env <= 0 || max_na <= 0) return;
-  dim3 grid(nblk(max_na, kNnT), n_env);
+  dim3 grid(nblk(max_na, kNnT * kNnQ), n_env);
   k_nearest<<<grid, kNnT, 0, s>>>(A, offA, B, offB, mind);
   k_segment_mean<<<n_env, 256, 0, s>>>(mind, offA, mean_out);
 }
