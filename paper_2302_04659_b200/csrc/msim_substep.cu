@@ -62,6 +62,16 @@ template <int NCH> constexpr int pay_floats() { return NCH == 4 ? 24 : 32; }  //
 #define MSIM_CTAS_PER_SM 5  // measured: 4 -> 1.12, 5 -> 1.05, 6 -> 1.10 ms per launch (config D, 256 envs)
 #endif
 constexpr int kCtasPerSm = MSIM_CTAS_PER_SM;
+
+// Particle state is streamed once per launch: evict-first loads / stores
+// (ld/st .cs) keep L1 for the register spills and the per-bucket tiles.
+#ifdef MSIM_NO_STREAM_HINTS  // variant build: plain cached accesses
+template <class T> __device__ __forceinline__ T lds(const T* p) { return *p; }
+template <class T> __device__ __forceinline__ void sts(T* p, T v) { *p = v; }
+#else
+template <class T> __device__ __forceinline__ T lds(const T* p) { return __ldcs(p); }
+template <class T> __device__ __forceinline__ void sts(T* p, T v) { __stcs(p, v); }
+#endif
 #ifdef MSIM_NO_CULL  // variant build: no bounding test ahead of the collider SDFs
 constexpr bool kNoCull = true;
 #else
@@ -179,7 +189,7 @@ __device__ __forceinline__ void item_rounds(const SimParams& P, Smem<NCH>& S, bo
         const bool valid = t < rn;
         const int j = r0 + t;
         const int i = valid ? P.perm[j] : 0;
-        unsigned meta = valid ? P.cur.meta[i] : (1u << kLostBit);
+        unsigned meta = valid ? lds(&P.cur.meta[i]) : (1u << kLostBit);
         const int penv = (meta >> 8) & kEnvMask;
         const bool was_lost = meta >> kLostBit;
         const int pact = IC.lostb ? (valid ? P.run[penv].action : kActIdle) : IC.act;
@@ -188,12 +198,12 @@ __device__ __forceinline__ void item_rounds(const SimParams& P, Smem<NCH>& S, bo
         float m = 0.f, V0 = 0.f;
         int pid = 0;
         if (valid) {
-          x = load3(P.cur.x, i);
+          x = {lds(&P.cur.x[0][i]), lds(&P.cur.x[1][i]), lds(&P.cur.x[2][i])};
 #pragma unroll
-          for (int k = 0; k < 9; ++k) G[k] = P.cur.G[k][i];
-          m = P.cur.mass[i];
-          V0 = P.cur.vol0[i];
-          pid = P.cur.pid[i];
+          for (int k = 0; k < 9; ++k) G[k] = lds(&P.cur.G[k][i]);
+          m = lds(&P.cur.mass[i]);
+          V0 = lds(&P.cur.vol0[i]);
+          pid = lds(&P.cur.pid[i]);
         } else {
 #pragma unroll
           for (int k = 0; k < 9; ++k) G[k] = 0.f;
@@ -281,10 +291,10 @@ __device__ __forceinline__ void item_rounds(const SimParams& P, Smem<NCH>& S, bo
 
         if (!redo && valid) {  // G is final here: store it now so it does not live on in registers
 #pragma unroll
-          for (int k = 0; k < 9; ++k) P.nxt.G[k][j] = G[k];
-          P.nxt.mass[j] = m;
-          P.nxt.vol0[j] = V0;
-          P.nxt.pid[j] = pid;
+          for (int k = 0; k < 9; ++k) sts(&P.nxt.G[k][j], G[k]);
+          sts(&P.nxt.mass[j], m);
+          sts(&P.nxt.vol0[j], V0);
+          sts(&P.nxt.pid[j], pid);
         }
 
         // ---------------- binning of the (new) position + P2G payload of the next cycle
@@ -417,12 +427,12 @@ __device__ __forceinline__ void item_rounds(const SimParams& P, Smem<NCH>& S, bo
         if (!redo) {
           // ---------------- write back in bucket order (the re-sort)
           if (valid) {
-            P.nxt.x[0][j] = x.x; P.nxt.x[1][j] = x.y; P.nxt.x[2][j] = x.z;
-            P.nxt.meta[j] = meta;
+            sts(&P.nxt.x[0][j], x.x); sts(&P.nxt.x[1][j], x.y); sts(&P.nxt.x[2][j], x.z);
+            sts(&P.nxt.meta[j], meta);
             if (write_vc) {
-              P.nxt.v[0][j] = v.x; P.nxt.v[1][j] = v.y; P.nxt.v[2][j] = v.z;
+              sts(&P.nxt.v[0][j], v.x); sts(&P.nxt.v[1][j], v.y); sts(&P.nxt.v[2][j], v.z);
 #pragma unroll
-              for (int k = 0; k < 9; ++k) P.nxt.C[k][j] = Cm[k];
+              for (int k = 0; k < 9; ++k) sts(&P.nxt.C[k][j], Cm[k]);
             }
             if (now_lost) key_new = P.n_keys - 1;
             P.key[j] = key_new;
