@@ -888,17 +888,27 @@ int msim_gpu_env_step(msim_gpu_ctx* c, int n_rigid, int n_soft, msim_step_report
     CK(cudaMemsetAsync(c->balance_d.p, 0, sizeof(double) * c->n_env, s));
     const int rc = step_call(c, n_rigid * n_soft, c->n_bodies > 0, n_soft, nullptr);
     c->time += n_rigid * n_soft * c->desc.dt;
-    if (report) {
+    if (report) {  // all envs' report words in one transfer (not one round trip per env)
+      const int ne = c->n_env;
+      std::vector<unsigned> pen(ne);
+      std::vector<double> bal(ne);
+      std::vector<long long> lost(ne);
+      std::vector<EnvRun> run(ne);
+      CK(cudaMemcpyAsync(pen.data(), c->max_pen_d.p, sizeof(unsigned) * ne, cudaMemcpyDeviceToHost, s));
+      CK(cudaMemcpyAsync(bal.data(), c->balance_d.p, sizeof(double) * ne, cudaMemcpyDeviceToHost, s));
+      CK(cudaMemcpyAsync(lost.data(), c->lost_d.p, sizeof(long long) * ne, cudaMemcpyDeviceToHost, s));
+      CK(cudaMemcpyAsync(run.data(), c->run_d.p, sizeof(EnvRun) * ne, cudaMemcpyDeviceToHost, s));
+      CK(cudaStreamSynchronize(s));
       msim_step_report agg{};
       agg.rigid_steps = n_rigid;
       agg.soft_substeps = n_rigid * n_soft;
-      for (int e = 0; e < c->n_env; ++e) {
-        msim_step_report r{};
-        msim_gpu_read_report(c, e, &r);
-        agg.cfl_cycles = std::max(agg.cfl_cycles, r.cfl_cycles);
-        agg.max_penetration = std::max(agg.max_penetration, r.max_penetration);
-        agg.max_force_balance_error = std::max(agg.max_force_balance_error, r.max_force_balance_error);
-        agg.lost_particles += r.lost_particles;
+      for (int e = 0; e < ne; ++e) {
+        float penf;
+        std::memcpy(&penf, &pen[e], sizeof penf);
+        agg.cfl_cycles = std::max(agg.cfl_cycles, run[e].cyc_sum);
+        agg.max_penetration = std::max(agg.max_penetration, (double)penf);
+        agg.max_force_balance_error = std::max(agg.max_force_balance_error, bal[e]);
+        agg.lost_particles += lost[e];
       }
       *report = agg;
     }
