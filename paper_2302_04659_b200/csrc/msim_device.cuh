@@ -212,13 +212,21 @@ __device__ __forceinline__ Sym hencky_strain(const float* G) {
   const float inv_det = 1.0f / (B.a00 * Cf.a00 + B.a01 * Cf.a01 + B.a02 * Cf.a02);  // det B >= 1
   Sym Z = sym_mul(E, Cf);
   Z = sym_scale_add_id(Z, inv_det, 0.0f);
+  const float nz2 = sym_norm2(Z);
 #ifndef MSIM_ABLATE_EIGEN
-  if (sym_norm2(Z) <= 0.0625f) {
+  if (nz2 <= 0.0625f) {
 #endif
     const Sym W = sym_mul(Z, Z);
-    Sym q = sym_scale_add_id(W, 1.0f / 11.0f, 1.0f / 9.0f);
-    q = sym_mul_add_id(W, q, 1.0f / 7.0f);
-    q = sym_mul_add_id(W, q, 1.0f / 5.0f);
+    // |Z|_F <= 0.03 (the elastic strains of the firm clays): Z^9/9 and Z^11/11
+    // are below 3e-15 and are dropped
+    Sym q;
+    if (nz2 > 9e-4f) {
+      q = sym_scale_add_id(W, 1.0f / 11.0f, 1.0f / 9.0f);
+      q = sym_mul_add_id(W, q, 1.0f / 7.0f);
+      q = sym_mul_add_id(W, q, 1.0f / 5.0f);
+    } else {
+      q = sym_scale_add_id(W, 1.0f / 7.0f, 1.0f / 5.0f);
+    }
     q = sym_mul_add_id(W, q, 1.0f / 3.0f);
     q = sym_mul_add_id(W, q, 1.0f);
     return sym_mul(Z, q);
