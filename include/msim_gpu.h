@@ -256,6 +256,11 @@ int msim_gpu_kernel_stats(msim_gpu_ctx* ctx, int id, const char** name, int64_t*
 int msim_gpu_constitutive(msim_gpu_ctx* ctx, int mat, int64_t n, const double* F, double* tau,
                           double* Fp);
 
+/* Tuning: particle buckets of factor^3 node blocks of 4x4x2 cells (1: dense
+ * scenes, 2: sparse ones, 0: chosen at set_particles from h^3 / mean volume0,
+ * the default). Results do not depend on it (bucketing is internal). */
+int msim_gpu_set_bucket_factor(msim_gpu_ctx* ctx, int factor);
+
 /* ---- task metrics over every env's device state -------
  * The reference evaluates these on the host particle vector after the
  * episode (scenario.hpp:63-209); here one launch covers all envs and only the

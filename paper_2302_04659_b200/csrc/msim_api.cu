@@ -79,6 +79,10 @@ struct msim_gpu_ctx {
   int bdims[3] = {0, 0, 0};
   int blocks_per_env = 0;
   int n_keys = 0;
+  int qf = 0;          // particle bucket = qf^3 node blocks (set_bucket_shape)
+  int qf_request = 0;  // 0: chosen from the particle density at set_particles
+  int qdims[3] = {0, 0, 0};
+  int buckets_per_env = 0;
 
   // particles
   long long n = 0;
@@ -161,6 +165,16 @@ SimParams params(msim_gpu_ctx* c) {
   P.d_inv_f = (float)(4.0 / (d.h * d.h));
   P.n = c->n;
   P.n_keys = c->n_keys;
+  P.qf = c->qf;
+  const int qb[3] = {kBX, kBY, kBZ};
+  for (int a = 0; a < 3; ++a) {
+    P.qdims[a] = c->qdims[a];
+    int sh = 0;
+    while ((1 << sh) < qb[a] * c->qf) ++sh;
+    P.qshift[a] = sh;
+  }
+  P.buckets_per_env = c->buckets_per_env;
+  P.n_blocks = c->n_env * c->blocks_per_env;
   P.split = split_mode(c) ? 1 : 0;
   P.grid_mode = c->coupling.mode == MSIM_COUPLING_GRID;
   P.r_c_particle = (float)(c->coupling.r_c_factor * d.h);
@@ -275,6 +289,31 @@ void alloc_binning(msim_gpu_ctx* c) {
     CK(c->base_dbg_d.ensure(sizeof(int) * 3 * n));
     CK(cudaMemsetAsync(c->base_dbg_d.p, 0xff, sizeof(int) * 3 * n, c->stream));
   }
+}
+
+// Particle buckets of f^3 node blocks: the key space and its scan buffers.
+// f = 2 for sparse scenes keeps a few hundred particles per bucket (one CTA
+// round) instead of a few dozen, amortising the per-bucket tile load and flush.
+void set_bucket_shape(msim_gpu_ctx* c, int f) {
+  if (f == c->qf) return;
+  const int kb[3] = {kBX, kBY, kBZ};
+  for (int a = 0; a < 3; ++a) c->qdims[a] = (c->desc.dims[a] + kb[a] * f - 1) / (kb[a] * f);
+  c->buckets_per_env = c->qdims[0] * c->qdims[1] * c->qdims[2];
+  c->n_keys = c->n_env * c->buckets_per_env + 1;
+  c->qf = f;
+  CK(c->bucket_count_d.ensure(sizeof(int) * c->n_keys));
+  for (int k = 0; k < 2; ++k) {
+    CK(c->bucket_start_d[k].ensure(sizeof(int) * (c->n_keys + 1)));
+    CK(c->active_buckets_d[k].ensure(sizeof(int) * c->n_keys));
+    CK(c->n_active_d[k].ensure(sizeof(int)));
+    CK(cudaMemset(c->n_active_d[k].p, 0, sizeof(int)));
+  }
+  CK(cudaMemset(c->bucket_count_d.p, 0, sizeof(int) * c->n_keys));
+  const long long scan_n = std::max<long long>(std::max(c->n_keys, c->n_env * c->blocks_per_env),
+                                               std::min<long long>(c->nodes_per_env + 1, INT_MAX));
+  CK(c->scan_tmp_d.ensure(sizeof(int) * scan_tmp_ints((int)scan_n)));
+  CK(cudaDeviceSynchronize());
+  c->perm_valid = false;
 }
 
 // Errors latched on the device: first env (lowest index) wins.
@@ -528,9 +567,8 @@ int msim_gpu_create(const msim_soft_desc* desc, const msim_material* materials, 
     for (int a = 0; a < 3; ++a) c->bdims[a] = (desc->dims[a] + kb[a] - 1) / kb[a];
     c->blocks_per_env = c->bdims[0] * c->bdims[1] * c->bdims[2];
     c->nodes_per_env = (long long)desc->dims[0] * desc->dims[1] * desc->dims[2];
-    long long nk = (long long)n_env * c->blocks_per_env + 1;
-    if (nk > INT_MAX / 2) throw std::runtime_error("too many node blocks for one context");
-    c->n_keys = (int)nk;
+    if ((long long)n_env * c->blocks_per_env + 1 > INT_MAX / 2)
+      throw std::runtime_error("too many node blocks for one context");
     c->env_off_h.assign(n_env + 1, 0);
     c->bodies_h.assign(n_env, {});
     c->shapes_h.assign(n_env, {});
@@ -566,23 +604,14 @@ int msim_gpu_create(const msim_soft_desc* desc, const msim_material* materials, 
     CK(cudaMemset(c->gPM_d.p, 0, sizeof(float4) * nodes));
     CK(cudaMemset(c->gF_d.p, 0, sizeof(float4) * nodes));
     CK(cudaMemset(c->gV_d.p, 0, sizeof(float4) * nodes));
-    int nblocks = c->n_keys - 1;
+    int nblocks = n_env * c->blocks_per_env;
     CK(c->nb_flag_d.ensure(sizeof(int) * nblocks));
     CK(c->nb_scan_d.ensure(sizeof(int) * (nblocks + 1)));
     CK(c->nb_list_d.ensure(sizeof(int) * nblocks));
     CK(c->n_nb_d.ensure(sizeof(int)));
     CK(cudaMemset(c->nb_flag_d.p, 0, sizeof(int) * nblocks));
     CK(cudaMemset(c->n_nb_d.p, 0, sizeof(int)));
-    CK(c->bucket_count_d.ensure(sizeof(int) * c->n_keys));
-    for (int k = 0; k < 2; ++k) {
-      CK(c->bucket_start_d[k].ensure(sizeof(int) * (c->n_keys + 1)));
-      CK(c->active_buckets_d[k].ensure(sizeof(int) * c->n_keys));
-      CK(c->n_active_d[k].ensure(sizeof(int)));
-      CK(cudaMemset(c->n_active_d[k].p, 0, sizeof(int)));
-    }
-    CK(cudaMemset(c->bucket_count_d.p, 0, sizeof(int) * c->n_keys));
-
-    CK(c->scan_tmp_d.ensure(sizeof(int) * scan_tmp_ints(std::max(c->n_keys, (int)std::min<long long>(c->nodes_per_env + 1, INT_MAX)))));
+    set_bucket_shape(c, 1);
     CK(cudaHostAlloc(&c->h_ctl, 4 * sizeof(int), cudaHostAllocMapped));
     CK(c->ctl_d.ensure(4 * sizeof(int)));
     CK(cudaMemset(c->ctl_d.p, 0, 4 * sizeof(int)));
@@ -614,6 +643,18 @@ void msim_gpu_destroy(msim_gpu_ctx* c) {
 
 const char* msim_gpu_last_error(const msim_gpu_ctx* c) { return c ? c->err.c_str() : ""; }
 
+int msim_gpu_set_bucket_factor(msim_gpu_ctx* c, int factor) {
+  return guarded(c, [&]() -> int {
+    if (factor < 0 || factor > 2) return fail(c, MSIM_ERR_INVALID, "set_bucket_factor: factor must be 0 (auto), 1 or 2");
+    c->qf_request = factor;
+    if (factor) {
+      set_device(c);
+      set_bucket_shape(c, factor);
+    }
+    return MSIM_OK;
+  });
+}
+
 int msim_gpu_set_particles(msim_gpu_ctx* c, int64_t n, const int64_t* env_offsets, const double* x,
                            const double* v, const double* F, const double* C, const double* mass,
                            const double* vol0, const int32_t* material) {
@@ -630,6 +671,16 @@ int msim_gpu_set_particles(msim_gpu_ctx* c, int64_t n, const int64_t* env_offset
           return fail(c, MSIM_ERR_INVALID, "set_particles: material index out of range");
     set_device(c);
     cudaStream_t s = c->stream;
+    {  // bucket shape from the particle density (unless requested): particles per cell = h^3 / V0
+      int f = c->qf_request;
+      if (f == 0) {
+        double vsum = 0.0;
+        for (int64_t i = 0; i < n; ++i) vsum += vol0[i];
+        const double ppc = n > 0 ? c->desc.h * c->desc.h * c->desc.h / (vsum / (double)n) : 16.0;
+        f = ppc < 6.0 ? 2 : 1;  // < ~190 particles in a 32-cell bucket: use 8x8x4-cell buckets
+      }
+      set_bucket_shape(c, f);
+    }
     c->n = n;
     c->cur = 0;
     carve_particles(c, 0, n);

@@ -46,7 +46,8 @@ __device__ __forceinline__ bool base_in_range(const SimParams& P, const int* b) 
 
 // Bucket (node block of the base cell) of an in-range base.
 __device__ __forceinline__ int bucket_of(const SimParams& P, int env, const int* b) {
-  return env * P.blocks_per_env + ((b[2] / kBZ) * P.bdims[1] + (b[1] / kBY)) * P.bdims[0] + (b[0] / kBX);
+  return env * P.buckets_per_env + ((b[2] >> P.qshift[2]) * P.qdims[1] + (b[1] >> P.qshift[1])) * P.qdims[0] +
+         (b[0] >> P.qshift[0]);
 }
 
 __device__ __forceinline__ f3 load3(float* const* a, long long i) { return {a[0][i], a[1][i], a[2][i]}; }

@@ -336,6 +336,19 @@ struct ShapeDev {
   int bplane;
 };
 
+// Can any point of the box [lo, hi] be within r_c of the shape? (the bucket-
+// level form of shape_may_touch; same bound, same relative margin)
+__device__ __forceinline__ bool shape_may_touch_box(const ShapeDev& sh, f3 lo, f3 hi, float r_c) {
+  const f3 c = 0.5f * (lo + hi), e = 0.5f * (hi - lo);
+  const float margin = r_c + 1e-4f * (fabsf(c.x) + fabsf(c.y) + fabsf(c.z) + e.x + e.y + e.z + fabsf(sh.bnd[3])) + 1e-6f;
+  if (sh.bplane)
+    return sh.bnd[0] * c.x + sh.bnd[1] * c.y + sh.bnd[2] * c.z + sh.bnd[3] -
+               (fabsf(sh.bnd[0]) * e.x + fabsf(sh.bnd[1]) * e.y + fabsf(sh.bnd[2]) * e.z) < margin;
+  const float dx = fmaxf(fabsf(sh.bnd[0] - c.x) - e.x, 0.0f), dy = fmaxf(fabsf(sh.bnd[1] - c.y) - e.y, 0.0f),
+              dz = fmaxf(fabsf(sh.bnd[2] - c.z) - e.z, 0.0f);
+  return sqrtf(dx * dx + dy * dy + dz * dz) - sh.bnd[3] < margin;
+}
+
 // Can the point x be within r_c of the shape (phi < r_c)? A bound test of a
 // few FMAs ahead of the SDF: a warp whose particles are all far from a
 // collider skips its transform + SDF + gradient. Conservative by a relative

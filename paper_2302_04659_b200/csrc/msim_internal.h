@@ -175,7 +175,14 @@ struct SimParams {
   float gravity[3];
   float h_f, d_inv_f;        // h, 4/h^2
   long long n;               // particles in context
-  int n_keys;                // n_env*blocks_per_env + 1 (lost bucket last)
+  int n_keys;                // n_env*buckets_per_env + 1 (lost bucket last)
+  // particle buckets = qf^3 node blocks (qf = 1 dense scenes, 2 sparse ones):
+  // bucket of base cell b = (b >> qshift) within qdims
+  int qf;
+  int qshift[3];
+  int qdims[3];
+  int buckets_per_env;
+  int n_blocks;              // n_env*blocks_per_env (node-block flags)
   int split;                 // keep momentum and force separately
   int grid_mode;             // coupling mode grid
   float r_c_particle, r_c_grid, c_d;

@@ -57,13 +57,23 @@ namespace {
 // 128 threads / 256 particles per round measured best (64 / 128 at 9 CTAs/SM: +12 %)
 constexpr int kT = MSIM_KT;      // threads per CTA (particle kernel), kCtasPerSm CTAs per SM
 constexpr int kCap = MSIM_KCAP;  // particles staged per round
-constexpr int GX = kBX + 2, GY = kBY + 2, GZ = kBZ + 2, GN = GX * GY * GZ;  // G2P velocity tile
-constexpr int PX = kBX + 4, PY = kBY + 4, PZ = kBZ + 4;  // P2G node tile (origin o-1)
-// z-layer stride padded from 64 to 68 words: the 32 base cells of a bucket then
-// hit 32 distinct shared-memory banks for every stencil offset (searched offline)
-constexpr int kTZS = PX * PY + 4;
-constexpr int PN = PZ * kTZS;
-constexpr int CX = kBX + 2, CY = kBY + 2, CZ = kBZ + 2;  // P2G base cells (origin o-1)
+// Tile geometry of a particle bucket of F^3 node blocks (QX x QY x QZ base cells).
+template <int F>
+struct Geo {
+  static constexpr int QX = kBX * F, QY = kBY * F, QZ = kBZ * F;
+  static constexpr int GX = QX + 2, GY = QY + 2, GZ = QZ + 2, GN = GX * GY * GZ;  // G2P velocity tile
+  static constexpr int PX = QX + 4, PY = QY + 4, PZ = QZ + 4;  // P2G node tile (origin o-1)
+  // z-layer stride padded by 4 words: for F = 1 (64 -> 68) the 32 base cells of a
+  // bucket hit 32 distinct shared-memory banks for every stencil offset
+  static constexpr int TZS = PX * PY + 4;
+  static constexpr int PN = PZ * TZS;
+  static constexpr int CX = QX + 2, CY = QY + 2, CZ = QZ + 2;  // P2G base cells (origin o-1)
+};
+#define MSIM_GEO_ALIASES(F)                                                                            \
+  using Gm = Geo<F>;                                                                                   \
+  [[maybe_unused]] constexpr int QX = Gm::QX, QY = Gm::QY, QZ = Gm::QZ, GX = Gm::GX, GY = Gm::GY,      \
+                                 GZ = Gm::GZ, GN = Gm::GN, PX = Gm::PX, PY = Gm::PY, PZ = Gm::PZ,      \
+                                 kTZS = Gm::TZS, PN = Gm::PN, CX = Gm::CX, CY = Gm::CY, CZ = Gm::CZ;
 template <int NCH> constexpr int pay_floats() { return NCH == 4 ? 24 : 32; }  // staged P2G payload
 #ifndef MSIM_CTAS_PER_SM
 #define MSIM_CTAS_PER_SM 5  // measured: 4 -> 1.12, 5 -> 1.05, 6 -> 1.10 ms per launch (config D, 256 envs)
@@ -112,12 +122,14 @@ struct ItemCtx {
   int key, benv, s, e, act, ox, oy, oz, s0, s1;
   float dt, dtp;
   int lostb, do_g2p, do_p2g, penalty;
+  unsigned smask;      // env shapes (bit k = shape s0 + k, k < 32) that can reach the bucket box
+  float blo[3], bhi[3];  // the bucket's particles' box widened by 2 h (positions after G2P)
 };
 
-template <int NCH>
+template <int NCH, int F>
 struct Smem {
-  float4 gtile[GN];
-  int itile[NCH][PN];      // fixed-point node accumulators (native int shared atomics)
+  float4 gtile[Geo<F>::GN];
+  int itile[NCH][Geo<F>::PN];  // fixed-point node accumulators (native int shared atomics)
   float4 pay[pay_floats<NCH>() / 4][kCap];  // float4 k of slot t at pay[k][t]: conflict-free
   int cellof[kCap];        // local P2G cell of each staged slot, -1 if not staged
   double wsum[kWs];
@@ -178,8 +190,9 @@ __device__ MSIM_COLD void scatter_global(const SimParams& P, int env, const int*
 
 // The rounds of one bucket (<= kCap particles each): per-particle phase, then
 // the fixed-point scatter and flush. Bucket-uniform values come from S.ic.
-template <int NCH>
-__device__ __forceinline__ void item_rounds(const SimParams& P, Smem<NCH>& S, bool redo) {
+template <int NCH, int F>
+__device__ __forceinline__ void item_rounds(const SimParams& P, Smem<NCH, F>& S, bool redo) {
+  MSIM_GEO_ALIASES(F)
   const int tid = threadIdx.x, lane = tid & 31;
   const unsigned FULL = 0xffffffffu;
   volatile ItemCtx& IC = S.ic;
@@ -338,7 +351,14 @@ __device__ __forceinline__ void item_rounds(const SimParams& P, Smem<NCH>& S, bo
 
         // IC.penalty hook: warp-cooperative per shape (coupling.hpp:151-172)
         if (IC.penalty) {
+          // shapes outside the bucket box are skipped warp-wide; a warp with a
+          // particle outside the box (moved > 2 h) tests every shape
+          const bool inbox = x.x >= IC.blo[0] && x.y >= IC.blo[1] && x.z >= IC.blo[2] && x.x <= IC.bhi[0] &&
+                             x.y <= IC.bhi[1] && x.z <= IC.bhi[2];
+          const unsigned smask = (kNoCull || __any_sync(FULL, scatter_me && !inbox)) ? ~0u : IC.smask;
           for (int sidx = IC.s0; sidx < IC.s1; ++sidx) {
+            const int k = sidx - IC.s0;
+            if (k < 32 && !((smask >> k) & 1u)) continue;  // warp-uniform
             const ShapeDev& sh = P.shapes[sidx];
             f3 f = {0.f, 0.f, 0.f};
             float pen = 0.f;
@@ -600,10 +620,11 @@ __device__ __forceinline__ void item_rounds(const SimParams& P, Smem<NCH>& S, bo
   }
 }
 
-template <int NCH>
+template <int NCH, int F>
 __global__ void __launch_bounds__(kT, kCtasPerSm) k_particles(SimParams P) {
+  MSIM_GEO_ALIASES(F)
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  Smem<NCH>& S = *reinterpret_cast<Smem<NCH>*>(smem_raw);
+  Smem<NCH, F>& S = *reinterpret_cast<Smem<NCH, F>*>(smem_raw);
   const int tid = threadIdx.x;
   const bool redo = P.redo_pass != 0;
   if (redo && !*P.any_redo) return;
@@ -615,15 +636,15 @@ __global__ void __launch_bounds__(kT, kCtasPerSm) k_particles(SimParams P) {
   for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
     const int key = P.active_buckets[item];
     const bool lostb = key == P.n_keys - 1;
-    const int benv = lostb ? 0 : key / P.blocks_per_env;
+    const int benv = lostb ? 0 : key / P.buckets_per_env;
     if (redo && (lostb || !P.run[benv].redo)) continue;  // CTA-uniform
     const int s = P.bucket_start[key], e = P.bucket_start[key + 1];
     const int act = lostb ? kActIdle : P.run[benv].action;
     const bool do_g2p = act == kActFused || act == kActG2P;
     const bool do_p2g = act == kActP2G || act == kActFused;
-    const int lb = key - benv * P.blocks_per_env;
-    const int ox = kBX * (lb % P.bdims[0]), oy = kBY * ((lb / P.bdims[0]) % P.bdims[1]),
-              oz = kBZ * (lb / (P.bdims[0] * P.bdims[1]));
+    const int lb = key - benv * P.buckets_per_env;
+    const int ox = QX * (lb % P.qdims[0]), oy = QY * ((lb / P.qdims[0]) % P.qdims[1]),
+              oz = QZ * (lb / (P.qdims[0] * P.qdims[1]));
     const float dt = do_g2p ? P.run[benv].dt_g2p : 0.0f;
     const float dtp = lostb ? 0.0f : (redo ? P.run[benv].dt_c : P.run[benv].dt_p2g);  // NCH == 4 only
     const int s0 = lostb ? 0 : P.shape_off[benv], s1 = lostb ? 0 : P.shape_off[benv + 1];
@@ -642,6 +663,21 @@ __global__ void __launch_bounds__(kT, kCtasPerSm) k_particles(SimParams P) {
     }
     if (penalty && !redo)
       for (int t = tid; t < kWs; t += kT) S.wsum[t] = 0.0;
+    if (penalty && tid < 32) {  // bucket-level collider culling (exact: see item_rounds)
+      // old positions lie in cells [o + 0.5, o + kB + 0.5) h; 2 h of slack for the G2P move
+      const float h = P.h_f;
+      const f3 lo = {(float)P.origin[0] + h * (ox - 1.5f), (float)P.origin[1] + h * (oy - 1.5f),
+                     (float)P.origin[2] + h * (oz - 1.5f)};
+      const f3 hi = {(float)P.origin[0] + h * (ox + QX + 2.5f), (float)P.origin[1] + h * (oy + QY + 2.5f),
+                     (float)P.origin[2] + h * (oz + QZ + 2.5f)};
+      const bool b = tid < s1 - s0 && shape_may_touch_box(P.shapes[s0 + tid], lo, hi, P.r_c_particle);
+      const unsigned m = __ballot_sync(0xffffffffu, b);
+      if (tid == 0) {
+        IC.smask = m;
+        IC.blo[0] = lo.x; IC.blo[1] = lo.y; IC.blo[2] = lo.z;
+        IC.bhi[0] = hi.x; IC.bhi[1] = hi.y; IC.bhi[2] = hi.z;
+      }
+    }
     if (tid == 0) {
       S.penmax = 0u;
       IC.key = key; IC.benv = benv; IC.s = s; IC.e = e; IC.act = act;
@@ -650,7 +686,7 @@ __global__ void __launch_bounds__(kT, kCtasPerSm) k_particles(SimParams P) {
       IC.lostb = lostb; IC.do_g2p = do_g2p; IC.do_p2g = do_p2g; IC.penalty = penalty;
     }
     __syncthreads();
-    item_rounds<NCH>(P, S, redo);
+    item_rounds<NCH, F>(P, S, redo);
   }
 }
 
@@ -974,18 +1010,34 @@ struct Timed {
   }
 };
 
+// persistent grid: as many CTAs as fit on the device at once (occupancy query)
+template <int NCH, int F>
+void launch_k_particles(const SimParams& P, cudaStream_t s) {
+  static int per_sm = 0;
+  if (!per_sm) {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_particles<NCH, F>, kT, sizeof(Smem<NCH, F>));
+    if (per_sm <= 0) per_sm = 1;
+  }
+  k_particles<NCH, F><<<sm_count() * per_sm, kT, sizeof(Smem<NCH, F>), s>>>(P);
+}
+
 void particle_kernel(const SimParams& P, cudaStream_t s) {
-  if (P.split)
-    k_particles<7><<<sm_count() * kCtasPerSm, kT, sizeof(Smem<7>), s>>>(P);
-  else
-    k_particles<4><<<sm_count() * kCtasPerSm, kT, sizeof(Smem<4>), s>>>(P);
+  if (P.qf == 2) {
+    if (P.split) launch_k_particles<7, 2>(P, s);
+    else launch_k_particles<4, 2>(P, s);
+  } else {
+    if (P.split) launch_k_particles<7, 1>(P, s);
+    else launch_k_particles<4, 1>(P, s);
+  }
 }
 
 }  // namespace
 
 void configure_kernels() {
-  cudaFuncSetAttribute(k_particles<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(Smem<4>));
-  cudaFuncSetAttribute(k_particles<7>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(Smem<7>));
+  cudaFuncSetAttribute(k_particles<4, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(Smem<4, 1>));
+  cudaFuncSetAttribute(k_particles<7, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(Smem<7, 1>));
+  cudaFuncSetAttribute(k_particles<4, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(Smem<4, 2>));
+  cudaFuncSetAttribute(k_particles<7, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(Smem<7, 2>));
 }
 
 void launch_rebin(const SimParams& P, cudaStream_t s) {
@@ -1033,7 +1085,7 @@ void launch_particles(const SimParams& P, cudaStream_t s) {
     if (P.n > 0) k_perm<<<nblk(P.n), 256, 0, s>>>(P);
   }
   Timed tm(P, kKBlockScan, s, 3);
-  scan_exclusive(P.nb_flag, P.nb_scan, P.n_keys - 1, P.nb_list, P.n_nb, P.scan_tmp, s);
+  scan_exclusive(P.nb_flag, P.nb_scan, P.n_blocks, P.nb_list, P.n_nb, P.scan_tmp, s);
 }
 
 void launch_grid(const SimParams& P, cudaStream_t s) {

@@ -84,6 +84,21 @@ def test_config_d_sampled_envs():
             assert np.linalg.norm(fg[b] - fo[b]) / max(np.linalg.norm(fo[b]), 1e-6) < WRENCH_TOL, (e, b)
 
 
+@pytest.mark.parametrize("cfg,factor", [(config_a, 2), (config_c, 1), (lambda: config_d(n_envs=4), 2)])
+def test_bucket_factor_is_internal(cfg, factor):
+    """Particle buckets of 1 or 2^3 node blocks (chosen from the density by
+    default: A/D dense -> 1, C sparse -> 2): the other shape gives the same
+    physics within the parity bars."""
+    scene = cfg()
+    gw = GpuWorld(scene, bucket_factor=factor)
+    _check_step(scene, env_g=0, gw=gw, label=f"{scene.name} factor {factor}")  # one env step vs the oracle
+    gw2 = GpuWorld(scene)  # the automatic choice
+    gw2.env_step()
+    for e in range(len(scene.envs)):
+        a, b = gw.particles(e), gw2.particles(e)
+        assert _x_err(a["x"], b["x"]) < X_TOL and rel(a["v"], b["v"]) < V_TOL
+
+
 def test_integer_binning_bit_exact():
     """base, cell_start, cell_particles (index-stable), active_nodes == reference layout."""
     scene = round_f32(config_a())
