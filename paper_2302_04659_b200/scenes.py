@@ -318,19 +318,20 @@ def config_d(n_envs: int = 1024, first_env: int = 0) -> Scene:
                  c_d=0.05)
 
 
-def config_e(clay_only: bool = True) -> Scene:
+def config_e(clay_only: bool = True, slab=(50, 200, 100), grid: int = 256) -> Scene:
     """E: 4M particles in 4 x-slabs (soft / stiff clay alternating in the clay-only
     parity variant), 256^3 h=0.005, 8 moving colliders (3 boxes, 2 spheres,
-    2 capsules, 1 SDF volume)."""
+    2 capsules, 1 SDF volume). `slab` / `grid` give reduced parity variants."""
     s = V0_SOFT ** (1.0 / 3.0)
-    span = lattice_span(200, V0_SOFT)
-    lo = ((1.28 - span) / 2, (1.28 - span) / 2, 0.021)
+    extent = grid * 0.005
+    span = lattice_span(slab[1], V0_SOFT)
+    lo = ((extent - span) / 2, (extent - span) / 2, 0.021)
     xs, ms, mats = [], [], []
     for k in range(4):
-        slab_lo = (lo[0] + k * 50 * s, lo[1], lo[2])
+        slab_lo = (lo[0] + k * slab[0] * s, lo[1], lo[2])
         mid = k % 2
         mat = SOFT_CLAY if mid == 0 else STIFF_CLAY
-        e = block_env(slab_lo, (50, 200, 100), mid, mat, V0_SOFT, seed=7 + 10 * k)
+        e = block_env(slab_lo, slab, mid, mat, V0_SOFT, seed=7 + 10 * k)
         xs.append(e.x)
         ms.append(e.mass)
         mats.append(e.material)
@@ -342,9 +343,10 @@ def config_e(clay_only: bool = True) -> Scene:
     rng = np.random.default_rng(7)
     bodies, shapes = [], []
     kinds = [abi.SHAPE_BOX] * 3 + [abi.SHAPE_SPHERE] * 2 + [abi.SHAPE_CAPSULE] * 2 + [abi.SHAPE_VOLUME]
-    top = lo[2] + lattice_span(100, V0_SOFT)
+    top = lo[2] + lattice_span(slab[2], V0_SOFT)
     for i, kind in enumerate(kinds):
-        cx, cy = rng.uniform(lo[0] + 0.05, lo[0] + span - 0.05, size=2)
+        margin = 0.05 * span / lattice_span(200, V0_SOFT)  # 0.05 m at full size
+        cx, cy = rng.uniform(lo[0] + margin, lo[0] + span - margin, size=2)
         q = quat_from_axis_angle(rng.normal(size=3), rng.uniform(0, math.pi))
         bodies.append(BodySpec(mode=abi.BODY_SCRIPTED, q=q, t=(cx, cy, top + 0.01),
                                v=tuple(rng.uniform(-0.05, 0.05, size=2)) + (-0.05,),
@@ -361,7 +363,7 @@ def config_e(clay_only: bool = True) -> Scene:
                                     **soft_contact()))
     env.bodies = bodies
     env.shapes = shapes
-    return Scene(name="E", dims=(256, 256, 256), h=0.005, dt=1e-4, materials=[SOFT_CLAY, STIFF_CLAY],
+    return Scene(name="E", dims=(grid, grid, grid), h=0.005, dt=1e-4, materials=[SOFT_CLAY, STIFF_CLAY],
                  envs=[env], c_d=0.05)
 
 

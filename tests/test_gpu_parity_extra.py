@@ -149,3 +149,16 @@ def test_divergence_errors_match_reference_semantics():
     gw = GpuWorld(scene)
     with pytest.raises(SimulationDiverged, match="lost particle fraction"):
         gw.env_step()
+
+
+def test_config_e_reduced_sparse_many_colliders():
+    """E's structure at a size the oracle runs in seconds: 55k particles in 4
+    soft / stiff slabs at 2 particles per cell (sparse: 2^3-node-block
+    buckets), 8 scripted colliders incl. an SDF volume (collider culling)."""
+    from paper_2302_04659_b200.scenes import config_e
+
+    scene = config_e(slab=(12, 48, 24), grid=64)
+    scene.n_rigid = 10
+    gw, ows, _ = compare(scene)
+    fg, _ = gw.wrenches(0, pending=True)
+    assert np.count_nonzero(np.linalg.norm(fg, axis=1)) >= 2  # colliders in contact
