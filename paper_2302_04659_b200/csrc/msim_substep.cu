@@ -68,13 +68,21 @@ struct Geo {
   static constexpr int TZS = PX * PY + 4;
   static constexpr int PN = PZ * TZS;
   static constexpr int CX = QX + 2, CY = QY + 2, CZ = QZ + 2;  // P2G base cells (origin o-1)
+  // particles per round (512 measured 5 % slower on D than 256: four trips
+  // between barriers instead of two)
+  static constexpr int CAP = kCap;
+  // fixed point: |contribution| <= 2^SC_LOG2, CAP contributions per node <= 2^30
+  static constexpr int SC_LOG2 = CAP == 512 ? 21 : (CAP == 256 ? 22 : 23);
 };
 #define MSIM_GEO_ALIASES(F)                                                                            \
   using Gm = Geo<F>;                                                                                   \
   [[maybe_unused]] constexpr int QX = Gm::QX, QY = Gm::QY, QZ = Gm::QZ, GX = Gm::GX, GY = Gm::GY,      \
                                  GZ = Gm::GZ, GN = Gm::GN, PX = Gm::PX, PY = Gm::PY, PZ = Gm::PZ,      \
-                                 kTZS = Gm::TZS, PN = Gm::PN, CX = Gm::CX, CY = Gm::CY, CZ = Gm::CZ;
-template <int NCH> constexpr int pay_floats() { return NCH == 4 ? 24 : 32; }  // staged P2G payload
+                                 kTZS = Gm::TZS, PN = Gm::PN, CX = Gm::CX, CY = Gm::CY, CZ = Gm::CZ,  \
+                                 CAP = Gm::CAP;
+// staged P2G payload per particle: m, fx (weights recomputed in the scatter), b, A
+// (+ b_f, symmetric A_f in 7-channel mode)
+template <int NCH> constexpr int pay_floats() { return NCH == 4 ? 16 : 28; }
 #ifndef MSIM_CTAS_PER_SM
 #define MSIM_CTAS_PER_SM 5  // measured: 4 -> 1.12, 5 -> 1.05, 6 -> 1.10 ms per launch (config D, 256 envs)
 #endif
@@ -130,8 +138,8 @@ template <int NCH, int F>
 struct Smem {
   float4 gtile[Geo<F>::GN];
   int itile[NCH][Geo<F>::PN];  // fixed-point node accumulators (native int shared atomics)
-  float4 pay[pay_floats<NCH>() / 4][kCap];  // float4 k of slot t at pay[k][t]: conflict-free
-  int cellof[kCap];        // local P2G cell of each staged slot, -1 if not staged
+  float4 pay[pay_floats<NCH>() / 4][Geo<F>::CAP];  // float4 k of slot t at pay[k][t]: conflict-free
+  int cellof[Geo<F>::CAP];  // local P2G cell of each staged slot, -1 if not staged
   double wsum[kWs];
   unsigned penmax;
   unsigned maxb[3];
@@ -148,14 +156,14 @@ __device__ __forceinline__ float warp_sum(float v) {
 constexpr int gcd_c(int a, int b) { return b ? gcd_c(b, a % b) : a; }
 // Scatter slot stride per round size rn: odd, coprime with rn, ~0.618 rn (see k_particles)
 struct SpreadTable {
-  unsigned char g[kCap + 1];
+  unsigned short g[kCap + 1];
 };
 constexpr SpreadTable make_spread() {
   SpreadTable t{};
   for (int rn = 1; rn <= kCap; ++rn) {
     int g = ((int)(0.618034 * rn)) | 1;
     while (gcd_c(g, rn) != 1) g += 2;
-    t.g[rn] = (unsigned char)g;
+    t.g[rn] = (unsigned short)g;
   }
   return t;
 }
@@ -198,8 +206,8 @@ __device__ __forceinline__ void item_rounds(const SimParams& P, Smem<NCH, F>& S,
   volatile ItemCtx& IC = S.ic;
   {
 
-    for (int r0 = IC.s; r0 < IC.e; r0 += kCap) {
-      const int rn = min(kCap, IC.e - r0);
+    for (int r0 = IC.s; r0 < IC.e; r0 += CAP) {
+      const int rn = min(CAP, IC.e - r0);
       const int trips = (rn + kT - 1) / kT;
       if (tid < 3) S.maxb[tid] = 0u;
       float mx_m = 0.f, mx_p = 0.f, mx_f = 0.f;
@@ -420,17 +428,16 @@ __device__ __forceinline__ void item_rounds(const SimParams& P, Smem<NCH, F>& S,
           const int lx = b2[0] - (IC.ox - 1), ly = b2[1] - (IC.oy - 1), lz = b2[2] - (IC.oz - 1);
           if (lx >= 0 && ly >= 0 && lz >= 0 && lx < CX && ly < CY && lz < CZ) {
             cell = (lz * CY + ly) * CX + lx;
-            // [m wx0 wx1 wx2] [wy0 wy1 wy2 wz0] [wz1 wz2 b.x b.y] [b.z A00 A01 A02] [A10 A11 A12 A20]
-            // [A21 A22 bf.x bf.y] [bf.z Af00 Af01 Af02] [Af11 Af12 Af22 -]   (Af symmetric)
-            S.pay[0][t] = make_float4(m, w9[0], w9[1], w9[2]);
-            S.pay[1][t] = make_float4(w9[3], w9[4], w9[5], w9[6]);
-            S.pay[2][t] = make_float4(w9[7], w9[8], bb.x, bb.y);
-            S.pay[3][t] = make_float4(bb.z, A[0], A[1], A[2]);
-            S.pay[4][t] = make_float4(A[3], A[4], A[5], A[6]);
-            S.pay[5][t] = make_float4(A[7], A[8], bf.x, bf.y);
+            // [m fx0 fx1 fx2] [b.x b.y b.z A00] [A01 A02 A10 A11] [A12 A20 A21 A22]
+            // (+ [bf.x bf.y bf.z Af00] [Af01 Af02 Af11 Af12] [Af22 - - -], Af symmetric)
+            S.pay[0][t] = make_float4(m, fx2[0], fx2[1], fx2[2]);
+            S.pay[1][t] = make_float4(bb.x, bb.y, bb.z, A[0]);
+            S.pay[2][t] = make_float4(A[1], A[2], A[3], A[4]);
+            S.pay[3][t] = make_float4(A[5], A[6], A[7], A[8]);
             if constexpr (NCH == 7) {
-              S.pay[6][t] = make_float4(bf.z, Af[0], Af[1], Af[2]);
-              S.pay[7][t] = make_float4(Af[4], Af[5], Af[8], 0.f);
+              S.pay[4][t] = make_float4(bf.x, bf.y, bf.z, Af[0]);
+              S.pay[5][t] = make_float4(Af[1], Af[2], Af[4], Af[5]);
+              S.pay[6][t] = make_float4(Af[8], 0.f, 0.f, 0.f);
             }
             staged = true;
             // bounds of |b + A off| over off in {0,1,2}^3 for the fixed-point scales
@@ -449,7 +456,7 @@ __device__ __forceinline__ void item_rounds(const SimParams& P, Smem<NCH, F>& S,
             scatter_global<NCH>(P, penv, b2, w9, m, bb, A, bf, Af, !redo);
           }
         }
-        if (t < kCap) S.cellof[t] = staged ? cell : -1;
+        if (t < CAP) S.cellof[t] = staged ? cell : -1;
 
         if (!redo) {
           // ---------------- write back in bucket order (the re-sort)
@@ -500,12 +507,13 @@ __device__ __forceinline__ void item_rounds(const SimParams& P, Smem<NCH, F>& S,
 
       // ---------------- per-thread scatter of one staged particle into the fixed-point tile
       {
-        // fixed-point scale: every contribution |w (b + A off)| <= bound -> |x| <= 2^22, so a
-        // node sum of <= kCap = 256 contributions stays below 2^30 (no int32 overflow)
+        // fixed-point scale: every contribution |w (b + A off)| <= bound -> |x| <= 2^SC_LOG2,
+        // so a node sum of <= CAP contributions stays below 2^30 (no int32 overflow)
+        constexpr float kFix = (float)(1 << Gm::SC_LOG2);
         const float bm = __uint_as_float(S.maxb[0]), bpm = __uint_as_float(S.maxb[1]), bfm = __uint_as_float(S.maxb[2]);
-        const float sc_m = bm > 0.f ? 4194304.0f / bm : 0.f;
-        const float sc_p = bpm > 0.f ? 4194304.0f / bpm : 0.f;
-        const float sc_f = bfm > 0.f ? 4194304.0f / bfm : 0.f;
+        const float sc_m = bm > 0.f ? kFix / bm : 0.f;
+        const float sc_p = bpm > 0.f ? kFix / bpm : 0.f;
+        const float sc_f = bfm > 0.f ? kFix / bfm : 0.f;
         // Golden-ratio spread: consecutive lanes take staged slots ~0.618 rn apart
         // (odd, coprime with rn: a bijection on [0, rn)), i.e. particles spread over
         // the whole bucket, so a warp's 27-node stencils rarely share a node (staged
@@ -520,15 +528,18 @@ __device__ __forceinline__ void item_rounds(const SimParams& P, Smem<NCH, F>& S,
 #ifdef MSIM_ABLATE_SCATTER  // profiling-only build: no shared atomics
           if (c >= 0) continue;
 #endif
-          const float4 q0 = S.pay[0][t], q1 = S.pay[1][t], q2 = S.pay[2][t], q3 = S.pay[3][t], q4 = S.pay[4][t],
-                       q5 = S.pay[5][t];
-          const float wx[3] = {q0.y, q0.z, q0.w}, wy[3] = {q1.x, q1.y, q1.z}, wz[3] = {q1.w, q2.x, q2.y};
+          const float4 q0 = S.pay[0][t], q1 = S.pay[1][t], q2 = S.pay[2][t], q3 = S.pay[3][t];
+          float wx[3], wy[3], wz[3];
+          bspline_w(q0.y, wx);
+          bspline_w(q0.z, wy);
+          bspline_w(q0.w, wz);
           const float ms = q0.x * sc_m;
-          // A row-major: A00 q3.y A01 q3.z A02 q3.w A10 q4.x A11 q4.y A12 q4.z A20 q4.w A21 q5.x A22 q5.y
-          float4 qf6 = make_float4(0.f, 0.f, 0.f, 0.f), qf7 = qf6;
+          // b = q1.xyz; A row-major: A00 q1.w A01 q2.x A02 q2.y A10 q2.z A11 q2.w A12 q3.x A20 q3.y A21 q3.z A22 q3.w
+          float4 qf4 = make_float4(0.f, 0.f, 0.f, 0.f), qf5 = qf4, qf6 = qf4;
           if constexpr (NCH == 7) {
+            qf4 = S.pay[4][t];
+            qf5 = S.pay[5][t];
             qf6 = S.pay[6][t];
-            qf7 = S.pay[7][t];
           }
           const int cx = c % CX, cy = (c / CX) % CY, cz = c / (CX * CY);
 #pragma unroll kScatterDkUnroll
@@ -537,14 +548,14 @@ __device__ __forceinline__ void item_rounds(const SimParams& P, Smem<NCH, F>& S,
 #pragma unroll kScatterDjUnroll
             for (int dj = 0; dj < 3; ++dj) {
               const float wyz = (dj == 0 ? wy[0] : (dj == 1 ? wy[1] : wy[2])) * wzk;
-              float rx = q2.z + q3.z * dj + q3.w * dk;
-              float ry = q2.w + q4.y * dj + q4.z * dk;
-              float rz = q3.x + q5.x * dj + q5.y * dk;
+              float rx = q1.x + q2.x * dj + q2.y * dk;  // b.x + A01 dj + A02 dk
+              float ry = q1.y + q2.w * dj + q3.x * dk;  // b.y + A11 dj + A12 dk
+              float rz = q1.z + q3.z * dj + q3.w * dk;  // b.z + A21 dj + A22 dk
               float fxr = 0.f, fyr = 0.f, fzr = 0.f;
               if (NCH == 7) {
-                fxr = q5.z + qf6.z * dj + qf6.w * dk;  // bf.x + Af01 dj + Af02 dk
-                fyr = q5.w + qf7.x * dj + qf7.y * dk;  // bf.y + Af11 dj + Af12 dk
-                fzr = qf6.x + qf7.y * dj + qf7.z * dk; // bf.z + Af12 dj + Af22 dk
+                fxr = qf4.x + qf5.x * dj + qf5.y * dk;  // bf.x + Af01 dj + Af02 dk
+                fyr = qf4.y + qf5.z * dj + qf5.w * dk;  // bf.y + Af11 dj + Af12 dk
+                fzr = qf4.z + qf5.w * dj + qf6.x * dk;  // bf.z + Af12 dj + Af22 dk
               }
               const int nt = (cz + dk) * kTZS + (cy + dj) * PX + cx;
 #pragma unroll kScatterDiUnroll
@@ -555,13 +566,13 @@ __device__ __forceinline__ void item_rounds(const SimParams& P, Smem<NCH, F>& S,
                 atomicAdd(&S.itile[0][nt + di], fix_rn(wp * rx));
                 atomicAdd(&S.itile[1][nt + di], fix_rn(wp * ry));
                 atomicAdd(&S.itile[2][nt + di], fix_rn(wp * rz));
-                rx += q3.y; ry += q4.x; rz += q4.w;  // + column 0 (A00, A10, A20)
+                rx += q1.w; ry += q2.z; rz += q3.y;  // + column 0 (A00, A10, A20)
                 if (NCH == 7) {
                   const float wf = w * sc_f;
                   atomicAdd(&S.itile[4 % NCH][nt + di], fix_rn(wf * fxr));
                   atomicAdd(&S.itile[5 % NCH][nt + di], fix_rn(wf * fyr));
                   atomicAdd(&S.itile[6 % NCH][nt + di], fix_rn(wf * fzr));
-                  fxr += qf6.y; fyr += qf6.z; fzr += qf6.w;  // + column 0 (Af00, Af01, Af02)
+                  fxr += qf4.w; fyr += qf5.x; fzr += qf5.y;  // + column 0 (Af00, Af01, Af02)
                 }
               }
             }
