@@ -76,7 +76,13 @@ extern "C" {
 
 /* Constitutive model selector. HENCKY_VON_MISES is the reference's only
  * model (mpm.hpp:150-181). */
-#define MSIM_MODEL_HENCKY_VON_MISES 0
+#define MSIM_MODEL_HENCKY_VON_MISES 0  /* mpm.hpp:152-181, the reference's model */
+/* The north_star's other materials (no reference implementation: parity with
+ * the oracle's restatement of the published algorithms):      */
+#define MSIM_MODEL_FIXED_COROTATED 1   /* elastic: tau = 2 mu (F - R) F^T + lambda (J - 1) J I   */
+#define MSIM_MODEL_DRUCKER_PRAGER 2    /* sand: Hencky + log-strain cone projection (Klar 2016);
+                                          yield_stress holds the friction angle in degrees     */
+#define MSIM_MODEL_FLUID 3             /* J-only weakly compressible: tau = K (J - 1) J I      */
 
 /* MpmGrid (mpm.hpp:65-107) + SoftState stepping parameters (mpm.hpp:115-120). */
 typedef struct msim_soft_desc {

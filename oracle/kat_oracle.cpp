@@ -1271,6 +1271,95 @@ TEST(Pinch, HalfwayInterpolationMatchesBruteForceRatio) {  // :259-273
   EXPECT(r.success == (r.ratio < 0.3));
 }
 
+// ---- north_star materials (analytic KATs: no reference test exists) --------
+namespace {
+Material model_mat(Model md, double yield = 2e3) {
+  Material m = soft_clay();
+  m.model = md;
+  m.yield_stress = yield;
+  return m;
+}
+}  // namespace
+TEST(FixedCorotated, RestAndRotationAreStressFree) {
+  Material m = model_mat(Model::FixedCorotated);
+  EXPECT(kirchhoff_fixed_corotated(M3::Identity(), m).norm() < 1e-12);
+  auto g = rng(41);
+  M3 r = random_quat(g).toRotationMatrix();
+  EXPECT(kirchhoff_fixed_corotated(r, m).norm() < 1e-9);
+}
+TEST(FixedCorotated, SmallStrainMatchesLinearElasticity) {
+  Material m = model_mat(Model::FixedCorotated);
+  const double e = 1e-4;
+  M3 f = M3::Identity();
+  f.m[0][0] = 1.0 + e;
+  M3 tau = kirchhoff_fixed_corotated(f, m);
+  EXPECT_NEAR(tau.m[0][0], (2.0 * m.mu() + m.lambda()) * e, 1e-3 * (2.0 * m.mu() + m.lambda()) * e);
+  EXPECT_NEAR(tau.m[1][1], m.lambda() * e, 1e-3 * m.lambda() * e);
+}
+TEST(FixedCorotated, IsotropicScalingClosedForm) {
+  Material m = model_mat(Model::FixedCorotated);
+  const double sc = 1.07, J = sc * sc * sc;
+  M3 tau = kirchhoff_fixed_corotated(M3::Identity() * sc, m);
+  const double expect = 2.0 * m.mu() * (sc - 1.0) * sc + m.lambda() * (J - 1.0) * J;
+  for (int i = 0; i < 3; ++i) EXPECT_NEAR(tau.m[i][i], expect, 1e-10 * std::abs(expect));
+  EXPECT(std::abs(tau.m[0][1]) < 1e-9 && std::abs(tau.m[1][2]) < 1e-9);
+}
+TEST(DruckerPrager, TensionProjectsToTheTip) {
+  Material m = model_mat(Model::DruckerPrager, 30.0);
+  auto g = rng(43);
+  M3 r = random_quat(g).toRotationMatrix();
+  M3 f = r * M3::diag(V3(1.02, 1.01, 1.005));
+  double q = 0.0;
+  M3 fp = drucker_prager_return_map(f, m, q);
+  Svd3 s = svd3(fp);
+  EXPECT(std::abs(s.s.x - 1.0) < 1e-12 && std::abs(s.s.y - 1.0) < 1e-12 && std::abs(s.s.z - 1.0) < 1e-12);
+  EXPECT_NEAR(q, V3(std::log(1.02), std::log(1.01), std::log(1.005)).norm(), 1e-12);
+}
+TEST(DruckerPrager, InsideTheConeUnchanged) {
+  Material m = model_mat(Model::DruckerPrager, 30.0);
+  M3 f = M3::diag(V3(0.99, 0.985, 0.99));  // compression, small shear
+  double q = 0.5;
+  M3 fp = drucker_prager_return_map(f, m, q);
+  EXPECT((fp - f).norm() == 0.0 && q == 0.5);
+}
+TEST(DruckerPrager, ProjectionLandsOnTheCone) {
+  Material m = model_mat(Model::DruckerPrager, 25.0);
+  auto g = rng(47);
+  for (int t = 0; t < 50; ++t) {
+    M3 r = random_quat(g).toRotationMatrix();
+    V3 sig(std::exp(uniform(g, -0.02, 0.002)), std::exp(uniform(g, -0.02, 0.002)), std::exp(uniform(g, -0.08, 0.0)));
+    M3 f = r * M3::diag(sig);
+    double q = 0.0;
+    M3 fp = drucker_prager_return_map(f, m, q);
+    Svd3 s = svd3(fp);
+    V3 e(std::log(s.s.x), std::log(s.s.y), std::log(s.s.z));
+    const double tr = e.x + e.y + e.z;
+    const double dn = (e - V3(tr / 3.0, tr / 3.0, tr / 3.0)).norm();
+    const double yield = dn + (3.0 * m.lambda() + 2.0 * m.mu()) / (2.0 * m.mu()) * tr * m.dp_alpha();
+    EXPECT(yield <= 1e-10);                       // never outside the cone
+    if (q > 0.0) EXPECT(std::abs(yield) < 1e-10 || (dn < 1e-12 && std::abs(tr) < 1e-12));  // on it when projected
+    EXPECT(std::abs(fp.determinant() - std::exp(tr)) < 1e-10);
+  }
+}
+TEST(Fluid, PressureAndVolumeUpdate) {
+  Material m = model_mat(Model::Fluid);
+  Particle p;
+  p.jp = 0.97;
+  M3 tau = kirchhoff_of(p, m);
+  EXPECT_NEAR(tau.m[0][0], m.bulk() * (0.97 - 1.0) * 0.97, 1e-12 * m.bulk());
+  EXPECT(tau.m[0][1] == 0.0);
+  p.C = M3::diag(V3(0.5, -0.2, 0.1));
+  plasticity_update(p, m, 1e-3);
+  EXPECT_NEAR(p.jp, 0.97 * (1.0 + 1e-3 * 0.4), 1e-15);
+  EXPECT((p.F - M3::Identity()).norm() == 0.0);
+}
+TEST(Materials, ValidationPerModel) {
+  Material dp = model_mat(Model::DruckerPrager, 95.0);
+  EXPECT_THROW(dp.validate(), std::invalid_argument);
+  Material fl = model_mat(Model::Fluid, 0.0);
+  fl.validate();  // yield stress unused
+}
+
 int main(int argc, char** argv) {
   std::string filter = argc > 1 ? argv[1] : "";
   for (const Reg& r : registry()) {

@@ -304,14 +304,29 @@ void parallel_for(std::int64_t n, F&& body) {
 // ---------------------------------------------------------------------------
 // MPM state: mpm.hpp:24-145.
 
-struct Material {  // mpm.hpp:24-42
+// Constitutive models. Hencky + von Mises is the reference's (mpm.hpp:152-181);
+// the other three are the north_star's material set, absent from the reference
+// (parity unpinned): restated from their published algorithms below.
+enum class Model : int { HenckyVonMises = 0, FixedCorotated = 1, DruckerPrager = 2, Fluid = 3 };
+
+struct Material {  // mpm.hpp:24-42 (+ model; yield_stress = friction angle in degrees for DruckerPrager)
   double density = 1000.0, youngs = 1e4, poisson = 0.3, yield_stress = 2e3;
+  Model model = Model::HenckyVonMises;
   double mu() const { return youngs / (2.0 * (1.0 + poisson)); }
   double lambda() const { return youngs * poisson / ((1.0 + poisson) * (1.0 - 2.0 * poisson)); }
+  double bulk() const { return youngs / (3.0 * (1.0 - 2.0 * poisson)); }
+  // Klar et al. 2016: alpha = sqrt(2/3) 2 sin(phi) / (3 - sin(phi))
+  double dp_alpha() const {
+    const double sp = std::sin(yield_stress * 3.14159265358979323846 / 180.0);
+    return std::sqrt(2.0 / 3.0) * 2.0 * sp / (3.0 - sp);
+  }
   void validate() const {
     if (youngs <= 0.0) throw std::invalid_argument("Material: E must be > 0");
     if (poisson <= 0.0 || poisson >= 0.5) throw std::invalid_argument("Material: nu must be in (0, 0.5)");
-    if (yield_stress <= 0.0) throw std::invalid_argument("Material: yield stress must be > 0");
+    if (model == Model::HenckyVonMises && yield_stress <= 0.0)
+      throw std::invalid_argument("Material: yield stress must be > 0");
+    if (model == Model::DruckerPrager && !(yield_stress > 0.0 && yield_stress < 90.0))
+      throw std::invalid_argument("Material: friction angle must be in (0, 90) degrees");
     if (density <= 0.0) throw std::invalid_argument("Material: density must be > 0");
   }
 };
@@ -327,6 +342,7 @@ struct Particle {  // mpm.hpp:50-58
   M3 F = M3::Identity();
   M3 C = M3::Zero();
   int material = 0;
+  double jp = 1.0;  // Fluid: volume ratio J; DruckerPrager: accumulated plastic strain q; else unused
 };
 
 enum class BoundaryKind : std::uint8_t { Sticky, Slip };  // mpm.hpp:60
@@ -425,6 +441,73 @@ inline M3 von_mises_return_map(const M3& F_trial, const Material& m) {
   return s.U * M3::diag(sig_proj) * s.V.transpose();
 }
 
+// ---- north_star materials (no reference implementation: parity unpinned) ----
+
+// Fixed-corotated elasticity (Stomakhin et al. 2012): P = 2 mu (F - R) + lambda (J - 1) J F^-T,
+// tau = P F^T = 2 mu (F - R) F^T + lambda (J - 1) J I, R from the polar decomposition.
+inline M3 kirchhoff_fixed_corotated(const M3& F, const Material& m) {
+  const double J = F.determinant();
+  if (!(J > 0.0)) throw std::invalid_argument("kirchhoff_stress: det(F) must be > 0");
+  Svd3 s = svd3(F);
+  M3 R = s.U * s.V.transpose();
+  return 2.0 * m.mu() * ((F - R) * F.transpose()) + M3::Identity() * (m.lambda() * (J - 1.0) * J);
+}
+
+// Drucker-Prager sand (Klar et al. 2016, sec. 7.3.1): Hencky elasticity and a
+// projection of the log strain onto the cone; q accumulates the plastic strain.
+inline M3 drucker_prager_return_map(const M3& F_trial, const Material& m, double& q) {
+  if (!(F_trial.determinant() > 0.0))
+    throw std::invalid_argument("von_mises_return_map: det(F) must be > 0");
+  Svd3 s = svd3(F_trial);
+  V3 eps(std::log(s.s.x), std::log(s.s.y), std::log(s.s.z));
+  const double tr = eps.x + eps.y + eps.z;
+  V3 dev = eps - V3(tr / 3.0, tr / 3.0, tr / 3.0);
+  const double dn = dev.norm();
+  if (dn == 0.0 || tr > 0.0) {  // tension: project to the tip (sigma = 1)
+    q += eps.norm();
+    return s.U * s.V.transpose();
+  }
+  const double dgamma = dn + (3.0 * m.lambda() + 2.0 * m.mu()) / (2.0 * m.mu()) * tr * m.dp_alpha();
+  if (dgamma <= 0.0) return F_trial;
+  q += dgamma;
+  V3 e = eps - dev * (dgamma / dn);
+  return s.U * M3::diag(V3(std::exp(e.x), std::exp(e.y), std::exp(e.z))) * s.V.transpose();
+}
+
+// Weakly compressible fluid (the J-only model of MLS-MPM's mpm88): pressure from
+// the tracked volume ratio, tau = K (J - 1) J I; F carries no shear (kept I).
+inline M3 kirchhoff_fluid(double J, const Material& m) { return M3::Identity() * (m.bulk() * (J - 1.0) * J); }
+
+// Kirchhoff stress of particle p by its material model (P2G, mpm.hpp:235-237).
+inline M3 kirchhoff_of(const Particle& p, const Material& m) {
+  switch (m.model) {
+    case Model::FixedCorotated: return kirchhoff_fixed_corotated(p.F, m);
+    case Model::Fluid: return kirchhoff_fluid(p.jp, m);
+    default: return kirchhoff_stress(p.F, m);  // Hencky (von Mises and Drucker-Prager)
+  }
+}
+
+// F / J update after G2P by material model (mpm.hpp:367-373 for von Mises).
+inline void plasticity_update(Particle& p, const Material& m, double dt) {
+  const M3 f_trial = (M3::Identity() + dt * p.C) * p.F;
+  switch (m.model) {
+    case Model::HenckyVonMises: p.F = von_mises_return_map(f_trial, m); break;
+    case Model::FixedCorotated: p.F = f_trial; break;
+    case Model::DruckerPrager: p.F = drucker_prager_return_map(f_trial, m, p.jp); break;
+    case Model::Fluid: p.jp *= 1.0 + dt * (p.C.m[0][0] + p.C.m[1][1] + p.C.m[2][2]); break;
+  }
+}
+
+// Initial jp of an uploaded particle (and F of a fluid particle: J carries it).
+inline void init_model_state(Particle& p, const Material& m) {
+  if (m.model == Model::Fluid) {
+    p.jp = p.F.determinant();
+    p.F = M3::Identity();
+  } else {
+    p.jp = m.model == Model::DruckerPrager ? 0.0 : 1.0;
+  }
+}
+
 namespace detail {
 // mpm.hpp:188-193
 inline void bspline_weights(double fx, std::array<double, 3>& w) {
@@ -466,7 +549,7 @@ inline void p2g(SoftState& st) {
     }
     sc.base[ip] = base;
     for (int ax = 0; ax < 3; ++ax) detail::bspline_weights(local[ax] - base[ax], sc.w[ip][ax]);
-    M3 tau = kirchhoff_stress(p.F, st.material_of(p));
+    M3 tau = kirchhoff_of(p, st.material_of(p));
     sc.affine[ip] = p.mass * p.C;
     sc.stress[ip] = -(d_inv * p.volume0) * tau;
   });
@@ -590,10 +673,7 @@ inline void g2p_advect(SoftState& st) {
     p.v = v_new;
     p.C = c_new;
     p.x += st.dt * p.v;
-    if (st.dt != 0.0) {
-      M3 f_trial = (M3::Identity() + st.dt * p.C) * p.F;
-      p.F = von_mises_return_map(f_trial, st.material_of(p));
-    }
+    if (st.dt != 0.0) plasticity_update(p, st.material_of(p), st.dt);
     if (!p.x.allFinite() || !p.v.allFinite() || !p.F.allFinite()) bad[ip] = 1;
   });
   for (std::size_t ip = 0; ip < bad.size(); ++ip)

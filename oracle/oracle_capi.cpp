@@ -36,7 +36,7 @@ void put(double* dst, const M3& m) {
 Quat quat(const double* q) { return Quat(q[0], q[1], q[2], q[3]); }
 
 Material material_from(const msim_material& m) {
-  return Material{m.density, m.youngs, m.poisson, m.yield_stress};
+  return Material{m.density, m.youngs, m.poisson, m.yield_stress, static_cast<Model>(m.model)};
 }
 
 Shape shape_from(const msim_shape& s) {
@@ -132,7 +132,16 @@ int oracle_set_particles(oracle_world* w, int64_t n, const double* x, const doub
     p.mass = mass[i];
     p.volume0 = vol0[i];
     p.material = mat ? mat[i] : 0;
+    if (p.material >= 0 && p.material < (int)w->w.soft.materials.size())
+      init_model_state(p, w->w.soft.materials[p.material]);
   }
+  return MSIM_OK;
+}
+
+// plastic / volume scalar per particle (Fluid: J, DruckerPrager: q, else 1)
+int oracle_read_jp(oracle_world* w, double* jp) {
+  const auto& ps = w->w.soft.particles;
+  for (size_t i = 0; i < ps.size(); ++i) jp[i] = ps[i].jp;
   return MSIM_OK;
 }
 
