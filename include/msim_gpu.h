@@ -216,6 +216,9 @@ int msim_gpu_env_step(msim_gpu_ctx* ctx, int n_rigid, int n_soft, msim_step_repo
 int64_t msim_gpu_particle_count(const msim_gpu_ctx* ctx, int env);
 int msim_gpu_read_particles(msim_gpu_ctx* ctx, int env, double* x, double* v, double* F,
                             double* C, uint8_t* lost);
+/* The per-particle model scalar of env `env` (upload order): the fluid's
+ * volume ratio J, Drucker-Prager's accumulated plastic strain, 1 otherwise. */
+int msim_gpu_read_jp(msim_gpu_ctx* ctx, int env, double* jp);
 /* Dense per-env grid channels (node_count doubles / node_count*3). velocity
  * is written by grid_update; mass/momentum/force by p2g (+ grid hook). Any
  * pointer may be NULL. Momentum/force are only kept separately in "split"

@@ -350,9 +350,17 @@ int oracle_constitutive(const msim_material* mat, int64_t n, const double* F, do
   try {
     Material m = material_from(*mat);
     for (int64_t i = 0; i < n; ++i) {
-      M3 f = m3(F + 9 * i);
-      if (tau) put(tau + 9 * i, kirchhoff_stress(f, m));
-      if (Fp) put(Fp + 9 * i, von_mises_return_map(f, m));
+      Particle p;
+      p.F = m3(F + 9 * i);
+      if (!(p.F.determinant() > 0.0)) throw std::invalid_argument("kirchhoff_stress: det(F) must be > 0");
+      init_model_state(p, m);
+      if (tau) put(tau + 9 * i, kirchhoff_of(p, m));
+      if (Fp) {
+        M3 fp = p.F;
+        if (m.model == Model::HenckyVonMises) fp = von_mises_return_map(p.F, m);
+        else if (m.model == Model::DruckerPrager) fp = drucker_prager_return_map(p.F, m, p.jp);
+        put(Fp + 9 * i, fp);
+      }
     }
   } catch (const std::invalid_argument&) {
     return MSIM_ERR_INVALID;

@@ -73,6 +73,7 @@ _SIGS = {
     "oracle_seed_box": (C.c_int64, [_vp, _vp, _dp, _dp, C.c_int, C.c_double]),
     "oracle_lattice_count": (C.c_int64, [_dp, _dp, C.c_double]),
     "oracle_time_env_steps": (C.c_double, [_vp, C.c_int, _ip]),
+    "oracle_read_jp": (C.c_int, [_vp, _dp]),
     "oracle_bake_grid": (C.c_int, [_dp, C.c_int64, C.c_double, C.c_double, _dp, _ip]),
     "oracle_bake_mesh_sdf": (C.c_int, [_dp, C.c_int64, C.c_double, C.c_double, C.POINTER(C.c_float), C.c_int64]),
     "oracle_make_box_mesh": (None, [_dp, _dp, _dp]),
@@ -250,6 +251,11 @@ class OracleWorld:
         self.lib.oracle_read_bodies(self.h, B, nb)
         return [B[i] for i in range(nb)]
 
+    def jp(self):
+        out = np.zeros(self.env.n)
+        self.lib.oracle_read_jp(self.h, out.ctypes.data_as(_dp))
+        return out
+
     def lost_count(self):
         return int(self.lib.oracle_lost_count(self.h))
 
@@ -278,7 +284,8 @@ class OracleWorld:
 def constitutive(F: np.ndarray, mat=(1000.0, 1e4, 0.3, 2e3)):
     lib = load()
     m = abi.Material()
-    m.density, m.youngs, m.poisson, m.yield_stress = mat
+    m.density, m.youngs, m.poisson, m.yield_stress = mat[:4]
+    m.model = mat[4] if len(mat) > 4 else 0
     F = np.ascontiguousarray(np.asarray(F, np.float64).reshape(-1, 3, 3))
     tau, Fp = np.zeros_like(F), np.zeros_like(F)
     rc = lib.oracle_constitutive(C.byref(m), F.shape[0], F.ctypes.data_as(_dp), tau.ctypes.data_as(_dp),

@@ -25,6 +25,8 @@ COUPLING_PARTICLE = 0
 COUPLING_GRID = 1
 SHAPE_PLANE, SHAPE_SPHERE, SHAPE_BOX, SHAPE_CAPSULE, SHAPE_VOLUME = range(5)
 BODY_DYNAMIC, BODY_KINEMATIC, BODY_SCRIPTED = range(3)
+# material models (MSIM_MODEL_*)
+MODEL_HENCKY_VON_MISES, MODEL_FIXED_COROTATED, MODEL_DRUCKER_PRAGER, MODEL_FLUID = range(4)
 
 
 class SoftDesc(C.Structure):
@@ -133,7 +135,7 @@ EXPORTED = [
     "msim_seed_box_count", "msim_seed_box",
     "msim_gpu_metric_fill", "msim_gpu_render_heightmap", "msim_gpu_metric_write_iou", "msim_gpu_chamfer",
     "msim_gpu_metric_pinch", "msim_bake_grid", "msim_gpu_bake_mesh_sdf", "msim_make_box_mesh",
-    "msim_gpu_seed_envs", "msim_gpu_set_bucket_factor",
+    "msim_gpu_seed_envs", "msim_gpu_set_bucket_factor", "msim_gpu_read_jp",
 ]
 
 _dp = C.POINTER(C.c_double)
@@ -197,6 +199,7 @@ _SIGS = {
     "msim_gpu_bake_mesh_sdf": (C.c_int, [C.c_int, _dp, C.c_int64, C.c_double, C.c_double, C.POINTER(C.c_float), C.c_int64]),
     "msim_make_box_mesh": (None, [_dp, _dp, _dp]),
     "msim_gpu_set_bucket_factor": (C.c_int, [_vp, C.c_int]),
+    "msim_gpu_read_jp": (C.c_int, [_vp, C.c_int, _dp]),
     "msim_gpu_seed_envs": (C.c_int, [_vp, C.c_int, _ip, C.POINTER(C.c_uint64), _dp, C.c_int32, C.c_double]),
 }
 

@@ -150,11 +150,17 @@ bool split_mode(const msim_gpu_ctx* c) {
 MatParams mat_params(const msim_material& m) {
   double mu = m.youngs / (2.0 * (1.0 + m.poisson));
   double lambda = m.youngs * m.poisson / ((1.0 + m.poisson) * (1.0 - 2.0 * m.poisson));
-  MatParams p;
+  MatParams p{};
   p.two_mu = (float)(2.0 * mu);
   p.lambda = (float)lambda;
   p.yield_thr = (float)(std::sqrt(2.0 / 3.0) * m.yield_stress);
   p.density = (float)m.density;
+  p.model = m.model;
+  const double sp = std::sin(m.yield_stress * 3.14159265358979323846 / 180.0);  // Drucker-Prager: angle
+  const double alpha = std::sqrt(2.0 / 3.0) * 2.0 * sp / (3.0 - sp);
+  p.dp_alpha = (float)alpha;
+  p.dp_k = (float)((3.0 * lambda + 2.0 * mu) / (2.0 * mu) * alpha);
+  p.bulk = (float)(m.youngs / (3.0 * (1.0 - 2.0 * m.poisson)));
   return p;
 }
 
@@ -190,6 +196,8 @@ SimParams params(msim_gpu_ctx* c) {
   }
   P.buckets_per_env = c->buckets_per_env;
   P.n_blocks = c->n_env * c->blocks_per_env;
+  P.any_model = 0;
+  for (const auto& m : c->mats_h) P.any_model |= m.model != MSIM_MODEL_HENCKY_VON_MISES;
   P.split = split_mode(c) ? 1 : 0;
   P.grid_mode = c->coupling.mode == MSIM_COUPLING_GRID;
   P.r_c_particle = (float)(c->coupling.r_c_factor * d.h);
@@ -275,8 +283,8 @@ int fail(msim_gpu_ctx* c, int code, const std::string& msg) {
 }
 
 void carve_particles(msim_gpu_ctx* c, int b, long long n) {
-  // 24 float fields: x3 v3 C9 G9 + mass + vol0 = 26
-  const size_t nf = 26;
+  // float fields: x3 v3 C9 G9 + mass + vol0 + jp = 27
+  const size_t nf = 27;
   CK(c->pool_f[b].ensure(sizeof(float) * nf * (size_t)std::max<long long>(n, 1)));
   CK(c->meta_b[b].ensure(sizeof(uint32_t) * (size_t)std::max<long long>(n, 1)));
   CK(c->pid_b[b].ensure(sizeof(int32_t) * (size_t)std::max<long long>(n, 1)));
@@ -290,6 +298,7 @@ void carve_particles(msim_gpu_ctx* c, int b, long long n) {
   for (int a = 0; a < 9; ++a) q.G[a] = f + stride * k++;
   q.mass = f + stride * k++;
   q.vol0 = f + stride * k++;
+  q.jp = f + stride * k++;
   q.meta = c->meta_b[b].as<uint32_t>();
   q.pid = c->pid_b[b].as<int32_t>();
 }
@@ -585,9 +594,13 @@ int step_call(msim_gpu_ctx* c, int n_sub, bool integrate_rigid, int n_soft, int3
 bool valid_material(const msim_material& m, std::string& why) {
   if (m.youngs <= 0.0) { why = "Material: E must be > 0"; return false; }
   if (m.poisson <= 0.0 || m.poisson >= 0.5) { why = "Material: nu must be in (0, 0.5)"; return false; }
-  if (m.yield_stress <= 0.0) { why = "Material: yield stress must be > 0"; return false; }
+  if (m.model == MSIM_MODEL_HENCKY_VON_MISES && m.yield_stress <= 0.0) { why = "Material: yield stress must be > 0"; return false; }
+  if (m.model == MSIM_MODEL_DRUCKER_PRAGER && !(m.yield_stress > 0.0 && m.yield_stress < 90.0)) {
+    why = "Material: friction angle must be in (0, 90) degrees";
+    return false;
+  }
   if (m.density <= 0.0) { why = "Material: density must be > 0"; return false; }
-  if (m.model != MSIM_MODEL_HENCKY_VON_MISES) { why = "Material: unknown constitutive model"; return false; }
+  if (m.model < MSIM_MODEL_HENCKY_VON_MISES || m.model > MSIM_MODEL_FLUID) { why = "Material: unknown constitutive model"; return false; }
   return true;
 }
 
@@ -1065,6 +1078,28 @@ int msim_gpu_read_particles(msim_gpu_ctx* c, int env, double* x, double* v, doub
     if (F) CK(cudaMemcpyAsync(F, dF, sizeof(double) * 9 * ne, cudaMemcpyDeviceToHost, s));
     if (C) CK(cudaMemcpyAsync(C, dC, sizeof(double) * 9 * ne, cudaMemcpyDeviceToHost, s));
     if (lost) CK(cudaMemcpyAsync(lost, dl, ne, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    return MSIM_OK;
+  });
+}
+
+int msim_gpu_read_jp(msim_gpu_ctx* c, int env, double* jp) {
+  return guarded(c, [&]() -> int {
+    if (env < 0 || env >= c->n_env) return fail(c, MSIM_ERR_INVALID, "read_jp: env out of range");
+    if (!jp) return fail(c, MSIM_ERR_INVALID, "read_jp: null output");
+    set_device(c);
+    cudaStream_t s = c->stream;
+    long long first = c->env_off_h[env], ne = c->env_off_h[env + 1] - first;
+    if (ne == 0) return MSIM_OK;
+    if (!params(c).any_model) {  // von Mises only: the particle kernel does not carry jp (always 1)
+      std::fill(jp, jp + ne, 1.0);
+      return MSIM_OK;
+    }
+    DevBuf st;
+    CK(st.ensure(sizeof(double) * ne));
+    launch_jp_out(params(c), first, ne, st.as<double>(), s);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(jp, st.p, sizeof(double) * ne, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
     return MSIM_OK;
   });

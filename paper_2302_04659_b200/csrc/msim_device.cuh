@@ -105,11 +105,18 @@ __device__ __forceinline__ void sym_eigen3(float a00, float a11, float a22, floa
 // ---------------------------------------------------------------------------
 // Constitutive model on the displacement gradient G = F - I (stored state).
 
+// model ids = MSIM_MODEL_* (include/msim_gpu.h)
+constexpr int kModelVonMises = 0, kModelFixedCorotated = 1, kModelDruckerPrager = 2, kModelFluid = 3;
+
 struct MatParams {
   float two_mu;       // 2 mu
   float lambda;
-  float yield_thr;    // sqrt(2/3) * yield_stress
+  float yield_thr;    // sqrt(2/3) * yield_stress (von Mises)
   float density;
+  int model;
+  float dp_alpha;     // Drucker-Prager cone: sqrt(2/3) 2 sin(phi) / (3 - sin(phi))
+  float dp_k;         // (3 lambda + 2 mu) / (2 mu) * dp_alpha
+  float bulk;         // fluid bulk modulus E / (3 (1 - 2 nu))
 };
 
 // det(I + G) without forming I + G (exact expansion).
@@ -300,6 +307,104 @@ __device__ __forceinline__ bool von_mises_project_strain(float* G, Sym& eps, con
 #pragma unroll
   for (int i = 0; i < 9; ++i) G[i] = Gn[i];
   return true;
+}
+
+// G' = G + X + X G (F' = (I + X) F) for a symmetric X
+__device__ __forceinline__ void left_update(float* G, const Sym& X) {
+  const float Xm[9] = {X.a00, X.a01, X.a02, X.a01, X.a11, X.a12, X.a02, X.a12, X.a22};
+  float Gn[9];
+#pragma unroll
+  for (int r = 0; r < 3; ++r)
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+      Gn[r * 3 + c] = G[r * 3 + c] + Xm[r * 3 + c] + Xm[r * 3 + 0] * G[0 * 3 + c] + Xm[r * 3 + 1] * G[1 * 3 + c] +
+                      Xm[r * 3 + 2] * G[2 * 3 + c];
+#pragma unroll
+  for (int i = 0; i < 9; ++i) G[i] = Gn[i];
+}
+
+// ---- the north_star's other materials (oracle: msim_oracle.hpp) ----
+
+// Drucker-Prager sand (Klar et al. 2016) on the Hencky strain tensor: tension
+// (or a purely volumetric strain) projects to the cone tip (eps = 0, F = R),
+// otherwise dgamma = |dev eps| + (3 lambda + 2 mu)/(2 mu) tr(eps) alpha > 0
+// moves eps by -dgamma dev / |dev| (F' = exp(d eps) F as in the von Mises map);
+// q accumulates the plastic strain.
+__device__ __forceinline__ void drucker_prager_project_strain(float* G, Sym& eps, float& q, const MatParams& m) {
+  const float tr = eps.a00 + eps.a11 + eps.a22;
+  const float mean = tr * (1.0f / 3.0f);
+  const Sym dev = {eps.a00 - mean, eps.a11 - mean, eps.a22 - mean, eps.a01, eps.a02, eps.a12};
+  const float dn = sqrtf(sym_norm2(dev));
+  Sym M;
+  if (dn == 0.0f || tr > 0.0f) {
+    q += sqrtf(sym_norm2(eps));
+    M = sym_scale_add_id(eps, -1.0f, 0.0f);
+  } else {
+    const float dgamma = dn + m.dp_k * tr;
+    if (dgamma <= 0.0f) return;
+    q += dgamma;
+    M = sym_scale_add_id(dev, -dgamma / dn, 0.0f);
+  }
+  eps = {eps.a00 + M.a00, eps.a11 + M.a11, eps.a22 + M.a22, eps.a01 + M.a01, eps.a02 + M.a02, eps.a12 + M.a12};
+  left_update(G, sym_expm1(M));
+}
+
+// sqrt(I + E) - I = V - I (V = sqrt(F F^T), the left stretch) as a matrix
+// function of E = F F^T - I: with Z = E (2I + E)^-1, I + E = (I + Z)(I - Z)^-1,
+// so sqrt(I + E) = (I + Z)(I - Z^2)^-1/2 and
+//   V - I = Z r + (r - I),  r = (I - Z^2)^-1/2 = sum_k C(2k, k) / 4^k Z^2k,
+// summed to Z^12 (truncation < 1e-8 for |Z|_F <= 1/4); larger strains take the
+// Jacobi frame, where sigma - 1 = e / (1 + sqrt(1 + e)).
+__device__ __forceinline__ Sym left_stretch_m1(const float* G) {
+  const Sym E = left_strain(G);
+  const Sym B = {2.0f + E.a00, 2.0f + E.a11, 2.0f + E.a22, E.a01, E.a02, E.a12};
+  const Sym Cf = {B.a11 * B.a22 - B.a12 * B.a12, B.a00 * B.a22 - B.a02 * B.a02, B.a00 * B.a11 - B.a01 * B.a01,
+                  B.a02 * B.a12 - B.a01 * B.a22, B.a01 * B.a12 - B.a02 * B.a11, B.a01 * B.a02 - B.a00 * B.a12};
+  const float inv_det = 1.0f / (B.a00 * Cf.a00 + B.a01 * Cf.a01 + B.a02 * Cf.a02);
+  const Sym Z = sym_scale_add_id(sym_mul(E, Cf), inv_det, 0.0f);
+  if (sym_norm2(Z) <= 0.0625f) {
+    const Sym W = sym_mul(Z, Z);
+    Sym r = sym_scale_add_id(W, 231.0f / 1024.0f, 63.0f / 256.0f);
+    r = sym_mul_add_id(W, r, 35.0f / 128.0f);
+    r = sym_mul_add_id(W, r, 5.0f / 16.0f);
+    r = sym_mul_add_id(W, r, 3.0f / 8.0f);
+    r = sym_mul_add_id(W, r, 0.5f);
+    const Sym rm1 = sym_mul(W, r);  // r - I
+    const Sym zr = sym_mul(Z, sym_scale_add_id(rm1, 1.0f, 1.0f));
+    return {zr.a00 + rm1.a00, zr.a11 + rm1.a11, zr.a22 + rm1.a22, zr.a01 + rm1.a01, zr.a02 + rm1.a02,
+            zr.a12 + rm1.a12};
+  }
+  float U[9], d[3], S[9];
+  sym_eigen3(E.a00, E.a11, E.a22, E.a01, E.a02, E.a12, d, U);
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    const float e = fmaxf(d[i], -0.99999994f);
+    d[i] = e / (1.0f + sqrtf(1.0f + e));
+  }
+  sym_from_frame(U, d, S);
+  return {S[0], S[4], S[8], S[1], S[2], S[5]};
+}
+
+// Kirchhoff stress (as a symmetric tensor) of the stored state for P2G
+// (mpm.hpp:235-237), by model: Hencky for von Mises and Drucker-Prager (from
+// eps), fixed corotated 2 mu (E - (V - I)) + lambda (J - 1) J I (2 mu (F - R) F^T
+// = 2 mu (F F^T - V)), fluid K (J - 1) J I with J = jp.
+__device__ __forceinline__ Sym stress_of(int model, const float* G, const Sym& eps, float jp, const MatParams& m) {
+  if (model == kModelFixedCorotated) {
+    const Sym E = left_strain(G);
+    const Sym S = left_stretch_m1(G);
+    const float J = det_I_plus(G);
+    const float p = m.lambda * (J - 1.0f) * J;
+    return {m.two_mu * (E.a00 - S.a00) + p, m.two_mu * (E.a11 - S.a11) + p, m.two_mu * (E.a22 - S.a22) + p,
+            m.two_mu * (E.a01 - S.a01), m.two_mu * (E.a02 - S.a02), m.two_mu * (E.a12 - S.a12)};
+  }
+  if (model == kModelFluid) {
+    const float p = m.bulk * (jp - 1.0f) * jp;
+    return {p, p, p, 0.f, 0.f, 0.f};
+  }
+  const float lt = m.lambda * (eps.a00 + eps.a11 + eps.a22);
+  return {m.two_mu * eps.a00 + lt, m.two_mu * eps.a11 + lt, m.two_mu * eps.a22 + lt, m.two_mu * eps.a01,
+          m.two_mu * eps.a02, m.two_mu * eps.a12};
 }
 
 // ---------------------------------------------------------------------------

@@ -68,6 +68,7 @@ struct Particles {
   float* G[9];  // displacement gradient F - I
   float* mass;
   float* vol0;
+  float* jp;     // Fluid: volume ratio J; Drucker-Prager: accumulated plastic strain; else 1
   uint32_t* meta;
   int32_t* pid;  // original (upload-order) index within the context
 };
@@ -183,6 +184,7 @@ struct SimParams {
   int qdims[3];
   int buckets_per_env;
   int n_blocks;              // n_env*blocks_per_env (node-block flags)
+  int any_model;             // some material is not the reference's von Mises clay (jp + dispatch)
   int split;                 // keep momentum and force separately
   int grid_mode;             // coupling mode grid
   float r_c_particle, r_c_grid, c_d;
@@ -259,6 +261,7 @@ void launch_overwrite(const SimParams& P, long long first_pid, long long n, cons
 void launch_convert_out(const SimParams& P, long long first_pid, long long n, double* x, double* v,
                         double* F, double* C, uint8_t* lost, cudaStream_t s);
 void launch_vmax(const SimParams& P, cudaStream_t s);
+void launch_jp_out(const SimParams& P, long long first_pid, long long n, double* jp, cudaStream_t s);
 void launch_rigid(const SimParams& P, int integrate, int only_env, cudaStream_t s);
 void launch_stage_wrenches(const SimParams& P, int n_bodies, cudaStream_t s);
 void launch_constitutive(const msim_dev::MatParams m, long long n, const double* F, double* tau,

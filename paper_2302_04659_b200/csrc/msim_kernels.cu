@@ -169,6 +169,20 @@ __global__ void k_convert_in(SimParams P, long long n, const double* x, const do
   unsigned m = mat ? (unsigned)mat[j] : 0u;
   q.meta[i] = ((unsigned)env_of[j] << 8) | (m & 0xFFu);
   q.pid[i] = (int)i;
+  // per-model scalar (the oracle's init_model_state): fluid carries det F in J and no shear
+  const int model = P.mats[m].model;
+  if (model == msim_dev::kModelFluid) {
+    double Fd[9];
+#pragma unroll
+    for (int k = 0; k < 9; ++k) Fd[k] = F ? F[9 * j + k] : ((k % 4 == 0) ? 1.0 : 0.0);
+    const double J = Fd[0] * (Fd[4] * Fd[8] - Fd[5] * Fd[7]) - Fd[1] * (Fd[3] * Fd[8] - Fd[5] * Fd[6]) +
+                     Fd[2] * (Fd[3] * Fd[7] - Fd[4] * Fd[6]);
+    q.jp[i] = (float)J;
+#pragma unroll
+    for (int k = 0; k < 9; ++k) q.G[k][i] = 0.0f;
+  } else {
+    q.jp[i] = model == msim_dev::kModelDruckerPrager ? 0.0f : 1.0f;
+  }
 }
 
 __global__ void k_overwrite(SimParams P, long long first_pid, long long n,
@@ -188,6 +202,21 @@ __global__ void k_overwrite(SimParams P, long long first_pid, long long n,
     if (C) q.C[k][i] = (float)C[9 * j + k];
     if (F) q.G[k][i] = (float)(F[9 * j + k] - ((k % 4 == 0) ? 1.0 : 0.0));
   }
+  if (F && P.mats[q.meta[i] & 0xFFu].model == msim_dev::kModelFluid) {  // as at upload: J = det F, no shear
+    const double* f = F + 9 * j;
+    q.jp[i] = (float)(f[0] * (f[4] * f[8] - f[5] * f[7]) - f[1] * (f[3] * f[8] - f[5] * f[6]) +
+                      f[2] * (f[3] * f[7] - f[4] * f[6]));
+#pragma unroll
+    for (int k = 0; k < 9; ++k) q.G[k][i] = 0.0f;
+  }
+}
+
+__global__ void k_jp_out(SimParams P, long long first_pid, long long n, double* jp) {
+  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= P.n) return;
+  long long j = (long long)P.cur.pid[i] - first_pid;
+  if (j < 0 || j >= n) return;
+  jp[j] = P.cur.jp[i];
 }
 
 __global__ void k_convert_out(SimParams P, long long first_pid, long long n, double* x, double* v,
@@ -246,14 +275,21 @@ __global__ void k_constitutive(MatParams m, long long n, const double* F, double
     atomicOr(bad, 1);
     return;
   }
-  Sym eps = hencky_strain(G);
+  float jp = m.model == msim_dev::kModelDruckerPrager ? 0.0f : 1.0f;
+  if (m.model == msim_dev::kModelFluid) {  // J carries the volume, F no shear
+    jp = det_I_plus(G);
+    for (int k = 0; k < 9; ++k) G[k] = 0.0f;
+  }
+  Sym eps = (m.model == msim_dev::kModelVonMises || m.model == msim_dev::kModelDruckerPrager)
+                ? hencky_strain(G) : Sym{0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
   if (tau) {
-    float t[9];
-    kirchhoff_from_strain(eps, m, t);
-    for (int k = 0; k < 9; ++k) tau[9 * i + k] = t[k];
+    const Sym t = stress_of(m.model, G, eps, jp, m);
+    const float tm[9] = {t.a00, t.a01, t.a02, t.a01, t.a11, t.a12, t.a02, t.a12, t.a22};
+    for (int k = 0; k < 9; ++k) tau[9 * i + k] = tm[k];
   }
   if (Fp) {
-    von_mises_project_strain(G, eps, m);
+    if (m.model == msim_dev::kModelVonMises) von_mises_project_strain(G, eps, m);
+    else if (m.model == msim_dev::kModelDruckerPrager) drucker_prager_project_strain(G, eps, jp, m);
     for (int k = 0; k < 9; ++k) Fp[9 * i + k] = (double)G[k] + ((k % 4 == 0) ? 1.0 : 0.0);
   }
 }
@@ -373,6 +409,9 @@ void launch_convert_in(const SimParams& P, long long n, const double* x, const d
 void launch_overwrite(const SimParams& P, long long first_pid, long long n, const double* x,
                       const double* v, const double* F, const double* C, cudaStream_t s) {
   if (P.n > 0) k_overwrite<<<nblk(P.n), 256, 0, s>>>(P, first_pid, n, x, v, F, C);
+}
+void launch_jp_out(const SimParams& P, long long first_pid, long long n, double* jp, cudaStream_t s) {
+  if (P.n > 0) k_jp_out<<<nblk(P.n), 256, 0, s>>>(P, first_pid, n, jp);
 }
 void launch_convert_out(const SimParams& P, long long first_pid, long long n, double* x, double* v,
                         double* F, double* C, uint8_t* lost, cudaStream_t s) {

@@ -198,7 +198,7 @@ __device__ MSIM_COLD void scatter_global(const SimParams& P, int env, const int*
 
 // The rounds of one bucket (<= kCap particles each): per-particle phase, then
 // the fixed-point scatter and flush. Bucket-uniform values come from S.ic.
-template <int NCH, int F>
+template <int NCH, int F, bool AM>
 __device__ __forceinline__ void item_rounds(const SimParams& P, Smem<NCH, F>& S, bool redo) {
   MSIM_GEO_ALIASES(F)
   const int tid = threadIdx.x, lane = tid & 31;
@@ -223,7 +223,7 @@ __device__ __forceinline__ void item_rounds(const SimParams& P, Smem<NCH, F>& S,
         const int pact = IC.lostb ? (valid ? P.run[penv].action : kActIdle) : IC.act;
         f3 x = {0.f, 0.f, 0.f}, v = {0.f, 0.f, 0.f};
         float G[9], Cm[9];
-        float m = 0.f, V0 = 0.f;
+        float m = 0.f, V0 = 0.f, jp = 1.f;
         int pid = 0;
         if (valid) {
           x = {lds(&P.cur.x[0][i]), lds(&P.cur.x[1][i]), lds(&P.cur.x[2][i])};
@@ -231,6 +231,7 @@ __device__ __forceinline__ void item_rounds(const SimParams& P, Smem<NCH, F>& S,
           for (int k = 0; k < 9; ++k) G[k] = lds(&P.cur.G[k][i]);
           m = lds(&P.cur.mass[i]);
           V0 = lds(&P.cur.vol0[i]);
+          if (AM) jp = lds(&P.cur.jp[i]);
           pid = lds(&P.cur.pid[i]);
         } else {
 #pragma unroll
@@ -248,8 +249,17 @@ __device__ __forceinline__ void item_rounds(const SimParams& P, Smem<NCH, F>& S,
         bool write_vc = valid && (IC.lostb || IC.act != kActFused);
         const bool live = valid && !IC.lostb && !was_lost && IC.act != kActIdle;
         float speed = -1.0f;
-        Sym eps = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};  // Hencky strain tensor (one evaluation per substep)
-        const MatParams mp = P.mats[meta & 0xFFu];
+        // Kirchhoff stress of the updated state for the next P2G (one strain evaluation per substep)
+        Sym ts = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+        // AM = false (every material of the context is the reference's von Mises
+        // clay): the model dispatch and the jp field compile away (7 % of the kernel)
+        MatParams mp = P.mats[meta & 0xFFu];
+        if (!AM) mp.model = kModelVonMises;
+        // Hencky strain for the models that use it (von Mises, Drucker-Prager)
+        auto hencky_of = [&](const float* g) -> Sym {
+          return (mp.model == kModelVonMises || mp.model == kModelDruckerPrager) ? hencky_strain(g)
+                                                                                 : Sym{0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+        };
 
         // ---------------- G2P of this cycle (mpm.hpp:346-379)
         if (live && IC.do_g2p) {
@@ -288,7 +298,11 @@ __device__ __forceinline__ void item_rounds(const SimParams& P, Smem<NCH, F>& S,
           Cm[6] = k4h * (Sx.z - vs.z * fx[0]); Cm[7] = k4h * (Sy.z - vs.z * fx[1]); Cm[8] = k4h * (Sz.z - vs.z * fx[2]);
           v = vs;
           x = x + IC.dt * vs;
-          if (IC.dt != 0.0f) {
+          if (IC.dt != 0.0f && mp.model == kModelFluid) {  // J-only: J *= 1 + dt tr(C)
+            jp *= 1.0f + IC.dt * (Cm[0] + Cm[4] + Cm[8]);
+            if (!(jp > 0.0f)) set_error(P, penv, kErrDetReturn, pid);
+            ts = stress_of(kModelFluid, G, ts, jp, mp);
+          } else if (IC.dt != 0.0f) {  // F <- (I + dt C) F, then the model's return map (mpm.hpp:367-373)
             float Gn[9];
 #pragma unroll
             for (int r = 0; r < 3; ++r)
@@ -297,12 +311,14 @@ __device__ __forceinline__ void item_rounds(const SimParams& P, Smem<NCH, F>& S,
                 Gn[r * 3 + c] = G[r * 3 + c] + IC.dt * (Cm[r * 3 + c] + Cm[r * 3 + 0] * G[0 * 3 + c] +
                                                      Cm[r * 3 + 1] * G[1 * 3 + c] + Cm[r * 3 + 2] * G[2 * 3 + c]);
             if (!(det_I_plus(Gn) > 0.0f)) set_error(P, penv, kErrDetReturn, pid);
-            eps = hencky_strain(Gn);
-            von_mises_project_strain(Gn, eps, mp);
+            Sym eps = hencky_of(Gn);
+            if (mp.model == kModelVonMises) von_mises_project_strain(Gn, eps, mp);
+            else if (mp.model == kModelDruckerPrager) drucker_prager_project_strain(Gn, eps, jp, mp);
 #pragma unroll
             for (int k = 0; k < 9; ++k) G[k] = Gn[k];
+            ts = stress_of(mp.model, G, eps, jp, mp);
           } else if (IC.do_p2g) {
-            eps = hencky_strain(G);
+            ts = stress_of(mp.model, G, hencky_of(G), jp, mp);
           }
           bool bad = false;
 #pragma unroll
@@ -314,7 +330,7 @@ __device__ __forceinline__ void item_rounds(const SimParams& P, Smem<NCH, F>& S,
           if (!(speed >= 0.0f)) speed = FLT_MAX;
         } else if (live && IC.do_p2g) {
           if (!(det_I_plus(G) > 0.0f)) set_error(P, penv, kErrDetStress, pid);
-          eps = hencky_strain(G);
+          ts = stress_of(mp.model, G, hencky_of(G), jp, mp);
         }
 
         if (!redo && valid) {  // G is final here: store it now so it does not live on in registers
@@ -322,6 +338,7 @@ __device__ __forceinline__ void item_rounds(const SimParams& P, Smem<NCH, F>& S,
           for (int k = 0; k < 9; ++k) sts(&P.nxt.G[k][j], G[k]);
           sts(&P.nxt.mass[j], m);
           sts(&P.nxt.vol0[j], V0);
+          if (AM) sts(&P.nxt.jp[j], jp);
           sts(&P.nxt.pid[j], pid);
         }
 
@@ -396,8 +413,7 @@ __device__ __forceinline__ void item_rounds(const SimParams& P, Smem<NCH, F>& S,
         }
 
         if (scatter_me) {
-          float tau[9];
-          kirchhoff_from_strain(eps, mp, tau);
+          const float tau[9] = {ts.a00, ts.a01, ts.a02, ts.a01, ts.a11, ts.a12, ts.a02, ts.a12, ts.a22};
           const float h = P.h_f;
           const float hm = h * m;
           const float hs = -h * P.d_inv_f * V0;  // h * (-(4/h^2) V0): stress -> force matrix
@@ -631,7 +647,7 @@ __device__ __forceinline__ void item_rounds(const SimParams& P, Smem<NCH, F>& S,
   }
 }
 
-template <int NCH, int F>
+template <int NCH, int F, bool AM>
 __global__ void __launch_bounds__(kT, kCtasPerSm) k_particles(SimParams P) {
   MSIM_GEO_ALIASES(F)
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -697,7 +713,7 @@ __global__ void __launch_bounds__(kT, kCtasPerSm) k_particles(SimParams P) {
       IC.lostb = lostb; IC.do_g2p = do_g2p; IC.do_p2g = do_p2g; IC.penalty = penalty;
     }
     __syncthreads();
-    item_rounds<NCH, F>(P, S, redo);
+    item_rounds<NCH, F, AM>(P, S, redo);
   }
 }
 
@@ -1022,33 +1038,40 @@ struct Timed {
 };
 
 // persistent grid: as many CTAs as fit on the device at once (occupancy query)
-template <int NCH, int F>
+template <int NCH, int F, bool AM>
 void launch_k_particles(const SimParams& P, cudaStream_t s) {
   static int per_sm = 0;
   if (!per_sm) {
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_particles<NCH, F>, kT, sizeof(Smem<NCH, F>));
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_particles<NCH, F, AM>, kT, sizeof(Smem<NCH, F>));
     if (per_sm <= 0) per_sm = 1;
   }
-  k_particles<NCH, F><<<sm_count() * per_sm, kT, sizeof(Smem<NCH, F>), s>>>(P);
+  k_particles<NCH, F, AM><<<sm_count() * per_sm, kT, sizeof(Smem<NCH, F>), s>>>(P);
+}
+
+template <bool AM>
+void particle_kernel_m(const SimParams& P, cudaStream_t s) {
+  if (P.qf == 2) {
+    if (P.split) launch_k_particles<7, 2, AM>(P, s);
+    else launch_k_particles<4, 2, AM>(P, s);
+  } else {
+    if (P.split) launch_k_particles<7, 1, AM>(P, s);
+    else launch_k_particles<4, 1, AM>(P, s);
+  }
 }
 
 void particle_kernel(const SimParams& P, cudaStream_t s) {
-  if (P.qf == 2) {
-    if (P.split) launch_k_particles<7, 2>(P, s);
-    else launch_k_particles<4, 2>(P, s);
-  } else {
-    if (P.split) launch_k_particles<7, 1>(P, s);
-    else launch_k_particles<4, 1>(P, s);
-  }
+  if (P.any_model) particle_kernel_m<true>(P, s);
+  else particle_kernel_m<false>(P, s);
 }
 
 }  // namespace
 
 void configure_kernels() {
-  cudaFuncSetAttribute(k_particles<4, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(Smem<4, 1>));
-  cudaFuncSetAttribute(k_particles<7, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(Smem<7, 1>));
-  cudaFuncSetAttribute(k_particles<4, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(Smem<4, 2>));
-  cudaFuncSetAttribute(k_particles<7, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(Smem<7, 2>));
+#define MSIM_SET_SMEM(NCH, F, AM) \
+  cudaFuncSetAttribute(k_particles<NCH, F, AM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(Smem<NCH, F>))
+  MSIM_SET_SMEM(4, 1, false); MSIM_SET_SMEM(7, 1, false); MSIM_SET_SMEM(4, 2, false); MSIM_SET_SMEM(7, 2, false);
+  MSIM_SET_SMEM(4, 1, true); MSIM_SET_SMEM(7, 1, true); MSIM_SET_SMEM(4, 2, true); MSIM_SET_SMEM(7, 2, true);
+#undef MSIM_SET_SMEM
 }
 
 void launch_rebin(const SimParams& P, cudaStream_t s) {

@@ -378,6 +378,7 @@ __global__ void k_seed_apply(SimParams P, const unsigned char* env_reset, const 
   q.mass[i] = mass;
   q.vol0[i] = vol0;
   q.meta[i] = (env << 8) | (material & 0xFFu);  // lost flag cleared
+  q.jp[i] = P.mats[material].model == msim_dev::kModelDruckerPrager ? 0.0f : 1.0f;  // fresh: J = 1, q = 0
 }
 
 inline unsigned nblk(long long n, int t = 256) { return (unsigned)((n + t - 1) / t); }

@@ -19,6 +19,11 @@ from . import abi
 SOFT_CLAY = (1000.0, 1e4, 0.3, 2e3)     # mpm.hpp:45
 STIFF_CLAY = (1000.0, 3e5, 0.3, 1e4)    # mpm.hpp:46
 FIRM_CLAY = (1000.0, 1e5, 0.3, 4e3)     # scenario.hpp:390 (write-mini)
+# north_star materials without a reference implementation (parity with the
+# oracle's restatement of the published algorithms): (density, E, nu, param, model)
+SAND = (1600.0, 3.5e4, 0.3, 30.0, abi.MODEL_DRUCKER_PRAGER)      # param = friction angle (deg)
+WATER = (1000.0, 2e4, 0.2, 0.0, abi.MODEL_FLUID)                 # K = E / (3 (1 - 2 nu))
+JELLY = (1000.0, 5e4, 0.3, 0.0, abi.MODEL_FIXED_COROTATED)
 V0_SOFT = 6.2e-8                        # mpm.hpp:47
 V0_STIFF = 1.2e-7                       # mpm.hpp:48
 
@@ -135,9 +140,10 @@ class Scene:
 
     def material_array(self):
         arr = (abi.Material * len(self.materials))()
-        for i, (rho, E, nu, sy) in enumerate(self.materials):
+        for i, mat in enumerate(self.materials):  # (density, E, nu, yield [, model])
+            rho, E, nu, sy = mat[:4]
             arr[i].density, arr[i].youngs, arr[i].poisson, arr[i].yield_stress = rho, E, nu, sy
-            arr[i].model = 0
+            arr[i].model = mat[4] if len(mat) > 4 else abi.MODEL_HENCKY_VON_MISES
         return arr
 
     @property
@@ -236,11 +242,11 @@ def box_sdf_volume(half, voxel, pad):
 # ---------------------------------------------------------------------------
 # Configurations.
 
-def config_a() -> Scene:
-    """A: 8k soft clay, 64^3, one dynamic box falling onto the block."""
+def config_a(material: tuple = SOFT_CLAY) -> Scene:
+    """A: 8k soft clay (or another material), 64^3, one dynamic box falling onto the block."""
     s = V0_SOFT ** (1.0 / 3.0)
     lo = (0.28, 0.28, 0.05)
-    env = block_env(lo, (20, 20, 20), 0, SOFT_CLAY, V0_SOFT, seed=1, vel_seed=2)
+    env = block_env(lo, (20, 20, 20), 0, material, V0_SOFT, seed=1, vel_seed=2)
     top = lo[2] + lattice_span(20, V0_SOFT)
     cxy = lo[0] + 0.5 * lattice_span(20, V0_SOFT)
     box = BodySpec(mode=abi.BODY_DYNAMIC, t=(cxy, cxy, top + 0.002 + 0.01), v=(0.0, 0.0, -0.2),
@@ -248,7 +254,7 @@ def config_a() -> Scene:
     env.bodies = [box]
     env.shapes = [ShapeSpec(abi.SHAPE_BOX, 0, params=(0.03, 0.03, 0.01), **soft_contact())]
     del s
-    return Scene(name="A", dims=(64, 64, 64), h=0.01, dt=5e-4, envs=[env], c_d=0.05)
+    return Scene(name="A", dims=(64, 64, 64), h=0.01, dt=5e-4, envs=[env], c_d=0.05, materials=[material])
 
 
 def _bucket_shapes(body: int, half_w: float, half_h: float, wall: float, friction=0.2):
@@ -265,27 +271,29 @@ def _bucket_shapes(body: int, half_w: float, half_h: float, wall: float, frictio
     return sh
 
 
-def config_b() -> Scene:
-    """B (clay parity variant): 32k bed, 64^3, scripted 5-box bucket scooping."""
+def config_b(material: tuple = SOFT_CLAY) -> Scene:
+    """B: 32k bed (clay parity variant by default; SAND = Drucker-Prager), 64^3,
+    scripted 5-box bucket scooping."""
     lo = (0.2399, 0.2399, 0.021)
-    env = block_env(lo, (40, 40, 20), 0, SOFT_CLAY, V0_SOFT, seed=3, vel_seed=4)
+    env = block_env(lo, (40, 40, 20), 0, material, V0_SOFT, seed=3, vel_seed=4)
     top = lo[2] + lattice_span(20, V0_SOFT)
     bucket = BodySpec(mode=abi.BODY_SCRIPTED, t=(lo[0] + 0.04, 0.32, top + 0.02), v=(0.05, 0.0, -0.05))
     env.bodies = [bucket]
     env.shapes = _bucket_shapes(0, 0.03, 0.02, 0.004)
-    return Scene(name="B", dims=(64, 64, 64), h=0.01, dt=5e-4, envs=[env], c_d=0.05)
+    return Scene(name="B", dims=(64, 64, 64), h=0.01, dt=5e-4, envs=[env], c_d=0.05, materials=[material])
 
 
-def config_c() -> Scene:
-    """C (clay parity variant): 64k column, 128^3 h=0.005, rotating bottle + static beaker."""
+def config_c(material: tuple = SOFT_CLAY) -> Scene:
+    """C: 64k column (clay parity variant by default; WATER = J-only fluid),
+    128^3 h=0.005, rotating bottle + static beaker."""
     lo = (0.24, 0.24, 0.06)
-    env = block_env(lo, (40, 40, 40), 0, SOFT_CLAY, V0_SOFT, seed=5, vel_seed=6)
+    env = block_env(lo, (40, 40, 40), 0, material, V0_SOFT, seed=5, vel_seed=6)
     c = lo[0] + 0.5 * lattice_span(40, V0_SOFT)
     bottle = BodySpec(mode=abi.BODY_SCRIPTED, t=(c, c, lo[2] + 0.085), w=(0.0, 0.5, 0.0))
     beaker = BodySpec(mode=abi.BODY_KINEMATIC, t=(c + 0.2, c, 0.06))
     env.bodies = [bottle, beaker]
     env.shapes = _bucket_shapes(0, 0.09, 0.085, 0.005) + _bucket_shapes(1, 0.06, 0.04, 0.005)
-    return Scene(name="C", dims=(128, 128, 128), h=0.005, dt=5e-4, envs=[env], c_d=0.05)
+    return Scene(name="C", dims=(128, 128, 128), h=0.005, dt=5e-4, envs=[env], c_d=0.05, materials=[material])
 
 
 def config_d_env(e: int) -> EnvSpec:

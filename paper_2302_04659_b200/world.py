@@ -161,6 +161,12 @@ class GpuWorld:
             self.ctx, env, abi.dptr(x), abi.dptr(v), abi.dptr(F), abi.dptr(Cm), abi.u8ptr(lost)))
         return dict(x=x, v=v, F=F, C=Cm, lost=lost)
 
+    def jp(self, env: int = 0) -> np.ndarray:
+        """Per-particle model scalar (fluid J, Drucker-Prager plastic strain, else 1)."""
+        out = np.zeros(self.counts[env])
+        _check(self.lib, self.ctx, self.lib.msim_gpu_read_jp(self.ctx, env, abi.dptr(out)))
+        return out
+
     def grid(self, env: int = 0):
         nn = int(np.prod(self.scene.dims))
         m = np.zeros(nn)
