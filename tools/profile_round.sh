@@ -13,3 +13,5 @@ ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/la
     python bench.py --steps 1 --warmup 1 --no-cpu-baseline > $O/ncu_launches.log 2>&1; echo "launch list rc=$?"
 ncu --set full --import-source on --clock-control none -k regex:k_particles -s 41 -c 1 -f -o $O/kp_D \
     python bench.py --steps 1 --warmup 1 --no-cpu-baseline > $O/ncu_full.log 2>&1; echo "ncu full rc=$?"
+python tools/bench_small.py > $O/small.json 2>&1; echo "small configs rc=$?"
+python tools/bench_tasks.py --out $O/tasks.json > /dev/null 2>&1; echo "tasks rc=$?"
