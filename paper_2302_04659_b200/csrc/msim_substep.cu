@@ -217,6 +217,9 @@ __device__ __forceinline__ void item_rounds(const SimParams& P, Smem<NCH, F>& S,
         const bool valid = t < rn;
         const int j = r0 + t;
         const int i = valid ? P.perm[j] : 0;
+#ifndef MSIM_NO_L2_PREFETCH  // L2 prefetch of this thread's next particle, one trip ahead (-1 %)
+        const int i_pf = j + kT < IC.e ? P.perm[j + kT] : -1;
+#endif
         unsigned meta = valid ? lds(&P.cur.meta[i]) : (1u << kLostBit);
         const int penv = (meta >> 8) & kEnvMask;
         const bool was_lost = meta >> kLostBit;
@@ -341,6 +344,19 @@ __device__ __forceinline__ void item_rounds(const SimParams& P, Smem<NCH, F>& S,
           if (AM) sts(&P.nxt.jp[j], jp);
           sts(&P.nxt.pid[j], pid);
         }
+#ifndef MSIM_NO_L2_PREFETCH
+        if (i_pf >= 0) {
+          auto pf = [](const void* a) { asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(a)); };
+#pragma unroll
+          for (int a = 0; a < 3; ++a) pf(&P.cur.x[a][i_pf]);
+#pragma unroll
+          for (int k = 0; k < 9; ++k) pf(&P.cur.G[k][i_pf]);
+          pf(&P.cur.mass[i_pf]);
+          pf(&P.cur.vol0[i_pf]);
+          pf(&P.cur.meta[i_pf]);
+          pf(&P.cur.pid[i_pf]);
+        }
+#endif
 
         // ---------------- binning of the (new) position + P2G payload of the next cycle
         int key_new = P.n_keys - 1;
