@@ -4,20 +4,22 @@
 // grid hook -> grid_update -> g2p_advect (mpm.hpp:410-418). Here one
 // batched launch sequence per cycle does, for every environment at once:
 //
-//   k_particles  one CTA per bucket (node block of kBX x kBY x kBZ base
-//                cells). Gathers the bucket's particles (perm), runs G2P of
-//                this cycle against a shared-memory velocity tile
-//                (mpm.hpp:346-379) with the von Mises return map
-//                (mpm.hpp:166-181), and in the same pass the P2G of the next
-//                cycle: penalty hook (coupling.hpp:151-172), Kirchhoff stress
-//                from the SAME principal frame (mpm.hpp:152-161), and a
-//                scatter into a shared-memory node tile: staged particles are
-//                ordered by (rank within cell, cell) so the lanes of a warp
-//                hold distinct cells, and each thread adds its particle's 27
-//                node contributions with native int32 shared atomics on a
-//                per-round fixed-point scale (no CAS loops, no conflicts).
-//                The tile goes to HBM with vector REDs. Particles are written back in bucket
-//                order with their next bucket key (the per-cycle re-sort).
+//   k_particles  persistent CTAs over buckets (1 or 2^3 node blocks of
+//                kBX x kBY x kBZ base cells, by particle density). Gathers the
+//                bucket's particles (perm), runs G2P of this cycle against a
+//                shared-memory velocity tile (mpm.hpp:346-379), the F update
+//                and the material's return map (mpm.hpp:166-181 for the
+//                reference's von Mises clay), and in the same pass the P2G of
+//                the next cycle: penalty hook (coupling.hpp:151-172), Kirchhoff
+//                stress from the SAME strain evaluation (mpm.hpp:152-161; the
+//                Hencky strain as a matrix function of F F^T, msim_device.cuh),
+//                and a scatter into a shared-memory node tile: each thread adds
+//                one staged particle's 27 node contributions with native int32
+//                shared atomics on a per-round fixed-point scale, lanes taking
+//                slots ~0.618 rn apart so a warp's stencils rarely collide.
+//                The tile goes to HBM with vector REDs. Particles are written
+//                back in bucket order with their next bucket key (the
+//                per-cycle re-sort).
 //   scans        bucket offsets + active list, node-block list
 //   k_iter_end   per env: substep/cycle counters, CFL plan (mpm.hpp:400-409),
 //                lost-fraction check, force-balance diagnostic
