@@ -205,10 +205,12 @@ def run_ours(args):
     lib = abi.load()
     t_setup = time.perf_counter()
     if args.config == "E":
-        scene = config_e()
+        scene = config_e(clay_only=args.clay_only)
         n_envs = 1
-        workload = ("E: 4M mixed soft/stiff clay (clay-only parity variant), 256^3 grid h=0.005, 8 moving colliders "
-                    "(boxes, spheres, capsules, SDF volume), 25 substeps/env step, replica per GPU")
+        workload = (("E: 4M soft/stiff clay (clay-only variant)" if args.clay_only else
+                     "E: 4M mixed clay / Drucker-Prager sand / J-only water / fixed-corotated jelly slabs")
+                    + ", 256^3 grid h=0.005, 8 moving colliders (boxes, spheres, capsules, SDF volume), "
+                    "25 substeps/env step, replica per GPU")
     else:
         n_envs = args.envs
         scene = config_d(n_envs=n_envs, first_env=weak_first_env(n_envs, rank))
@@ -368,6 +370,7 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--envs", type=int, default=1024, help="config-D envs per GPU")
     ap.add_argument("--config", choices=["D", "E"], default="D", help="workload (SURVEY.md App. B)")
+    ap.add_argument("--clay-only", action="store_true", help="config E: the reference's model only")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--traffic", type=float, default=None, help="ncu dram bytes per launch of the dominant kernel")
     args = ap.parse_args()

@@ -327,18 +327,20 @@ def config_d(n_envs: int = 1024, first_env: int = 0) -> Scene:
 
 
 def config_e(clay_only: bool = True, slab=(50, 200, 100), grid: int = 256) -> Scene:
-    """E: 4M particles in 4 x-slabs (soft / stiff clay alternating in the clay-only
-    parity variant), 256^3 h=0.005, 8 moving colliders (3 boxes, 2 spheres,
-    2 capsules, 1 SDF volume). `slab` / `grid` give reduced parity variants."""
+    """E: 4M particles in 4 x-slabs, 256^3 h=0.005, 8 moving colliders (3 boxes,
+    2 spheres, 2 capsules, 1 SDF volume). Mixed materials (clay, sand, water,
+    jelly slabs) or the clay-only variant (soft / stiff clay alternating, the
+    reference's model only). `slab` / `grid` give reduced parity variants."""
     s = V0_SOFT ** (1.0 / 3.0)
     extent = grid * 0.005
     span = lattice_span(slab[1], V0_SOFT)
     lo = ((extent - span) / 2, (extent - span) / 2, 0.021)
     xs, ms, mats = [], [], []
+    materials = [SOFT_CLAY, STIFF_CLAY] if clay_only else [SOFT_CLAY, SAND, WATER, JELLY]
     for k in range(4):
         slab_lo = (lo[0] + k * slab[0] * s, lo[1], lo[2])
-        mid = k % 2
-        mat = SOFT_CLAY if mid == 0 else STIFF_CLAY
+        mid = k % 2 if clay_only else k
+        mat = materials[mid]
         e = block_env(slab_lo, slab, mid, mat, V0_SOFT, seed=7 + 10 * k)
         xs.append(e.x)
         ms.append(e.mass)
@@ -371,7 +373,7 @@ def config_e(clay_only: bool = True, slab=(50, 200, 100), grid: int = 256) -> Sc
                                     **soft_contact()))
     env.bodies = bodies
     env.shapes = shapes
-    return Scene(name="E", dims=(grid, grid, grid), h=0.005, dt=1e-4, materials=[SOFT_CLAY, STIFF_CLAY],
+    return Scene(name="E", dims=(grid, grid, grid), h=0.005, dt=1e-4, materials=materials,
                  envs=[env], c_d=0.05)
 
 

@@ -78,3 +78,23 @@ def test_mixed_models_in_one_scene():
     pg, po = gw.particles(0), ow.particles()
     assert np.linalg.norm(pg["x"] - po["x"]) / np.linalg.norm(po["x"]) < 1e-4
     assert rel(pg["v"], po["v"]) < 1e-4
+
+
+def test_config_e_reduced_mixed_materials():
+    """E's mixed-material form (clay / sand / water / jelly slabs, 8 colliders
+    incl. an SDF volume, sparse buckets) at a size the oracle runs in seconds."""
+    from paper_2302_04659_b200.scenes import config_e
+
+    scene = config_e(clay_only=False, slab=(12, 48, 24), grid=64)
+    scene.n_rigid = 10
+    gw, ow = GpuWorld(scene), OracleWorld(scene)
+    gw.env_step()
+    ow.env_step()
+    pg, po = gw.particles(0), ow.particles()
+    assert np.linalg.norm(pg["x"] - po["x"]) / np.linalg.norm(po["x"]) < 1e-4
+    assert rel(pg["v"], po["v"]) < 1e-4
+    assert np.abs(gw.jp(0) - ow.jp()).max() < 1e-4
+    fg, _ = gw.wrenches(0, pending=True)
+    fo, _ = ow.wrenches(pending=True)
+    for b in range(len(fo)):
+        assert np.linalg.norm(fg[b] - fo[b]) / max(np.linalg.norm(fo[b]), 1e-6) < 1e-3, (b, fg[b], fo[b])
