@@ -1,4 +1,4 @@
-"""env-steps/s of the small single-scene configs A, B, C (launch/latency bound,
+"""env-steps/s of the small single-scene configs A (clay), B (sand), C (water) (launch/latency bound,
 SURVEY.md §8d: reported in absolute terms, not as a roofline fraction)."""
 import json
 import os
@@ -8,10 +8,11 @@ import time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
 from paper_2302_04659_b200 import GpuWorld  # noqa: E402
-from paper_2302_04659_b200.scenes import config_a, config_b, config_c  # noqa: E402
+from paper_2302_04659_b200.scenes import SAND, WATER, config_a, config_b, config_c  # noqa: E402
 
 out = {}
-for name, fn in (("A", config_a), ("B", config_b), ("C", config_c)):
+# BASELINE.json configs: A elastoplastic clay + box; B Drucker-Prager sand + bucket; C fluid + bottle/beaker
+for name, fn in (("A", config_a), ("B", lambda: config_b(material=SAND)), ("C", lambda: config_c(material=WATER))):
     scene = fn()
     gw = GpuWorld(scene)
     for _ in range(3):
