@@ -116,10 +116,8 @@ struct msim_gpu_ctx {
   DevBuf gPM_d, gF_d, gV_d, nb_flag_d, nb_scan_d, nb_list_d, n_nb_d, scan_tmp_d;
   std::vector<char> env_grid_dirty;
 
-  // host-mapped control words
-  int* h_ctl = nullptr;  // host-mapped control words (unused by the fused pipeline)
+  // device control words
   DevBuf ctl_d;          // [0] device redo flag
-  int* d_ctl = nullptr;
 
   double time = 0.0;
   KernelTimer timer;
@@ -693,10 +691,8 @@ int msim_gpu_create(const msim_soft_desc* desc, const msim_material* materials, 
     CK(cudaMemset(c->nb_flag_d.p, 0, sizeof(int) * nblocks));
     CK(cudaMemset(c->n_nb_d.p, 0, sizeof(int)));
     set_bucket_shape(c, 1);
-    CK(cudaHostAlloc(&c->h_ctl, 4 * sizeof(int), cudaHostAllocMapped));
     CK(c->ctl_d.ensure(4 * sizeof(int)));
     CK(cudaMemset(c->ctl_d.p, 0, 4 * sizeof(int)));
-    CK(cudaHostGetDevicePointer(&c->d_ctl, c->h_ctl, 0));
     carve_particles(c, 0, 0);
     carve_particles(c, 1, 0);
     alloc_binning(c);
@@ -717,7 +713,6 @@ void msim_gpu_destroy(msim_gpu_ctx* c) {
   if (!c) return;
   cudaSetDevice(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
-  if (c->h_ctl) cudaFreeHost(c->h_ctl);
   if (c->stream) cudaStreamDestroy(c->stream);
   delete c;
 }
