@@ -10,6 +10,7 @@
 #include <algorithm>
 #include <climits>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <random>
 #include <stdexcept>
@@ -636,6 +637,7 @@ int msim_gpu_create(const msim_soft_desc* desc, const msim_material* materials, 
   auto* c = new msim_gpu_ctx();
   int rc = guarded(c, [&]() -> int {
     c->device = device;
+    c->use_graphs = std::getenv("MSIM_NO_GRAPHS") == nullptr;  // eager launches (debugging / A-B checks)
     set_device(c);
     configure_kernels();
     CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
