@@ -190,3 +190,16 @@ np.save(sys.argv[1], np.concatenate([gw.particles(e)["x"].ravel() for e in range
         subprocess.run([sys.executable, "-c", code, path], check=True, env={**os.environ, **env_extra}, timeout=300)
         outs.append(np.load(path))
     assert np.linalg.norm(outs[0] - outs[1]) <= 1e-6 * np.linalg.norm(outs[1])
+
+
+def test_scene_json_world_steps_like_the_oracle():
+    """A reference-format scene file -> batched device world (3 identical envs)
+    -> one env step, against the oracle stepping the same Scene."""
+    import json as _json
+
+    from test_scene_json import SCENE
+
+    from paper_2302_04659_b200.scene_json import scene_from_json
+
+    scene = scene_from_json(_json.loads(_json.dumps(SCENE)), n_envs=3)
+    gw, ows, _ = compare(scene, envs=[0, 2])
