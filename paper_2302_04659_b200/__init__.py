@@ -10,5 +10,7 @@ abi.load()
 
 from .scenes import CONFIGS, Scene  # noqa: E402
 from .world import DeviceError, GpuWorld, SimulationDiverged, bake_mesh_sdf, make_box_mesh  # noqa: E402
+from .scene_json import SceneConfigError, scene_from_json  # noqa: E402
 
-__all__ = ["abi", "CONFIGS", "Scene", "GpuWorld", "SimulationDiverged", "DeviceError", "bake_mesh_sdf", "make_box_mesh"]
+__all__ = ["abi", "CONFIGS", "Scene", "GpuWorld", "SimulationDiverged", "DeviceError", "bake_mesh_sdf", "make_box_mesh",
+           "scene_from_json", "SceneConfigError"]
