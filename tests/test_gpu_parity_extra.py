@@ -203,3 +203,24 @@ def test_scene_json_world_steps_like_the_oracle():
 
     scene = scene_from_json(_json.loads(_json.dumps(SCENE)), n_envs=3)
     gw, ows, _ = compare(scene, envs=[0, 2])
+
+
+def test_batch_with_empty_and_single_particle_envs():
+    """Edge cases of a batch: an env without particles and an env with one
+    particle step alongside a normal one (each against the oracle)."""
+    from paper_2302_04659_b200.scenes import EnvSpec
+
+    normal = small_block(81)
+    empty = EnvSpec(x=np.zeros((0, 3)), mass=np.zeros(0), vol0=np.zeros(0), material=np.zeros(0, np.int32))
+    single = EnvSpec(x=np.array([[0.15, 0.15, 0.15]]), mass=np.array([6.2e-5]), vol0=np.array([6.2e-8]),
+                     v=np.array([[0.3, -0.2, 0.1]]), material=np.zeros(1, np.int32))
+    scene = Scene(name="edge", dims=(32, 32, 32), h=0.01, dt=5e-4, envs=[normal, empty, single], n_rigid=5)
+    gw = GpuWorld(scene)
+    gw.env_step()
+    for e in (0, 2):
+        o = OracleWorld(scene, env=e)
+        o.env_step()
+        pg, po = gw.particles(e), o.particles()
+        assert np.linalg.norm(pg["x"] - po["x"]) / np.linalg.norm(po["x"]) < 1e-4, e
+        assert rel(pg["v"], po["v"]) < 1e-4, e
+    assert gw.particles(1)["x"].shape == (0, 3)
