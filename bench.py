@@ -191,7 +191,7 @@ def run_ours(args):
 
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
     if world > 1:
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
@@ -344,7 +344,7 @@ def run_ours(args):
             "config": {"workload": workload, "envs_per_gpu": n_envs,
                        "particles_per_gpu": n_part, "substeps_per_env_step": S, "dt": scene.dt,
                        "parallelism": f"env-sharded x{world} (no data-path collective)",
-                       "l2": "inputs larger than L2 (particle state 2 x %.2f GB)" % (n_part * 112 / 1e9)},
+                       "l2": "inputs larger than L2 (particle state 2 x %.2f GB)" % (n_part * 116 / 1e9)},
             "roofline": roofline,
             "roofline_path": roofline_path,
             "kernels": kernels,
@@ -374,6 +374,16 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--traffic", type=float, default=None, help="ncu dram bytes per launch of the dominant kernel")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # one process per GPU: relaunch this command under torch.distributed.run
+        import socket
+
+        with socket.socket() as so:
+            so.bind(("127.0.0.1", 0))
+            port = so.getsockname()[1]
+        os.execvp(sys.executable, [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+                                   f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+                                   "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]])
     if args.impl == "reference":
         return run_reference(args)
     return run_ours(args)
