@@ -58,5 +58,15 @@ int main() {
   double f[3], t[3];
   msim_gpu_read_wrenches(st.handle(), 0, 1, f, t);
   std::printf("free_fall_err %.3e cycles %d lost %zu wrench_z %.6g\n", err, cycles, st.lost_count(), f[2]);
+
+  // episode-level consumers: metric_fill (scenario.hpp:63-75) and a baked mesh SDF (sdf.hpp:277-310)
+  const auto fill = msim_gpu::metric_fill(st, {msim_region{{0.0, 0.0, 0.0}, {0.32, 0.32, 0.32}}});
+  std::vector<double> tri(108);
+  const double half[3] = {0.02, 0.02, 0.01};
+  msim_make_box_mesh(half, nullptr, tri.data());
+  const auto vol = msim_gpu::bake_mesh_sdf(tri, 0.005, 0.01);
+  float smin = vol.samples[0];
+  for (float v : vol.samples) smin = v < smin ? v : smin;
+  std::printf("fill_fraction %.6f sdf_samples %zu sdf_min %.6f\n", fill[0].fraction, vol.samples.size(), smin);
   return err < 1e-3 ? 0 : 1;
 }

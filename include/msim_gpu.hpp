@@ -102,6 +102,21 @@ class SoftState {
   void set_dt(double dt) { check(msim_gpu_set_dt(ctx_, dt), ctx_); }
   std::size_t lost_count(int env = 0) const { return (std::size_t)msim_gpu_lost_count(ctx_, env); }
 
+  // per-particle material scalar (fluid J, Drucker-Prager plastic strain, else 1)
+  std::vector<double> jp(int env = 0) const {
+    std::vector<double> out((size_t)msim_gpu_particle_count(ctx_, env));
+    check(msim_gpu_read_jp(ctx_, env, out.data()), ctx_);
+    return out;
+  }
+
+  // batched reset: seed_particles_box (seeding.hpp:13-35) on the device for the listed envs
+  void seed_envs(const std::vector<int32_t>& envs, const std::vector<uint64_t>& seeds,
+                 const std::vector<double>& boxes, int material, double particle_volume) {
+    check(msim_gpu_seed_envs(ctx_, (int)envs.size(), envs.data(), seeds.data(), boxes.data(), material,
+                             particle_volume),
+          ctx_);
+  }
+
  private:
   msim_gpu_ctx* ctx_ = nullptr;
 };
@@ -129,6 +144,35 @@ inline void set_bodies(SoftState& st, int env, const std::vector<msim_body>& bod
   check(msim_gpu_set_bodies(st.handle(), env, bodies.data(), (int)bodies.size(), shapes.data(),
                             (int)shapes.size()),
         st.handle());
+}
+
+// ---- task metrics over every env (scenario.hpp:63-209) ----------------------
+inline std::vector<msim_fill_result> metric_fill(SoftState& st, const std::vector<msim_region>& regions) {
+  std::vector<msim_fill_result> out(regions.size());
+  check(msim_gpu_metric_fill(st.handle(), regions.data(), out.data()), st.handle());
+  return out;
+}
+inline std::vector<double> render_heightmap(SoftState& st, const std::vector<msim_region>& regions, int nx, int ny) {
+  std::vector<double> maps(regions.size() * (size_t)nx * ny);
+  check(msim_gpu_render_heightmap(st.handle(), regions.data(), nx, ny, maps.data()), st.handle());
+  return maps;
+}
+
+// ---- mesh SDF baking (sdf.hpp:277-310) ------------------------------------
+struct BakedVolume {
+  double origin[3];
+  int32_t dims[3];
+  std::vector<float> samples;  // x fastest, ready for msim_shape.vol_samples
+};
+inline BakedVolume bake_mesh_sdf(const std::vector<double>& triangles, double voxel, double padding, int device = 0) {
+  BakedVolume v{};
+  const int64_t n = (int64_t)(triangles.size() / 9);
+  check(msim_bake_grid(triangles.data(), n, voxel, padding, v.origin, v.dims), nullptr);
+  v.samples.resize((size_t)v.dims[0] * v.dims[1] * v.dims[2]);
+  check(msim_gpu_bake_mesh_sdf(device, triangles.data(), n, voxel, padding, v.samples.data(),
+                               (int64_t)v.samples.size()),
+        nullptr);
+  return v;
 }
 
 // sync_rigid_to_soft (coupling.hpp:106-117) with new body states of one env.

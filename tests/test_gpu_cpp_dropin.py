@@ -21,3 +21,5 @@ def test_cpp_drop_in_runs_on_device():
     assert fields[0] == "free_fall_err" and float(fields[1]) < 1e-3
     assert int(fields[3]) == 20  # 20 substeps, no halving
     assert float(fields[7]) < 0.0  # the floor pushes the clay up: reaction on the body points down
+    assert fields[8] == "fill_fraction" and float(fields[9]) == 1.0  # every particle inside the domain box
+    assert int(fields[11]) > 0 and -0.011 < float(fields[13]) < -0.008  # box SDF minimum ~ -half_z
