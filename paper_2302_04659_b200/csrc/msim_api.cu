@@ -216,6 +216,7 @@ SimParams params(msim_gpu_ctx* c) {
   P.pending = c->pending_d.as<double>();
   P.n_running = nullptr;
   P.any_redo = c->ctl_d.as<int>();
+  P.item_counter = c->ctl_d.as<int>() + 2;
   P.redo_pass = 0;
   P.hooks = 1;
   P.cur = c->buf[c->cur];

@@ -89,6 +89,11 @@ template <int NCH> constexpr int pay_floats() { return NCH == 4 ? 16 : 28; }
 #define MSIM_CTAS_PER_SM 5  // measured: 4 -> 1.12, 5 -> 1.05, 6 -> 1.10 ms per launch (config D, 256 envs)
 #endif
 constexpr int kCtasPerSm = MSIM_CTAS_PER_SM;
+#ifdef MSIM_STATIC_ITEMS  // variant build: static round-robin bucket assignment
+constexpr bool kDynamicItems = false;
+#else
+constexpr bool kDynamicItems = true;
+#endif
 
 // Particle state is streamed once per launch: evict-first loads / stores
 // (ld/st .cs) keep L1 for the register spills and the per-bucket tiles.
@@ -146,6 +151,7 @@ struct Smem {
   unsigned penmax;
   unsigned maxb[3];
   ItemCtx ic;              // the current bucket's uniform context (read back instead of held in registers)
+  int next_item;
 };
 
 
@@ -678,11 +684,21 @@ __global__ void __launch_bounds__(kT, kCtasPerSm) k_particles(SimParams P) {
   for (int t = tid; t < NCH * PN; t += kT) (&S.itile[0][0])[t] = 0;
 
   volatile ItemCtx& IC = S.ic;
-  for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
+  // Buckets are handed out dynamically (one atomic per bucket): their sizes
+  // vary, and a static round-robin leaves a tail of CTAs with more work.
+  if (tid == 0) S.next_item = kDynamicItems ? atomicAdd(P.item_counter + redo, 1) : (int)blockIdx.x;
+  __syncthreads();
+  for (int item = S.next_item; item < nitems;) {
     const int key = P.active_buckets[item];
     const bool lostb = key == P.n_keys - 1;
     const int benv = lostb ? 0 : key / P.buckets_per_env;
-    if (redo && (lostb || !P.run[benv].redo)) continue;  // CTA-uniform
+    if (redo && (lostb || !P.run[benv].redo)) {  // CTA-uniform
+      __syncthreads();
+      if (tid == 0) S.next_item = kDynamicItems ? atomicAdd(P.item_counter + redo, 1) : item + (int)gridDim.x;
+      __syncthreads();
+      item = S.next_item;
+      continue;
+    }
     const int s = P.bucket_start[key], e = P.bucket_start[key + 1];
     const int act = lostb ? kActIdle : P.run[benv].action;
     const bool do_g2p = act == kActFused || act == kActG2P;
@@ -732,6 +748,10 @@ __global__ void __launch_bounds__(kT, kCtasPerSm) k_particles(SimParams P) {
     }
     __syncthreads();
     item_rounds<NCH, F, AM>(P, S, redo);
+    __syncthreads();
+    if (tid == 0) S.next_item = kDynamicItems ? atomicAdd(P.item_counter + redo, 1) : item + (int)gridDim.x;
+    __syncthreads();
+    item = S.next_item;
   }
 }
 
@@ -1063,6 +1083,7 @@ void launch_k_particles(const SimParams& P, cudaStream_t s) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_particles<NCH, F, AM>, kT, sizeof(Smem<NCH, F>));
     if (per_sm <= 0) per_sm = 1;
   }
+  if (kDynamicItems) cudaMemsetAsync(P.item_counter + (P.redo_pass ? 1 : 0), 0, sizeof(int), s);
   k_particles<NCH, F, AM><<<sm_count() * per_sm, kT, sizeof(Smem<NCH, F>), s>>>(P);
 }
 
