@@ -694,8 +694,8 @@ int msim_gpu_create(const msim_soft_desc* desc, const msim_material* materials, 
     CK(cudaMemset(c->nb_flag_d.p, 0, sizeof(int) * nblocks));
     CK(cudaMemset(c->n_nb_d.p, 0, sizeof(int)));
     set_bucket_shape(c, 1);
-    CK(c->ctl_d.ensure(4 * sizeof(int)));
-    CK(cudaMemset(c->ctl_d.p, 0, 4 * sizeof(int)));
+    CK(c->ctl_d.ensure(8 * sizeof(int)));  // [0] redo flag, [2..5] particle-kernel hand-out counters
+    CK(cudaMemset(c->ctl_d.p, 0, 8 * sizeof(int)));
     carve_particles(c, 0, 0);
     carve_particles(c, 1, 0);
     alloc_binning(c);

@@ -202,7 +202,7 @@ struct SimParams {
   double* pending;           // staged wrenches (pending_wrenches)
   int* n_running;            // envs with substeps left after the last iteration
   int* any_redo;             // device flag: some env must redo its P2G (see EnvRun::redo)
-  int* item_counter;         // [2] dynamic bucket hand-out of the particle kernel (main, redo)
+  int* item_counter;         // [4] dynamic bucket hand-out of the particle kernel: next (main, redo), CTAs done (main, redo)
   int redo_pass;             // this particle launch is the redo pass
   int hooks;                 // run the penalty hooks (0: hook-free phase API, like p2g())
 

@@ -684,17 +684,17 @@ __global__ void __launch_bounds__(kT, kCtasPerSm) k_particles(SimParams P) {
   for (int t = tid; t < NCH * PN; t += kT) (&S.itile[0][0])[t] = 0;
 
   volatile ItemCtx& IC = S.ic;
-  // Buckets are handed out dynamically (one atomic per bucket): their sizes
-  // vary, and a static round-robin leaves a tail of CTAs with more work.
-  if (tid == 0) S.next_item = kDynamicItems ? atomicAdd(P.item_counter + redo, 1) : (int)blockIdx.x;
-  __syncthreads();
-  for (int item = S.next_item; item < nitems;) {
+  // Buckets are handed out dynamically after a first static one per CTA (one
+  // atomic per further bucket): their sizes vary, and a static round-robin
+  // leaves a tail of CTAs with more work (-12 % per launch at D).
+  for (int item = blockIdx.x; item < nitems;) {
     const int key = P.active_buckets[item];
     const bool lostb = key == P.n_keys - 1;
     const int benv = lostb ? 0 : key / P.buckets_per_env;
     if (redo && (lostb || !P.run[benv].redo)) {  // CTA-uniform
       __syncthreads();
-      if (tid == 0) S.next_item = kDynamicItems ? atomicAdd(P.item_counter + redo, 1) : item + (int)gridDim.x;
+      if (tid == 0)
+        S.next_item = (int)gridDim.x + (kDynamicItems ? atomicAdd(P.item_counter + redo, 1) : item);
       __syncthreads();
       item = S.next_item;
       continue;
@@ -749,9 +749,19 @@ __global__ void __launch_bounds__(kT, kCtasPerSm) k_particles(SimParams P) {
     __syncthreads();
     item_rounds<NCH, F, AM>(P, S, redo);
     __syncthreads();
-    if (tid == 0) S.next_item = kDynamicItems ? atomicAdd(P.item_counter + redo, 1) : item + (int)gridDim.x;
+    if (tid == 0) S.next_item = (int)gridDim.x + (kDynamicItems ? atomicAdd(P.item_counter + redo, 1) : item);
     __syncthreads();
     item = S.next_item;
+  }
+  // the last fetching CTA out resets the hand-out counter for the next launch
+  // (no memset node; CTAs without a first bucket never fetched)
+  if (kDynamicItems && tid == 0 && (int)blockIdx.x < nitems) {
+    __threadfence();
+    if (atomicAdd(P.item_counter + 2 + redo, 1) == min((int)gridDim.x, nitems) - 1) {
+      P.item_counter[redo] = 0;
+      P.item_counter[2 + redo] = 0;
+      __threadfence();
+    }
   }
 }
 
@@ -1083,7 +1093,6 @@ void launch_k_particles(const SimParams& P, cudaStream_t s) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_particles<NCH, F, AM>, kT, sizeof(Smem<NCH, F>));
     if (per_sm <= 0) per_sm = 1;
   }
-  if (kDynamicItems) cudaMemsetAsync(P.item_counter + (P.redo_pass ? 1 : 0), 0, sizeof(int), s);
   k_particles<NCH, F, AM><<<sm_count() * per_sm, kT, sizeof(Smem<NCH, F>), s>>>(P);
 }
 
