@@ -54,9 +54,11 @@ namespace {
 #define MSIM_KT 128
 #endif
 #ifndef MSIM_KCAP
-#define MSIM_KCAP 256
+#define MSIM_KCAP 128
 #endif
-// 128 threads / 256 particles per round measured best (64 / 128 at 9 CTAs/SM: +12 %)
+// 128 threads / 128 particles per round measured best with the dynamic bucket
+// hand-out (D, 1024 envs: 2.85 vs 2.98 ms per launch at 256 particles, 4.06 at 64;
+// 256 threads at 2-3 CTAs/SM +6-15 %; 64 threads / 128 at 9 CTAs/SM +12 %)
 constexpr int kT = MSIM_KT;      // threads per CTA (particle kernel), kCtasPerSm CTAs per SM
 constexpr int kCap = MSIM_KCAP;  // particles staged per round
 // Tile geometry of a particle bucket of F^3 node blocks (QX x QY x QZ base cells).
@@ -70,10 +72,10 @@ struct Geo {
   static constexpr int TZS = PX * PY + 4;
   static constexpr int PN = PZ * TZS;
   static constexpr int CX = QX + 2, CY = QY + 2, CZ = QZ + 2;  // P2G base cells (origin o-1)
-  // particles per round (512 measured 5 % slower on D than 256: four trips
-  // between barriers instead of two)
+  // particles per round: one trip per thread between barriers (see MSIM_KCAP)
   static constexpr int CAP = kCap;
-  // fixed point: |contribution| <= 2^SC_LOG2, CAP contributions per node <= 2^30
+  // fixed point: |contribution| <= 0.75^3 * 2^SC_LOG2 < 2^22 (the fix_rn range),
+  // CAP contributions per node <= 2^30
   static constexpr int SC_LOG2 = CAP == 512 ? 21 : (CAP == 256 ? 22 : 23);
 };
 #define MSIM_GEO_ALIASES(F)                                                                            \
