@@ -474,8 +474,11 @@ inline M3 drucker_prager_return_map(const M3& F_trial, const Material& m, double
   return s.U * M3::diag(V3(std::exp(e.x), std::exp(e.y), std::exp(e.z))) * s.V.transpose();
 }
 
-// Weakly compressible fluid (the J-only model of MLS-MPM's mpm88): pressure from
-// the tracked volume ratio, tau = K (J - 1) J I; F carries no shear (kept I).
+// Weakly compressible J-only fluid: linear equation of state on the tracked
+// volume ratio, Cauchy sigma = K (J - 1) I, Kirchhoff tau = J sigma =
+// K (J - 1) J I; F carries no shear (kept I). (MLS-MPM's mpm88 example drops
+// the J factor, tau ~ E (J - 1); this model keeps it, so the two agree only to
+// first order in J - 1. No reference implementation pins either.)
 inline M3 kirchhoff_fluid(double J, const Material& m) { return M3::Identity() * (m.bulk() * (J - 1.0) * J); }
 
 // Kirchhoff stress of particle p by its material model (P2G, mpm.hpp:235-237).

@@ -6,7 +6,11 @@ tests/, __graft_entry__.smoke() and bench.py's CPU-baseline legs use it, as
 the checker; the product path never imports this module.
 
 ``OracleWorld`` runs one environment of a ``paper_2302_04659_b200.scenes``
-Scene (the reference World is single-environment).
+Scene (the reference World is single-environment). ``RefWorld`` runs the
+same environment through oracle/_ref/libmsim_ref.so: the REFERENCE's own
+sources compiled against the Eigen subset in oracle/ref_shim/ (see
+ref_capi.cpp), with the same surface. This module never imports the product
+package (it uses its own struct mirror, oracle/cabi.py).
 """
 from __future__ import annotations
 
@@ -16,11 +20,13 @@ import subprocess
 
 import numpy as np
 
-from paper_2302_04659_b200 import abi
+from oracle import cabi as abi
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 BUILD = os.path.join(HERE, "_build")
 LIB = os.path.join(BUILD, "liboracle.so")
+REF_DIR = os.path.join(HERE, "_ref")
+REF_LIB = os.path.join(REF_DIR, "libmsim_ref.so")
 KAT = os.path.join(BUILD, "kat_oracle")
 
 _dp = C.POINTER(C.c_double)
@@ -29,23 +35,25 @@ _lp = C.POINTER(C.c_int64)
 _u8p = C.POINTER(C.c_uint8)
 _vp = C.c_void_p
 
+# struct pointers are passed untyped (void*): the product's and the checker's
+# layout-identical ctypes mirrors are both accepted
 _SIGS = {
-    "oracle_create": (_vp, [C.POINTER(abi.SoftDesc), C.POINTER(abi.Material), C.c_int]),
+    "oracle_create": (_vp, [_vp, _vp, C.c_int]),
     "oracle_destroy": (None, [_vp]),
     "oracle_last_error": (C.c_char_p, [_vp]),
     "oracle_set_threads": (None, [C.c_int]),
     "oracle_set_particles": (C.c_int, [_vp, C.c_int64, _dp, _dp, _dp, _dp, _dp, _dp, _ip]),
     "oracle_write_particles": (C.c_int, [_vp, C.c_int64, _dp, _dp, _dp, _dp]),
-    "oracle_set_bodies": (C.c_int, [_vp, C.POINTER(abi.Body), C.c_int, C.POINTER(abi.Shape), C.c_int]),
-    "oracle_sync_bodies": (C.c_int, [_vp, C.POINTER(abi.Body), C.c_int]),
-    "oracle_set_coupling": (C.c_int, [_vp, C.POINTER(abi.Coupling)]),
+    "oracle_set_bodies": (C.c_int, [_vp, _vp, C.c_int, _vp, C.c_int]),
+    "oracle_sync_bodies": (C.c_int, [_vp, _vp, C.c_int]),
+    "oracle_set_coupling": (C.c_int, [_vp, _vp]),
     "oracle_set_stepping": (C.c_int, [_vp, C.c_int, C.c_int, _dp]),
     "oracle_set_dt": (C.c_int, [_vp, C.c_double]),
     "oracle_set_gravity": (C.c_int, [_vp, _dp]),
     "oracle_set_lost_fraction_threshold": (C.c_int, [_vp, C.c_double]),
     "oracle_init": (C.c_int, [_vp]),
     "oracle_init_buffers": (C.c_int, [_vp]),
-    "oracle_env_step": (C.c_int, [_vp, C.POINTER(abi.StepReport)]),
+    "oracle_env_step": (C.c_int, [_vp, _vp]),
     "oracle_soft_substep": (C.c_int, [_vp, C.c_int, C.c_int, _ip]),
     "oracle_p2g": (C.c_int, [_vp]),
     "oracle_grid_update": (C.c_int, [_vp]),
@@ -60,12 +68,12 @@ _SIGS = {
     "oracle_write_grid_velocity": (C.c_int, [_vp, _dp]),
     "oracle_read_binning": (C.c_int, [_vp, _ip, _ip, C.c_int64, _ip, C.c_int64, _lp, _lp, C.c_int64, _lp]),
     "oracle_read_wrenches": (C.c_int, [_vp, C.c_int, _dp, _dp]),
-    "oracle_read_bodies": (C.c_int, [_vp, C.POINTER(abi.Body), C.c_int]),
+    "oracle_read_bodies": (C.c_int, [_vp, _vp, C.c_int]),
     "oracle_lost_count": (C.c_int64, [_vp]),
     "oracle_time": (C.c_double, [_vp]),
     "oracle_mean_particle_mass": (C.c_double, [_vp]),
-    "oracle_constitutive": (C.c_int, [C.POINTER(abi.Material), C.c_int64, _dp, _dp, _dp]),
-    "oracle_sdf": (C.c_int, [C.POINTER(abi.Shape), C.c_int64, _dp, _dp, _dp]),
+    "oracle_constitutive": (C.c_int, [_vp, C.c_int64, _dp, _dp, _dp]),
+    "oracle_sdf": (C.c_int, [_vp, C.c_int64, _dp, _dp, _dp]),
     "oracle_state_hash": (C.c_uint64, [_vp]),
     "oracle_rng_create": (_vp, [C.c_uint64]),
     "oracle_rng_destroy": (None, [_vp]),
@@ -84,7 +92,50 @@ _SIGS = {
     "oracle_metric_pinch": (C.c_int, [C.c_int64, _dp, C.c_int64, _dp, C.c_int64, _dp, _dp, _ip]),
 }
 
+# reference-harness-only entry points (ref_capi.cpp)
+_REF_SIGS = {
+    "ref_unsupported": (C.c_int, [_vp]),
+    "ref_set_kinematic_schedule": (C.c_int, [_vp, C.c_int, _dp, _u8p]),
+    "ref_bench_worlds": (C.c_double, [C.POINTER(_vp), C.c_int, C.c_int, _ip]),
+    "ref_config_d_env": (_vp, [C.c_int]),
+}
+
 _lib = None
+_ref = None
+
+
+class _RefAdapter:
+    """The reference harness library seen through the oracle's names."""
+
+    def __init__(self, cdll):
+        self.cdll = cdll
+        for name, (res, args) in _SIGS.items():
+            rname = "ref_" + name[len("oracle_"):]
+            f = getattr(cdll, rname, None)
+            if f is None:
+                continue
+            f.restype = res
+            f.argtypes = args
+            setattr(self, name, f)
+        for name, (res, args) in _REF_SIGS.items():
+            f = getattr(cdll, name)
+            f.restype = res
+            f.argtypes = args
+            setattr(self, name, f)
+
+
+def ref_available() -> bool:
+    return os.path.exists(REF_LIB)
+
+
+def load_ref():
+    """oracle/_ref/libmsim_ref.so (built here by Makefile.ref from /root/reference)."""
+    global _ref
+    if _ref is None:
+        if not os.path.exists(REF_LIB):
+            raise FileNotFoundError(f"{REF_LIB} not built (make -C oracle -f Makefile.ref needs /root/reference)")
+        _ref = _RefAdapter(C.CDLL(REF_LIB))
+    return _ref
 
 
 def build():
@@ -117,14 +168,19 @@ def _d(a):
 class OracleWorld:
     """One environment of a Scene in the CPU restatement (World + SoftState)."""
 
+    def _load(self):
+        return load()
+
     def __init__(self, scene, env: int = 0, threads: int = 1, init: bool = True):
-        self.lib = lib = load()
+        self.lib = lib = self._load()
         self.scene = scene
         e = scene.envs[env]
         self.env = e
-        mats = scene.material_array()
-        desc = scene.desc()
-        self.h = lib.oracle_create(C.byref(desc), mats, len(scene.materials))
+        nm = len(scene.materials)
+        mats = abi.convert(scene.material_array(), abi.Material * nm)
+        desc = abi.convert(scene.desc(), abi.SoftDesc)
+        self.h = lib.oracle_create(C.byref(desc), mats, nm)
+        self._after_create()
         lib.oracle_set_threads(threads)
         n = e.n
         self._keep = []
@@ -147,11 +203,14 @@ class OracleWorld:
         g = np.asarray(scene.rigid_gravity, dtype=np.float64)
         lib.oracle_set_stepping(self.h, scene.n_rigid, scene.n_soft, _d(g))
         if e.bodies:
-            B = (abi.Body * len(e.bodies))(*[b.to_c() for b in e.bodies])
-            S = (abi.Shape * max(len(e.shapes), 1))(*[s.to_c() for s in e.shapes])
+            B = (abi.Body * len(e.bodies))(*[abi.convert(b.to_c(), abi.Body) for b in e.bodies])
+            S = (abi.Shape * max(len(e.shapes), 1))(*[abi.convert(s.to_c(), abi.Shape) for s in e.shapes])
             self._check(lib.oracle_set_bodies(self.h, B, len(e.bodies), S, len(e.shapes)))
         if init:
             self._check(lib.oracle_init(self.h))
+
+    def _after_create(self):
+        pass
 
     def _check(self, rc):
         if rc == abi.MSIM_OK:
@@ -279,6 +338,35 @@ class OracleWorld:
             self.close()
         except Exception:
             pass
+
+
+class RefUnsupported(ValueError):
+    """The scene uses something the reference does not have (a non-von-Mises model)."""
+
+
+class RefWorld(OracleWorld):
+    """One environment of a Scene run by the REFERENCE's own code (oracle/_ref)."""
+
+    def _load(self):
+        return load_ref()
+
+    def _after_create(self):
+        if self.lib.ref_unsupported(self.h):
+            msg = self.lib.oracle_last_error(self.h).decode()
+            self.lib.oracle_destroy(self.h)
+            self.h = None
+            raise RefUnsupported(msg)
+
+    def set_kinematic_schedule(self, poses, mask=None):
+        """poses[n_steps, n_bodies, 7] = (qw qx qy qz tx ty tz) per rigid step of the next env step."""
+        p = np.ascontiguousarray(poses, dtype=np.float64)
+        m = None if mask is None else np.ascontiguousarray(mask, dtype=np.uint8)
+        self._sched = (p, m)
+        self._check(self.lib.ref_set_kinematic_schedule(self.h, p.shape[0], p.ctypes.data_as(_dp),
+                                                        None if m is None else m.ctypes.data_as(_u8p)))
+
+    def state_hash(self) -> int:
+        return int(self.lib.oracle_state_hash(self.h))
 
 
 def constitutive(F: np.ndarray, mat=(1000.0, 1e4, 0.3, 2e3)):

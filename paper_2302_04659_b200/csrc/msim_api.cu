@@ -568,6 +568,7 @@ int step_call(msim_gpu_ctx* c, int n_sub, bool integrate_rigid, int n_soft, int3
   int planned = n_sub;  // one launch per substep when no env halves its step
   int launched = n_sub;
   std::vector<EnvRun> run(c->n_env);
+  int more = 0;
   for (int guard = 0; guard < 64; ++guard) {
     for (; launched < planned; ++launched) {  // beyond the plan: some env halved its step further
       launch_iteration(P(), true, true, s);
@@ -577,7 +578,7 @@ int step_call(msim_gpu_ctx* c, int n_sub, bool integrate_rigid, int n_soft, int3
     CK(cudaMemcpyAsync(run.data(), c->run_d.p, sizeof(EnvRun) * c->n_env, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
     c->timer.flush();
-    int more = 0;
+    more = 0;
     for (const EnvRun& r : run)
       if (r.substeps_left > 0) more = std::max(more, (r.cycles - r.cycle) + (r.substeps_left - 1));
     if (more == 0) break;
@@ -588,7 +589,14 @@ int step_call(msim_gpu_ctx* c, int n_sub, bool integrate_rigid, int n_soft, int3
   c->perm_valid = true;
   if (cycles_out)
     for (int e = 0; e < c->n_env; ++e) cycles_out[e] = run[e].cycles;
-  return collect_errors(c);
+  const int rc = collect_errors(c);
+  if (rc != MSIM_OK) return rc;
+  if (more > 0) {  // 64 host passes did not finish every env's substeps: never return a short step as OK
+    for (int e = 0; e < c->n_env; ++e)
+      if (run[e].substeps_left > 0)
+        return fail(c, MSIM_ERR_DIVERGED, "substeps left unfinished after 64 launch passes (env " + std::to_string(e) + ")");
+  }
+  return MSIM_OK;
 }
 
 bool valid_material(const msim_material& m, std::string& why) {

@@ -151,7 +151,10 @@ struct Smem {
   int cellof[Geo<F>::CAP];  // local P2G cell of each staged slot, -1 if not staged
   double wsum[kWs];
   unsigned penmax;
-  unsigned maxb[3];
+  // per-round fixed-point bounds, double-buffered by round parity: round r
+  // publishes into maxb[r & 1] before its post-staging barrier while slot
+  // (r + 1) & 1 is zeroed between that barrier and the post-scatter one
+  unsigned maxb[2][3];
   ItemCtx ic;              // the current bucket's uniform context (read back instead of held in registers)
   int next_item;
 };
@@ -183,6 +186,11 @@ __constant__ SpreadTable kSpread = make_spread();
 // integer lands in the low mantissa bits of x + 1.5 * 2^23 (avoids F2I).
 __device__ __forceinline__ int fix_rn(float x) { return __float_as_int(x + 12582912.0f) - 0x4B400000; }
 
+// Fire-and-forget vector float add to global memory (RED, no return value).
+__device__ __forceinline__ void red_add_v4(float4* a, float x, float y, float z, float w) {
+  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(a), "f"(x), "f"(y), "f"(z), "f"(w) : "memory");
+}
+
 // Global-memory scatter of one particle (fallback when its stencil leaves the
 // bucket's P2G tile, e.g. a particle faster than the CFL bound assumed).
 template <int NCH>
@@ -196,11 +204,11 @@ __device__ MSIM_COLD void scatter_global(const SimParams& P, int env, const int*
                        bp.z + Ap[6] * di + Ap[7] * dj + Ap[8] * dk};
         const int gx = b[0] + di, gy = b[1] + dj, gz = b[2] + dk;
         const long long gi = env * P.nodes_per_env + ((long long)gz * P.dims[1] + gy) * P.dims[0] + gx;
-        atomicAdd(&P.gPM[gi], make_float4(w * pq.x, w * pq.y, w * pq.z, w * m));
+        red_add_v4(&P.gPM[gi], w * pq.x, w * pq.y, w * pq.z, w * m);
         if (NCH == 7) {
           const f3 fq = {bf.x + Af[0] * di + Af[1] * dj + Af[2] * dk, bf.y + Af[3] * di + Af[4] * dj + Af[5] * dk,
                          bf.z + Af[6] * di + Af[7] * dj + Af[8] * dk};
-          atomicAdd(&P.gF[gi], make_float4(w * fq.x, w * fq.y, w * fq.z, 0.0f));
+          red_add_v4(&P.gF[gi], w * fq.x, w * fq.y, w * fq.z, 0.0f);
         }
         if (mark) P.nb_flag[env * P.blocks_per_env + ((gz / kBZ) * P.bdims[1] + gy / kBY) * P.bdims[0] + gx / kBX] = 1;
       }
@@ -216,10 +224,9 @@ __device__ __forceinline__ void item_rounds(const SimParams& P, Smem<NCH, F>& S,
   volatile ItemCtx& IC = S.ic;
   {
 
-    for (int r0 = IC.s; r0 < IC.e; r0 += CAP) {
+    for (int r0 = IC.s, rpar = 0; r0 < IC.e; r0 += CAP, rpar ^= 1) {
       const int rn = min(CAP, IC.e - r0);
       const int trips = (rn + kT - 1) / kT;
-      if (tid < 3) S.maxb[tid] = 0u;
       float mx_m = 0.f, mx_p = 0.f, mx_f = 0.f;
       // ---------------- per-particle phase (CTA-uniform trip count for warp collectives)
       for (int trip = 0; trip < trips; ++trip) {
@@ -541,9 +548,9 @@ __device__ __forceinline__ void item_rounds(const SimParams& P, Smem<NCH, F>& S,
         mx_f = fmaxf(mx_f, __shfl_xor_sync(FULL, mx_f, o));
       }
       if (lane == 0) {
-        atomicMax(&S.maxb[0], __float_as_uint(mx_m));
-        atomicMax(&S.maxb[1], __float_as_uint(mx_p));
-        atomicMax(&S.maxb[2], __float_as_uint(mx_f));
+        atomicMax(&S.maxb[rpar][0], __float_as_uint(mx_m));
+        atomicMax(&S.maxb[rpar][1], __float_as_uint(mx_p));
+        atomicMax(&S.maxb[rpar][2], __float_as_uint(mx_f));
       }
       __syncthreads();
 
@@ -552,7 +559,12 @@ __device__ __forceinline__ void item_rounds(const SimParams& P, Smem<NCH, F>& S,
         // fixed-point scale: every contribution |w (b + A off)| <= bound -> |x| <= 2^SC_LOG2,
         // so a node sum of <= CAP contributions stays below 2^30 (no int32 overflow)
         constexpr float kFix = (float)(1 << Gm::SC_LOG2);
-        const float bm = __uint_as_float(S.maxb[0]), bpm = __uint_as_float(S.maxb[1]), bfm = __uint_as_float(S.maxb[2]);
+        const float bm = __uint_as_float(S.maxb[rpar][0]), bpm = __uint_as_float(S.maxb[rpar][1]),
+                    bfm = __uint_as_float(S.maxb[rpar][2]);
+        // the next round's slot: its last readers (round r - 1's scatter) passed
+        // round r - 1's post-scatter barrier; its next writers come after this
+        // round's post-scatter barrier
+        if (tid < 3) S.maxb[rpar ^ 1][tid] = 0u;
         const float sc_m = bm > 0.f ? kFix / bm : 0.f;
         const float sc_p = bpm > 0.f ? kFix / bpm : 0.f;
         const float sc_f = bfm > 0.f ? kFix / bfm : 0.f;
@@ -636,11 +648,11 @@ __device__ __forceinline__ void item_rounds(const SimParams& P, Smem<NCH, F>& S,
             const int gx = IC.ox - 1 + lx, gy = IC.oy - 1 + ly, gz = IC.oz - 1 + lz;
             if (gx >= 0 && gy >= 0 && gz >= 0 && gx < P.dims[0] && gy < P.dims[1] && gz < P.dims[2]) {
               const long long gi = IC.benv * P.nodes_per_env + ((long long)gz * P.dims[1] + gy) * P.dims[0] + gx;
-              atomicAdd(&P.gPM[gi], make_float4(qs[0] * (float)S.itile[0][t], qs[1] * (float)S.itile[1][t],
-                                                qs[2] * (float)S.itile[2][t], qs[3] * (float)im));
+              red_add_v4(&P.gPM[gi], qs[0] * (float)S.itile[0][t], qs[1] * (float)S.itile[1][t],
+                         qs[2] * (float)S.itile[2][t], qs[3] * (float)im);
               if (NCH == 7)
-                atomicAdd(&P.gF[gi], make_float4(qs[4] * (float)S.itile[4][t], qs[5] * (float)S.itile[5][t],
-                                                 qs[6] * (float)S.itile[6][t], 0.0f));
+                red_add_v4(&P.gF[gi], qs[4] * (float)S.itile[4][t], qs[5] * (float)S.itile[5][t],
+                           qs[6] * (float)S.itile[6][t], 0.0f);
               if (!redo)
                 P.nb_flag[IC.benv * P.blocks_per_env + ((gz / kBZ) * P.bdims[1] + gy / kBY) * P.bdims[0] + gx / kBX] = 1;
             }
@@ -648,8 +660,9 @@ __device__ __forceinline__ void item_rounds(const SimParams& P, Smem<NCH, F>& S,
 #pragma unroll
           for (int q = 0; q < NCH; ++q) S.itile[q][t] = 0;
         }
-        // no barrier here: the next round touches itile / maxb only after its
-        // post-staging barrier, and the item loop starts with one
+        // no barrier here: the next round touches itile only after its
+        // post-staging barrier (and maxb[rpar] is not written again before
+        // the round after next), and the item loop starts with one
       }
     }
 
@@ -741,6 +754,7 @@ __global__ void __launch_bounds__(kT, kCtasPerSm) k_particles(SimParams P) {
         IC.bhi[0] = hi.x; IC.bhi[1] = hi.y; IC.bhi[2] = hi.z;
       }
     }
+    if (tid < 6) (&S.maxb[0][0])[tid] = 0u;
     if (tid == 0) {
       S.penmax = 0u;
       IC.key = key; IC.benv = benv; IC.s = s; IC.e = e; IC.act = act;
