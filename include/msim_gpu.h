@@ -13,6 +13,8 @@
  *   msim_gpu_set_bodies        World::bodies + BodyMirror shapes           coupling.hpp:54-104
  *   msim_gpu_set_coupling      World::coupling (CouplingConfig)            coupling.hpp:20-26
  *   msim_gpu_sync_bodies       sync_rigid_to_soft(World&)                  coupling.hpp:106-117
+ *   msim_gpu_set_kinematic_schedule  robot_drive_step / update_link_poses   coupling.hpp:252-258
+ *                              -> Robot::set_kinematic_pose per rigid step rigid.hpp:142-151
  *   msim_gpu_soft_substep      soft_substep(st, particle_hook, grid_hook)  mpm.hpp:397-421
  *                              with penalty_particle / penalty_grid hooks  coupling.hpp:151-214
  *   msim_gpu_p2g               p2g(SoftState&)                             mpm.hpp:199-311
@@ -192,6 +194,17 @@ int msim_gpu_set_coupling(msim_gpu_ctx* ctx, const msim_coupling* coupling);
 /* sync_rigid_to_soft: overwrite body state (pose/twist) of one env and zero
  * its accumulating wrenches. */
 int msim_gpu_sync_bodies(msim_gpu_ctx* ctx, int env, const msim_body* bodies, int n_bodies);
+/* Per-rigid-step kinematic collider schedule for the NEXT msim_gpu_env_step
+ * (SURVEY.md §8f #1): poses[(r * n_total + i) * 7 + (qw qx qy qz tx ty tz)]
+ * for rigid step r < n_steps and body i of all envs concatenated in env order
+ * (n_total = msim_gpu_body_count(ctx, -1)). At rigid step r each selected body
+ * jumps to its pose and takes the finite-difference twist over the rigid step,
+ * exactly how env_step moves robot-driven links (coupling.hpp:252-258 ->
+ * Robot::set_kinematic_pose, rigid.hpp:142-151). mask[n_total] selects the
+ * bodies (NULL: every MSIM_BODY_KINEMATIC body; dynamic bodies are refused).
+ * Uploaded once per env step: the whole env step still runs without a host
+ * round trip. n_steps must equal the env step's n_rigid; consumed by it. */
+int msim_gpu_set_kinematic_schedule(msim_gpu_ctx* ctx, int n_steps, const double* poses, const uint8_t* mask);
 int msim_gpu_set_dt(msim_gpu_ctx* ctx, double dt);
 /* World::rigid_gravity (coupling.hpp:60), used by msim_gpu_env_step. */
 int msim_gpu_set_rigid_gravity(msim_gpu_ctx* ctx, const double* g3);
@@ -237,6 +250,21 @@ int msim_gpu_read_binning(msim_gpu_ctx* ctx, int env, int32_t* base, int32_t* ce
                           int64_t cell_start_cap, int32_t* cell_particles, int64_t cell_particles_cap,
                           int64_t* n_alive, int64_t* active_nodes, int64_t active_cap,
                           int64_t* n_active);
+/* The hot path's OWN integer binning (not a rebuild), for bit-exact parity
+ * with the reference's counting sort and active nodes (mpm.hpp:251-280):
+ *   - particle buckets of bucket_cells[3] base cells, bucket_dims[3] of them
+ *     per env (bucket id = (bz*bucket_dims[1] + by)*bucket_dims[0] + bx of
+ *     base / bucket_cells); counts[bucket_dims product] = particles per bucket
+ *     in the bucket structure the NEXT particle launch reads (after msim_gpu_p2g:
+ *     the histogram of the base cells that P2G binned; lost particles excluded);
+ *   - the node blocks (4x4x2 nodes; block id = (kz*block_dims[1] + ky)*
+ *     block_dims[0] + kx) the LAST P2G launch touched, ascending: exactly the
+ *     blocks holding a node of some occupied base cell's 3x3x3 stencil, i.e.
+ *     the reference's active_nodes at block granularity.
+ * Any output pointer may be NULL. */
+int msim_gpu_read_buckets(msim_gpu_ctx* ctx, int env, int32_t* bucket_cells, int32_t* bucket_dims,
+                          int32_t* counts, int64_t counts_cap, int32_t* block_dims, int32_t* blocks,
+                          int64_t blocks_cap, int64_t* n_blocks);
 int msim_gpu_read_wrenches(msim_gpu_ctx* ctx, int env, int pending, double* force,
                            double* torque);
 int msim_gpu_read_bodies(msim_gpu_ctx* ctx, int env, msim_body* bodies, int n_bodies);

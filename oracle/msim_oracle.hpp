@@ -937,6 +937,29 @@ inline void advance_scripted_body(RigidBody& b, double dt) {
   b.pose = Pose(rot_new, com_new - rot_new * b.com_offset);
 }
 
+// geometry.hpp:89-96
+inline V3 quat_log(const Quat& q_in) {
+  Quat q = q_in.normalized();
+  if (q.w < 0.0) q = Quat(-q.w, -q.x, -q.y, -q.z);
+  const double vn = q.vec().norm();
+  if (vn < 1e-14) return 2.0 * q.vec();
+  const double ang = 2.0 * std::atan2(vn, q.w);
+  return (ang / vn) * q.vec();
+}
+
+// Robot::set_kinematic_pose (rigid.hpp:142-151): a kinematic link jumps to its
+// target pose; its twist is the finite difference over the rigid step.
+inline void set_kinematic_pose(RigidBody& b, const Pose& target, double dt) {
+  if (dt > 0.0) {
+    b.linear_velocity = (target.translation - b.pose.translation) / dt;
+    b.angular_velocity = quat_log(target.rotation * b.pose.rotation.conjugate()) / dt;
+  } else {
+    b.linear_velocity = V3();
+    b.angular_velocity = V3();
+  }
+  b.pose = target;
+}
+
 // ---------------------------------------------------------------------------
 // Coupling: coupling.hpp:18-294 (bodies only; the robot/controller caller
 // part of env_step is out of scope).
@@ -973,6 +996,12 @@ struct World {  // coupling.hpp:54-118
   std::vector<BodyMirror> mirrors;
   std::vector<WrenchBuffer> wrenches, pending_wrenches;
   double mean_particle_mass = 0.0;
+  // Harness: per-rigid-step target poses of kinematic bodies for the next
+  // env_step ([step][body][qw qx qy qz tx ty tz]), applied like robot-driven
+  // links (coupling.hpp:252-258 -> rigid.hpp:142-151); consumed by one env_step.
+  std::vector<double> schedule;
+  std::vector<std::uint8_t> sched_mask;
+  int sched_steps = 0;
   double dt_rigid() const { return n_soft * soft.dt; }
   void init() {
     if (n_rigid < 1 || n_soft < 1) throw std::invalid_argument("World: n_rigid and n_soft must be >= 1");
@@ -1089,10 +1118,22 @@ inline void penalty_grid(World& w, double* max_penetration = nullptr) {
 inline StepReport env_step(World& w) {
   StepReport rep;
   const double dt_r = w.dt_rigid();
+  if (w.sched_steps > 0 && w.sched_steps != w.n_rigid)
+    throw std::invalid_argument("kinematic schedule length != n_rigid");
+  struct Consume {  // a schedule drives exactly one env step
+    World& w;
+    ~Consume() { w.sched_steps = 0; w.schedule.clear(); }
+  } consume{w};
   for (int r = 0; r < w.n_rigid; ++r) {
     for (std::size_t i = 0; i < w.bodies.size(); ++i)
       integrate_free_body(w.bodies[i], w.pending_wrenches[i], w.rigid_gravity, dt_r);
     for (std::size_t i = 0; i < w.bodies.size(); ++i) advance_scripted_body(w.bodies[i], dt_r);
+    if (w.sched_steps > 0)
+      for (std::size_t i = 0; i < w.bodies.size(); ++i) {
+        if (!w.sched_mask[i]) continue;
+        const double* p = w.schedule.data() + 7 * (std::size_t(r) * w.bodies.size() + i);
+        set_kinematic_pose(w.bodies[i], Pose(Quat(p[0], p[1], p[2], p[3]), V3(p[4], p[5], p[6])), dt_r);
+      }
     w.sync_rigid_to_soft();
     for (int s = 0; s < w.n_soft; ++s) {
       auto wrench_sum = [&] {

@@ -194,6 +194,16 @@ int oracle_sync_bodies(oracle_world* w, const msim_body* bodies, int n_bodies) {
   return MSIM_OK;
 }
 
+int oracle_set_kinematic_schedule(oracle_world* w, int n_steps, const double* poses, const uint8_t* mask) {
+  World& W = w->w;
+  const std::size_t nb = W.bodies.size();
+  W.sched_steps = n_steps;
+  W.schedule.assign(poses, poses + 7 * nb * std::size_t(n_steps));
+  W.sched_mask.assign(nb, 0);
+  for (std::size_t i = 0; i < nb; ++i) W.sched_mask[i] = mask ? mask[i] : (W.bodies[i].mode == BodyMode::Kinematic);
+  return MSIM_OK;
+}
+
 int oracle_set_coupling(oracle_world* w, const msim_coupling* c) {
   w->w.coupling.mode = static_cast<CouplingMode>(c->mode);
   w->w.coupling.r_c_factor = c->r_c_factor;

@@ -47,6 +47,7 @@ _SIGS = {
     "oracle_set_bodies": (C.c_int, [_vp, _vp, C.c_int, _vp, C.c_int]),
     "oracle_sync_bodies": (C.c_int, [_vp, _vp, C.c_int]),
     "oracle_set_coupling": (C.c_int, [_vp, _vp]),
+    "oracle_set_kinematic_schedule": (C.c_int, [_vp, C.c_int, _dp, _u8p]),
     "oracle_set_stepping": (C.c_int, [_vp, C.c_int, C.c_int, _dp]),
     "oracle_set_dt": (C.c_int, [_vp, C.c_double]),
     "oracle_set_gravity": (C.c_int, [_vp, _dp]),
@@ -95,9 +96,7 @@ _SIGS = {
 # reference-harness-only entry points (ref_capi.cpp)
 _REF_SIGS = {
     "ref_unsupported": (C.c_int, [_vp]),
-    "ref_set_kinematic_schedule": (C.c_int, [_vp, C.c_int, _dp, _u8p]),
     "ref_bench_worlds": (C.c_double, [C.POINTER(_vp), C.c_int, C.c_int, _ip]),
-    "ref_config_d_env": (_vp, [C.c_int]),
 }
 
 _lib = None
@@ -225,6 +224,16 @@ class OracleWorld:
         rep = abi.StepReport()
         self._check(self.lib.oracle_env_step(self.h, C.byref(rep)))
         return rep
+
+    def set_kinematic_schedule(self, poses, mask=None):
+        """poses[n_steps, n_bodies, 7] = (qw qx qy qz tx ty tz) per rigid step of the
+        next env step, applied with Robot::set_kinematic_pose (rigid.hpp:142-151);
+        mask selects the bodies (default: every kinematic body)."""
+        p = np.ascontiguousarray(poses, dtype=np.float64)
+        m = None if mask is None else np.ascontiguousarray(mask, dtype=np.uint8)
+        self._sched = (p, m)
+        self._check(self.lib.oracle_set_kinematic_schedule(self.h, p.shape[0], p.ctypes.data_as(_dp),
+                                                           None if m is None else m.ctypes.data_as(_u8p)))
 
     def soft_substep(self, n=1, hooks=True):
         cyc = C.c_int32()
@@ -356,14 +365,6 @@ class RefWorld(OracleWorld):
             self.lib.oracle_destroy(self.h)
             self.h = None
             raise RefUnsupported(msg)
-
-    def set_kinematic_schedule(self, poses, mask=None):
-        """poses[n_steps, n_bodies, 7] = (qw qx qy qz tx ty tz) per rigid step of the next env step."""
-        p = np.ascontiguousarray(poses, dtype=np.float64)
-        m = None if mask is None else np.ascontiguousarray(mask, dtype=np.uint8)
-        self._sched = (p, m)
-        self._check(self.lib.ref_set_kinematic_schedule(self.h, p.shape[0], p.ctypes.data_as(_dp),
-                                                        None if m is None else m.ctypes.data_as(_u8p)))
 
     def state_hash(self) -> int:
         return int(self.lib.oracle_state_hash(self.h))

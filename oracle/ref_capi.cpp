@@ -22,8 +22,6 @@
 //   * when either of those is present, the rigid/soft loop of env_step
 //     (coupling.hpp:248-293) is driven here with the same call order and the
 //     same StepReport diagnostics; otherwise msim::env_step itself runs;
-//   * the config-D world builder for the reference bench arm (SURVEY.md
-//     App. B, scenes.config_d_env), seeded with the reference's seeder.
 #include "msim/coupling.hpp"
 #include "msim/seeding.hpp"
 
@@ -507,86 +505,6 @@ int64_t ref_seed_box(ref_world* w, ref_rng* r, const double* bmin, const double*
   const std::size_t before = w->w.soft.particles.size();
   seed_particles_box(w->w.soft, v3(bmin), v3(bmax), mat, particle_volume, r->g);
   return int64_t(w->w.soft.particles.size() - before);
-}
-
-// ---- config D (scenes.config_d_env) for the bench arm ----
-// 32 x 32 x 16 firm-clay slab seeded by seed_particles_box(mt19937_64(1000 + e)),
-// velocities U(-0.1, 0.1)^3 from mt19937_64(5000 + e); even envs: a scripted
-// write stamp descending at 0.02 m/s, odd envs: two scripted pinch fingers
-// closing at 0.01 m/s. Same doubles as the Python builder (pow for the lattice
-// span, its operation order).
-ref_world* ref_config_d_env(int e) {
-  msim_soft_desc d{};
-  d.h = 0.01;
-  d.dims[0] = d.dims[1] = d.dims[2] = 32;
-  d.gravity[2] = -9.81;
-  d.dt = 2.5e-4;
-  d.cfl_factor = 0.4;
-  d.max_cfl_halvings = 4;
-  d.lost_fraction_threshold = 0.01;
-  msim_material firm{1000.0, 1e5, 0.3, 4e3, MSIM_MODEL_HENCKY_VON_MISES, 0};
-  ref_world* w = ref_create(&d, &firm, 1);
-  // through a volatile: a compile-time constant would let GCC fold std::cbrt
-  // inside seed_particles_box with MPFR (correctly rounded), one ulp away from
-  // the run-time libm cbrt every other caller (and the Python builder) gets
-  volatile double v0_runtime = kSoftClayParticleVolume;
-  const double V0 = v0_runtime;
-  const int lat[3] = {32, 32, 16};
-  double span[3], lo[3], hi[3];
-  for (int a = 0; a < 3; ++a) span[a] = (lat[a] + 0.5) * std::pow(V0, 1.0 / 3.0);
-  lo[0] = (0.32 - span[0]) / 2;
-  lo[1] = (0.32 - span[1]) / 2;
-  lo[2] = 0.021;
-  for (int a = 0; a < 3; ++a) hi[a] = lo[a] + span[a];
-  std::mt19937_64 g(1000 + e);
-  seed_particles_box(w->w.soft, v3(lo), v3(hi), 0, V0, g);
-  std::mt19937_64 gv(5000 + e);
-  for (Particle& p : w->w.soft.particles)
-    for (int a = 0; a < 3; ++a) p.v[a] = std::uniform_real_distribution<double>(-0.1, 0.1)(gv);
-  const double cx = lo[0] + span[0] / 2, cy = lo[1] + span[1] / 2, top = lo[2] + span[2];
-  std::vector<msim_body> bodies;
-  std::vector<msim_shape> shapes;
-  auto body = [](double x, double y, double z, double vx, double vy, double vz) {
-    msim_body b{};
-    b.mode = MSIM_BODY_SCRIPTED;
-    b.q[0] = 1.0;
-    b.t[0] = x; b.t[1] = y; b.t[2] = z;
-    b.v[0] = vx; b.v[1] = vy; b.v[2] = vz;
-    b.mass = 1.0;
-    b.inertia[0] = b.inertia[1] = b.inertia[2] = 1e-3;
-    return b;
-  };
-  auto box = [](int b, double hx, double hy, double hz, double mu, double kn, double kt) {
-    msim_shape s{};
-    s.type = MSIM_SHAPE_BOX;
-    s.body = b;
-    s.local_q[0] = 1.0;
-    s.params[0] = hx; s.params[1] = hy; s.params[2] = hz;
-    s.friction = mu;
-    s.k_n = kn;
-    s.k_t = kt;
-    return s;
-  };
-  if (e % 2 == 0) {
-    bodies.push_back(body(cx, cy, top + 0.008 + 0.001, 0.0, 0.0, -0.02));
-    shapes.push_back(box(0, 0.03, 0.01, 0.008, 0.3, 80.0, 0.1));
-  } else {
-    const double zc = lo[2] + span[2] / 2, off = span[0] / 2 + 0.004 + 0.001;
-    bodies.push_back(body(cx - off, cy, zc, 0.01, 0.0, 0.0));
-    bodies.push_back(body(cx + off, cy, zc, -0.01, 0.0, 0.0));
-    shapes.push_back(box(0, 0.004, 0.012, 0.018, 0.5, 20.0, 0.1));
-    shapes.push_back(box(1, 0.004, 0.012, 0.018, 0.5, 20.0, 0.1));
-  }
-  ref_set_bodies(w, bodies.data(), int(bodies.size()), shapes.data(), int(shapes.size()));
-  msim_coupling c{MSIM_COUPLING_PARTICLE, 0, 0.5, 0.05};
-  ref_set_coupling(w, &c);
-  const double rg[3] = {0.0, 0.0, -9.81};
-  ref_set_stepping(w, 25, 1, rg);
-  if (ref_init(w) != MSIM_OK) {
-    ref_destroy(w);
-    return nullptr;
-  }
-  return w;
 }
 
 }  // extern "C"

@@ -121,12 +121,12 @@ class FillResult(C.Structure):  # msim_fill_result = FillResult (scenario.hpp:55
 EXPORTED = [
     "msim_gpu_create", "msim_gpu_destroy", "msim_gpu_last_error", "msim_gpu_create_error",
     "msim_gpu_version", "msim_gpu_set_particles", "msim_gpu_write_particles",
-    "msim_gpu_set_bodies", "msim_gpu_set_coupling", "msim_gpu_sync_bodies", "msim_gpu_set_dt",
+    "msim_gpu_set_bodies", "msim_gpu_set_kinematic_schedule", "msim_gpu_set_coupling", "msim_gpu_sync_bodies", "msim_gpu_set_dt",
     "msim_gpu_set_rigid_gravity", "msim_gpu_set_gravity", "msim_gpu_set_lost_fraction_threshold",
     "msim_gpu_soft_substep", "msim_gpu_p2g", "msim_gpu_grid_update", "msim_gpu_g2p",
     "msim_gpu_env_step", "msim_gpu_particle_count", "msim_gpu_read_particles",
     "msim_gpu_read_grid", "msim_gpu_write_grid_velocity", "msim_gpu_set_split_channels",
-    "msim_gpu_set_record_binning", "msim_gpu_read_binning", "msim_gpu_read_wrenches",
+    "msim_gpu_set_record_binning", "msim_gpu_read_binning", "msim_gpu_read_buckets", "msim_gpu_read_wrenches",
     "msim_gpu_read_bodies", "msim_gpu_read_report", "msim_gpu_lost_count",
     "msim_gpu_constitutive", "msim_rng_create", "msim_rng_destroy", "msim_rng_uniform",
     "msim_rng_fill_uniform", "msim_gpu_body_count", "msim_gpu_sync_all_bodies",
@@ -171,6 +171,8 @@ _SIGS = {
     "msim_gpu_set_split_channels": (C.c_int, [_vp, C.c_int]),
     "msim_gpu_set_record_binning": (C.c_int, [_vp, C.c_int]),
     "msim_gpu_read_binning": (C.c_int, [_vp, C.c_int, _ip, _ip, C.c_int64, _ip, C.c_int64, _lp, _lp, C.c_int64, _lp]),
+    "msim_gpu_read_buckets": (C.c_int, [_vp, C.c_int, _ip, _ip, _ip, C.c_int64, _ip, _ip, C.c_int64, _lp]),
+    "msim_gpu_set_kinematic_schedule": (C.c_int, [_vp, C.c_int, _dp, _u8p]),
     "msim_gpu_read_wrenches": (C.c_int, [_vp, C.c_int, C.c_int, _dp, _dp]),
     "msim_gpu_read_bodies": (C.c_int, [_vp, C.c_int, C.POINTER(Body), C.c_int]),
     "msim_gpu_read_report": (C.c_int, [_vp, C.c_int, C.POINTER(StepReport)]),

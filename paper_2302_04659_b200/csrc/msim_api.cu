@@ -102,6 +102,14 @@ struct msim_gpu_ctx {
   std::vector<std::vector<std::vector<float>>> vol_h;
   int n_bodies = 0, n_shapes = 0;
   bool bodies_on_device = false;
+  // set_bodies edits host copies only; the device tables are rebuilt once, at
+  // the next device-side use (set_device), so configuring n envs is O(n) and
+  // never disturbs the other envs' integrated poses or staged wrenches
+  bool bodies_dirty = false;
+  std::vector<std::vector<double>> wrench_h, pending_h;  // per env, 6 per body (while dirty)
+  // kinematic pose schedule of the next env_step (msim_gpu_set_kinematic_schedule)
+  DevBuf sched_d, sched_mask_d;
+  int sched_steps = 0;
   DevBuf bodies_d, shapes_host_d, shapes_d, shape_off_d, body_off_d, vol_pool_d, wrench_d, pending_d;
 
   // per env
@@ -210,6 +218,10 @@ SimParams params(msim_gpu_ctx* c) {
   P.clear_on_read = 1;
   for (int a = 0; a < 3; ++a) P.rigid_g[a] = c->rigid_gravity[a];
   P.dt_r = d.dt;
+  P.sched = c->sched_steps ? c->sched_d.as<double>() : nullptr;
+  P.sched_mask = c->sched_steps ? c->sched_mask_d.as<unsigned char>() : nullptr;
+  P.sched_steps = c->sched_steps;
+  P.n_bodies_total = c->n_bodies;
   P.run = c->run_d.as<EnvRun>();
   P.bodies = c->bodies_d.as<BodyDev>();
   P.shape_src = c->shapes_host_d.as<ShapeHost>();
@@ -275,7 +287,15 @@ int guarded(msim_gpu_ctx* c, F&& f) {
   }
 }
 
-void set_device(msim_gpu_ctx* c) { CK(cudaSetDevice(c->device)); }
+void upload_bodies(msim_gpu_ctx* c);
+// every device-side entry point comes through here: pending body edits land first
+void set_device(msim_gpu_ctx* c) {
+  CK(cudaSetDevice(c->device));
+  if (c->bodies_dirty) {
+    c->bodies_dirty = false;
+    upload_bodies(c);
+  }
+}
 
 int fail(msim_gpu_ctx* c, int code, const std::string& msg) {
   c->err = msg;
@@ -454,8 +474,18 @@ void upload_bodies(msim_gpu_ctx* c) {
   if (!pool.empty()) CK(cudaMemcpyAsync(c->vol_pool_d.p, pool.data(), sizeof(float) * pool.size(), cudaMemcpyHostToDevice, s));
   CK(cudaMemcpyAsync(c->body_off_d.p, boff.data(), sizeof(int) * boff.size(), cudaMemcpyHostToDevice, s));
   CK(cudaMemcpyAsync(c->shape_off_d.p, soff.data(), sizeof(int) * soff.size(), cudaMemcpyHostToDevice, s));
-  CK(cudaMemsetAsync(c->wrench_d.p, 0, sizeof(double) * 6 * std::max<size_t>(bd.size(), 1), s));
-  CK(cudaMemsetAsync(c->pending_d.p, 0, sizeof(double) * 6 * std::max<size_t>(bd.size(), 1), s));
+  // staged wrenches: carried over per env (zero for envs whose bodies were just set)
+  std::vector<double> wr(6 * std::max<size_t>(bd.size(), 1), 0.0), pd(wr.size(), 0.0);
+  if (!c->wrench_h.empty())
+    for (int e = 0; e < c->n_env; ++e)
+      for (size_t k = 0; k < c->wrench_h[e].size() && k < 6 * c->bodies_h[e].size(); ++k) {
+        wr[6 * boff[e] + k] = c->wrench_h[e][k];
+        pd[6 * boff[e] + k] = c->pending_h[e][k];
+      }
+  c->wrench_h.clear();
+  c->pending_h.clear();
+  CK(cudaMemcpyAsync(c->wrench_d.p, wr.data(), sizeof(double) * wr.size(), cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(c->pending_d.p, pd.data(), sizeof(double) * pd.size(), cudaMemcpyHostToDevice, s));
   c->bodies_on_device = true;
   SimParams P = params(c);
   launch_rigid(P, 0, -1, s);
@@ -887,12 +917,56 @@ int msim_gpu_set_bodies(msim_gpu_ctx* c, int env, const msim_body* bodies, int n
       }
       vols.push_back(std::move(smp));
     }
-    set_device(c);
-    download_bodies(c);
+    if (!c->bodies_dirty) {  // snapshot the device-side body state of every env once
+      set_device(c);
+      download_bodies(c);
+      std::vector<double> wr(6 * std::max(c->n_bodies, 1)), pd(wr.size());
+      if (c->n_bodies) {
+        CK(cudaMemcpyAsync(wr.data(), c->wrench_d.p, sizeof(double) * 6 * c->n_bodies, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaMemcpyAsync(pd.data(), c->pending_d.p, sizeof(double) * 6 * c->n_bodies, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+      }
+      c->wrench_h.assign(c->n_env, {});
+      c->pending_h.assign(c->n_env, {});
+      size_t off = 0;
+      for (int e = 0; e < c->n_env; ++e) {
+        const size_t nb = c->bodies_h[e].size();
+        c->wrench_h[e].assign(wr.begin() + 6 * off, wr.begin() + 6 * (off + nb));
+        c->pending_h[e].assign(pd.begin() + 6 * off, pd.begin() + 6 * (off + nb));
+        off += nb;
+      }
+      c->bodies_dirty = true;
+    }
     c->bodies_h[env].assign(bodies, bodies + n_bodies);
     c->shapes_h[env].assign(shapes, shapes + n_shapes);
     c->vol_h[env] = std::move(vols);
-    upload_bodies(c);
+    c->wrench_h[env].assign(6 * n_bodies, 0.0);  // this env's wrenches reset (sync_rigid_to_soft)
+    c->pending_h[env].assign(6 * n_bodies, 0.0);
+    return MSIM_OK;
+  });
+}
+
+int msim_gpu_set_kinematic_schedule(msim_gpu_ctx* c, int n_steps, const double* poses, const uint8_t* mask) {
+  return guarded(c, [&]() -> int {
+    set_device(c);
+    if (n_steps < 1 || !poses) return fail(c, MSIM_ERR_INVALID, "set_kinematic_schedule: need >= 1 rigid step of poses");
+    const int nb = c->n_bodies;
+    std::vector<unsigned char> m(std::max(nb, 1), 0);
+    int k = 0;
+    for (int e = 0; e < c->n_env; ++e)
+      for (const msim_body& b : c->bodies_h[e]) {
+        m[k] = mask ? (mask[k] ? 1 : 0) : (b.mode == MSIM_BODY_KINEMATIC ? 1 : 0);
+        if (m[k] && b.mode == MSIM_BODY_DYNAMIC)
+          return fail(c, MSIM_ERR_INVALID, "set_kinematic_schedule: a dynamic body cannot follow a schedule");
+        ++k;
+      }
+    const size_t n = 7ull * nb * n_steps;
+    CK(c->sched_d.ensure(sizeof(double) * std::max<size_t>(n, 1)));
+    CK(c->sched_mask_d.ensure(m.size()));
+    if (n) CK(cudaMemcpyAsync(c->sched_d.p, poses, sizeof(double) * n, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(c->sched_mask_d.p, m.data(), m.size(), cudaMemcpyHostToDevice, c->stream));
+    CK(cudaStreamSynchronize(c->stream));  // the caller's buffer may go away
+    c->sched_steps = n_steps;
     return MSIM_OK;
   });
 }
@@ -1024,7 +1098,12 @@ int msim_gpu_env_step(msim_gpu_ctx* c, int n_rigid, int n_soft, msim_step_report
     reset_errors(c);
     CK(cudaMemsetAsync(c->max_pen_d.p, 0, sizeof(unsigned) * c->n_env, s));
     CK(cudaMemsetAsync(c->balance_d.p, 0, sizeof(double) * c->n_env, s));
+    if (c->sched_steps > 0 && c->sched_steps != n_rigid) {
+      c->sched_steps = 0;
+      return fail(c, MSIM_ERR_INVALID, "kinematic schedule length != n_rigid");
+    }
     const int rc = step_call(c, n_rigid * n_soft, c->n_bodies > 0, n_soft, nullptr);
+    c->sched_steps = 0;  // a schedule drives exactly one env step
     c->time += n_rigid * n_soft * c->desc.dt;
     if (report) {  // all envs' report words in one transfer (not one round trip per env)
       const int ne = c->n_env;
@@ -1152,6 +1231,49 @@ int msim_gpu_write_grid_velocity(msim_gpu_ctx* c, int env, const double* velocit
     CK(cudaStreamSynchronize(s));
     c->env_grid_dirty[env] = 1;  // the next clear must wipe the whole env grid
     c->grid_clean = false;
+    return MSIM_OK;
+  });
+}
+
+int msim_gpu_read_buckets(msim_gpu_ctx* c, int env, int32_t* bucket_cells, int32_t* bucket_dims, int32_t* counts,
+                          int64_t counts_cap, int32_t* block_dims, int32_t* blocks, int64_t blocks_cap,
+                          int64_t* n_blocks) {
+  return guarded(c, [&]() -> int {
+    if (env < 0 || env >= c->n_env) return fail(c, MSIM_ERR_INVALID, "read_buckets: env out of range");
+    set_device(c);
+    cudaStream_t s = c->stream;
+    const int kb[3] = {kBX, kBY, kBZ};
+    for (int a = 0; a < 3; ++a) {
+      if (bucket_cells) bucket_cells[a] = kb[a] * c->qf;
+      if (bucket_dims) bucket_dims[a] = c->qdims[a];
+      if (block_dims) block_dims[a] = c->bdims[a];
+    }
+    if (counts) {
+      if (counts_cap < c->buckets_per_env) return fail(c, MSIM_ERR_INVALID, "read_buckets: counts capacity");
+      std::vector<int> st(c->buckets_per_env + 1);
+      CK(cudaMemcpyAsync(st.data(), c->bucket_start_d[c->bset].as<int>() + (long long)env * c->buckets_per_env,
+                         sizeof(int) * (c->buckets_per_env + 1), cudaMemcpyDeviceToHost, s));
+      CK(cudaStreamSynchronize(s));
+      for (int k = 0; k < c->buckets_per_env; ++k) counts[k] = st[k + 1] - st[k];
+    }
+    if (n_blocks) {
+      int nl = 0;
+      CK(cudaMemcpyAsync(&nl, c->n_nb_d.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+      CK(cudaStreamSynchronize(s));
+      std::vector<int> list(std::max(nl, 1));
+      if (nl) CK(cudaMemcpyAsync(list.data(), c->nb_list_d.p, sizeof(int) * nl, cudaMemcpyDeviceToHost, s));
+      CK(cudaStreamSynchronize(s));
+      int64_t k = 0;
+      for (int i = 0; i < nl; ++i) {
+        if (list[i] / c->blocks_per_env != env) continue;
+        if (blocks) {
+          if (k >= blocks_cap) return fail(c, MSIM_ERR_INVALID, "read_buckets: blocks capacity");
+          blocks[k] = list[i] - env * c->blocks_per_env;
+        }
+        ++k;
+      }
+      *n_blocks = k;
+    }
     return MSIM_OK;
   });
 }
@@ -1698,16 +1820,20 @@ int msim_gpu_kernel_stats(msim_gpu_ctx* c, int id, const char** name, int64_t* l
 }
 
 int msim_gpu_body_count(const msim_gpu_ctx* c, int env) {
-  if (env < 0) return c->n_bodies;
+  if (env < 0) {
+    int n = 0;
+    for (const auto& b : c->bodies_h) n += (int)b.size();
+    return n;
+  }
   if (env >= c->n_env) return -1;
   return (int)c->bodies_h[env].size();
 }
 
 int msim_gpu_sync_all_bodies(msim_gpu_ctx* c, const msim_body* bodies, int n_total) {
   return guarded(c, [&]() -> int {
+    set_device(c);
     if (n_total != c->n_bodies) return fail(c, MSIM_ERR_INVALID, "sync_all_bodies: body count mismatch");
     if (n_total == 0) return MSIM_OK;
-    set_device(c);
     static_assert(sizeof(msim_body) == sizeof(BodyDev), "body layouts differ");
     // msim_body and BodyDev share one layout; mass/inertia/com are taken from
     // the caller like sync_rigid_to_soft copies whole bodies.
@@ -1721,8 +1847,8 @@ int msim_gpu_sync_all_bodies(msim_gpu_ctx* c, const msim_body* bodies, int n_tot
 
 int msim_gpu_read_all_wrenches(msim_gpu_ctx* c, int pending, double* wrench6) {
   return guarded(c, [&]() -> int {
-    if (c->n_bodies == 0) return MSIM_OK;
     set_device(c);
+    if (c->n_bodies == 0) return MSIM_OK;
     const void* src = pending ? c->pending_d.p : c->wrench_d.p;
     CK(cudaMemcpyAsync(wrench6, src, sizeof(double) * 6 * c->n_bodies, cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));

@@ -145,9 +145,37 @@ __device__ inline void integrate_free_body(BodyDev& b, const double* wf, const d
   advance_pose(b, dt);
 }
 
+// quat_log (geometry.hpp:89-96): axis * angle of a rotation, angle in [0, pi].
+__device__ inline void quat_log(dq q, double out[3]) {
+  const double n = sqrt(q.w * q.w + q.x * q.x + q.y * q.y + q.z * q.z);
+  q = {q.w / n, q.x / n, q.y / n, q.z / n};
+  if (q.w < 0.0) q = {-q.w, -q.x, -q.y, -q.z};
+  const double vn = sqrt(q.x * q.x + q.y * q.y + q.z * q.z);
+  const double k = vn < 1e-14 ? 2.0 : 2.0 * atan2(vn, q.w) / vn;
+  out[0] = k * q.x;
+  out[1] = k * q.y;
+  out[2] = k * q.z;
+}
+
+// Robot::set_kinematic_pose (rigid.hpp:142-151): jump to the (canonicalized)
+// target pose, twist = finite difference of the two poses over dt.
+__device__ inline void set_kinematic_pose(BodyDev& b, const double* p, double dt) {
+  const dq tq = qnormcanon({p[0], p[1], p[2], p[3]});
+  const dq rel = qmul(tq, dq{b.q[0], -b.q[1], -b.q[2], -b.q[3]});
+  double w[3];
+  quat_log(rel, w);
+  for (int k = 0; k < 3; ++k) {
+    b.v[k] = dt > 0.0 ? (p[4 + k] - b.t[k]) / dt : 0.0;
+    b.w[k] = dt > 0.0 ? w[k] / dt : 0.0;
+    b.t[k] = p[4 + k];
+  }
+  b.q[0] = tq.w; b.q[1] = tq.x; b.q[2] = tq.y; b.q[3] = tq.z;
+}
+
 // One env's rigid step: optionally integrate (dynamic: with the staged
-// wrench; scripted: constant twist), then sync_rigid_to_soft: zero the
-// accumulating wrenches and rebuild the per-shape world transforms.
+// wrench; scripted: constant twist; scheduled kinematic: the schedule's pose
+// of this rigid step), then sync_rigid_to_soft: zero the accumulating
+// wrenches and rebuild the per-shape world transforms.
 __device__ inline void rigid_env(const SimParams& P, int env, int integrate) {
   const int b0 = P.body_off[env], b1 = P.body_off[env + 1];
   for (int bi = b0; bi < b1; ++bi) {
@@ -157,6 +185,10 @@ __device__ inline void rigid_env(const SimParams& P, int env, int integrate) {
         integrate_free_body(b, P.pending + 6 * bi, P.rigid_g, P.dt_r);
       else if (b.mode == MSIM_BODY_SCRIPTED)
         advance_pose(b, P.dt_r);
+      if (P.sched_steps > 0 && P.sched_mask[bi]) {
+        const int r = min(P.run[env].rigid_idx, P.sched_steps - 1);
+        set_kinematic_pose(b, P.sched + 7 * ((long long)r * P.n_bodies_total + bi), P.dt_r);
+      }
     }
     double* wr = P.wrench + 6 * bi;
     for (int k = 0; k < 6; ++k) wr[k] = 0.0;

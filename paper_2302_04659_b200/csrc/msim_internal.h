@@ -45,6 +45,7 @@ struct EnvRun {
                        // speculated as the current cycle dt when the P2G opens a new
                        // substep, re-done on the device when the CFL plan disagrees
   int redo;            // this env's P2G must be redone with dt_c (speculation missed)
+  int rigid_idx;       // rigid step of the current env_step (kinematic schedule row)
 };
 
 // Internal error codes latched per environment (first one wins); mapped to
@@ -196,6 +197,12 @@ struct SimParams {
   int clear_on_read;         // grid update zeroes consumed P2G accumulators
   double rigid_g[3];
   double dt_r;               // n_soft * dt
+  // per-rigid-step kinematic poses ([step][body][qw qx qy qz tx ty tz], bodies of
+  // all envs concatenated) for this env_step, applied to sched_mask bodies; 0 steps: none
+  const double* sched;
+  const unsigned char* sched_mask;
+  int sched_steps;
+  int n_bodies_total;
   EnvRun* run;
   BodyDev* bodies;
   const ShapeHost* shape_src;

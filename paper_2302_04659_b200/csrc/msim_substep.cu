@@ -72,6 +72,8 @@ struct Geo {
   static constexpr int TZS = PX * PY + 4;
   static constexpr int PN = PZ * TZS;
   static constexpr int CX = QX + 2, CY = QY + 2, CZ = QZ + 2;  // P2G base cells (origin o-1)
+  // node blocks (kBX x kBY x kBZ nodes) a tile cell's stencil can touch, origin block o / kB - 1
+  static constexpr int NBX = F + 2, NBY = F + 2, NBZ = F + 3, NBT = NBX * NBY * NBZ;
   // particles per round: one trip per thread between barriers (see MSIM_KCAP)
   static constexpr int CAP = kCap;
   // fixed point: |contribution| <= 0.75^3 * 2^SC_LOG2 < 2^22 (the fix_rn range),
@@ -149,6 +151,10 @@ struct Smem {
   int itile[NCH][Geo<F>::PN];  // fixed-point node accumulators (native int shared atomics)
   float4 pay[pay_floats<NCH>() / 4][Geo<F>::CAP];  // float4 k of slot t at pay[k][t]: conflict-free
   int cellof[Geo<F>::CAP];  // local P2G cell of each staged slot, -1 if not staged
+  // node blocks of the tile touched by the staged particles' 3x3x3 stencils
+  // during the current bucket (the reference's active nodes, mpm.hpp:266-280, at
+  // block granularity); written out and cleared once per bucket
+  unsigned char bflag[Geo<F>::NBT];
   double wsum[kWs];
   unsigned penmax;
   // per-round fixed-point bounds, double-buffered by round parity: round r
@@ -489,6 +495,19 @@ __device__ __forceinline__ void item_rounds(const SimParams& P, Smem<NCH, F>& S,
               S.pay[6][t] = make_float4(Af[8], 0.f, 0.f, 0.f);
             }
             staged = true;
+            if (!redo) {  // the stencil's node blocks: nodes o - 1 + l .. o + 1 + l per axis
+              const int x0 = (lx + 3) >> 2, x1 = (lx + 5) >> 2, y0 = (ly + 3) >> 2, y1 = (ly + 5) >> 2;
+              const int z0 = (lz + 1) >> 1;
+              static_assert(kBX == 4 && kBY == 4 && kBZ == 2, "block shape");
+              unsigned char* bf = S.bflag + z0 * (Gm::NBX * Gm::NBY);
+#pragma unroll
+              for (int dz = 0; dz < 2; ++dz, bf += Gm::NBX * Gm::NBY) {  // 3 nodes span 2 z-blocks
+                bf[y0 * Gm::NBX + x0] = 1;
+                bf[y0 * Gm::NBX + x1] = 1;
+                bf[y1 * Gm::NBX + x0] = 1;
+                bf[y1 * Gm::NBX + x1] = 1;
+              }
+            }
             // bounds of |b + A off| over off in {0,1,2}^3 for the fixed-point scales
             mx_m = fmaxf(mx_m, m);
             const float a0 = fabsf(A[0]) + fabsf(A[1]) + fabsf(A[2]);
@@ -653,8 +672,6 @@ __device__ __forceinline__ void item_rounds(const SimParams& P, Smem<NCH, F>& S,
               if (NCH == 7)
                 red_add_v4(&P.gF[gi], qs[4] * (float)S.itile[4][t], qs[5] * (float)S.itile[5][t],
                            qs[6] * (float)S.itile[6][t], 0.0f);
-              if (!redo)
-                P.nb_flag[IC.benv * P.blocks_per_env + ((gz / kBZ) * P.bdims[1] + gy / kBY) * P.bdims[0] + gx / kBX] = 1;
             }
           }
 #pragma unroll
@@ -697,6 +714,7 @@ __global__ void __launch_bounds__(kT, kCtasPerSm) k_particles(SimParams P) {
   const int nitems = *P.n_active_buckets;
 
   for (int t = tid; t < NCH * PN; t += kT) (&S.itile[0][0])[t] = 0;
+  for (int t = tid; t < Gm::NBT; t += kT) S.bflag[t] = 0;
 
   volatile ItemCtx& IC = S.ic;
   // Buckets are handed out dynamically after a first static one per CTA (one
@@ -765,6 +783,14 @@ __global__ void __launch_bounds__(kT, kCtasPerSm) k_particles(SimParams P) {
     __syncthreads();
     item_rounds<NCH, F, AM>(P, S, redo);
     __syncthreads();
+    if (!redo && tid < Gm::NBT) {  // the bucket's touched node blocks (once per bucket)
+      if (S.bflag[tid]) {
+        S.bflag[tid] = 0;
+        const int kx = IC.ox / kBX - 1 + tid % Gm::NBX, ky = IC.oy / kBY - 1 + (tid / Gm::NBX) % Gm::NBY,
+                  kz = IC.oz / kBZ - 1 + tid / (Gm::NBX * Gm::NBY);
+        P.nb_flag[IC.benv * P.blocks_per_env + (kz * P.bdims[1] + ky) * P.bdims[0] + kx] = 1;
+      }
+    }
     if (tid == 0) S.next_item = (int)gridDim.x + (kDynamicItems ? atomicAdd(P.item_counter + redo, 1) : item);
     __syncthreads();
     item = S.next_item;
@@ -978,6 +1004,7 @@ __global__ void k_call_begin(SimParams P, int n_sub, int first_action) {
     r.substeps_left = 0;
     return;
   }
+  r.rigid_idx = 0;
   if (n_sub > 0 && P.integrate_rigid) rigid_env(P, env, 1);  // rigid step 0: integrate + sync
   if (n_sub > 0) plan_cycles(P, env, r);
   r.dt_g2p = 0.0f;
@@ -1012,6 +1039,7 @@ __global__ void k_iter_begin(SimParams P) {
       // next rigid step integrates with them and syncs (coupling.hpp:250-259)
       const int b0 = P.body_off[env], b1 = P.body_off[env + 1];
       for (int k = 6 * b0; k < 6 * b1; ++k) P.pending[k] = P.wrench[k];
+      r.rigid_idx += 1;
       rigid_env(P, env, 1);
     }
   }

@@ -271,29 +271,44 @@ def _bucket_shapes(body: int, half_w: float, half_h: float, wall: float, frictio
     return sh
 
 
-def config_b(material: tuple = SOFT_CLAY) -> Scene:
-    """B: 32k bed (clay parity variant by default; SAND = Drucker-Prager), 64^3,
-    scripted 5-box bucket scooping."""
+def config_b_env(e: int = 0, material: tuple = SOFT_CLAY) -> EnvSpec:
+    """One Excavate-shaped env: 40x40x20 bed, scripted 5-box bucket scooping.
+    Env e is seeded with (3 + 10 e, 4 + 10 e)."""
     lo = (0.2399, 0.2399, 0.021)
-    env = block_env(lo, (40, 40, 20), 0, material, V0_SOFT, seed=3, vel_seed=4)
+    env = block_env(lo, (40, 40, 20), 0, material, V0_SOFT, seed=3 + 10 * e, vel_seed=4 + 10 * e)
     top = lo[2] + lattice_span(20, V0_SOFT)
     bucket = BodySpec(mode=abi.BODY_SCRIPTED, t=(lo[0] + 0.04, 0.32, top + 0.02), v=(0.05, 0.0, -0.05))
     env.bodies = [bucket]
     env.shapes = _bucket_shapes(0, 0.03, 0.02, 0.004)
-    return Scene(name="B", dims=(64, 64, 64), h=0.01, dt=5e-4, envs=[env], c_d=0.05, materials=[material])
+    return env
 
 
-def config_c(material: tuple = SOFT_CLAY) -> Scene:
-    """C: 64k column (clay parity variant by default; WATER = J-only fluid),
-    128^3 h=0.005, rotating bottle + static beaker."""
+def config_b(material: tuple = SOFT_CLAY, n_envs: int = 1, first_env: int = 0) -> Scene:
+    """B: 32k bed per env (clay parity variant by default; SAND = Drucker-Prager),
+    64^3, scripted 5-box bucket scooping; n_envs batched Excavate-shaped envs."""
+    envs = [config_b_env(first_env + e, material) for e in range(n_envs)]
+    return Scene(name="B", dims=(64, 64, 64), h=0.01, dt=5e-4, envs=envs, c_d=0.05, materials=[material])
+
+
+def config_c_env(e: int = 0, material: tuple = SOFT_CLAY) -> EnvSpec:
+    """One Pour-shaped env: 40^3 column, rotating 5-box bottle + static beaker.
+    Env e is seeded with (5 + 10 e, 6 + 10 e)."""
     lo = (0.24, 0.24, 0.06)
-    env = block_env(lo, (40, 40, 40), 0, material, V0_SOFT, seed=5, vel_seed=6)
+    env = block_env(lo, (40, 40, 40), 0, material, V0_SOFT, seed=5 + 10 * e, vel_seed=6 + 10 * e)
     c = lo[0] + 0.5 * lattice_span(40, V0_SOFT)
     bottle = BodySpec(mode=abi.BODY_SCRIPTED, t=(c, c, lo[2] + 0.085), w=(0.0, 0.5, 0.0))
     beaker = BodySpec(mode=abi.BODY_KINEMATIC, t=(c + 0.2, c, 0.06))
     env.bodies = [bottle, beaker]
     env.shapes = _bucket_shapes(0, 0.09, 0.085, 0.005) + _bucket_shapes(1, 0.06, 0.04, 0.005)
-    return Scene(name="C", dims=(128, 128, 128), h=0.005, dt=5e-4, envs=[env], c_d=0.05, materials=[material])
+    return env
+
+
+def config_c(material: tuple = SOFT_CLAY, n_envs: int = 1, first_env: int = 0) -> Scene:
+    """C: 64k column per env (clay parity variant by default; WATER = J-only
+    fluid), 128^3 h=0.005, rotating bottle + static beaker; n_envs batched
+    Pour-shaped envs."""
+    envs = [config_c_env(first_env + e, material) for e in range(n_envs)]
+    return Scene(name="C", dims=(128, 128, 128), h=0.005, dt=5e-4, envs=envs, c_d=0.05, materials=[material])
 
 
 def config_d_env(e: int) -> EnvSpec:

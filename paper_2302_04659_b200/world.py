@@ -128,6 +128,15 @@ class GpuWorld:
             self.ctx, env, n, abi.dptr(x), abi.dptr(v), abi.dptr(F), abi.dptr(Cm)))
 
     # ---- stepping ----------------------------------------------------------
+    def set_kinematic_schedule(self, poses, mask=None):
+        """poses[n_steps, n_total_bodies, 7] (qw qx qy qz tx ty tz per rigid step and
+        body, all envs concatenated) for the next env_step; mask[n_total_bodies]
+        selects the bodies (default: every kinematic body). See msim_gpu.h."""
+        p = np.ascontiguousarray(poses, dtype=np.float64)
+        m = None if mask is None else np.ascontiguousarray(mask, dtype=np.uint8)
+        _check(self.lib, self.ctx, self.lib.msim_gpu_set_kinematic_schedule(
+            self.ctx, p.shape[0], abi.dptr(p), abi.u8ptr(m) if m is not None else None))
+
     def soft_substep(self, n: int = 1):
         cyc = np.zeros(self.n_env, dtype=np.int32)
         _check(self.lib, self.ctx, self.lib.msim_gpu_soft_substep(self.ctx, n, abi.iptr(cyc)))
@@ -196,6 +205,22 @@ class GpuWorld:
             self.ctx, env, abi.iptr(base), abi.iptr(cs), cs.size, abi.iptr(cp), cp.size, C.byref(n_alive),
             abi.lptr(act), act.size, C.byref(n_act)))
         return dict(base=base, cell_start=cs, cell_particles=cp[: n_alive.value], active_nodes=act[: n_act.value])
+
+    def buckets(self, env: int = 0):
+        """The hot path's own binning: bucket shape, per-bucket counts for the next
+        particle launch, and the node blocks the last P2G touched (msim_gpu_read_buckets)."""
+        cells, bdims, kdims = (np.zeros(3, np.int32) for _ in range(3))
+        _check(self.lib, self.ctx, self.lib.msim_gpu_read_buckets(
+            self.ctx, env, abi.iptr(cells), abi.iptr(bdims), None, 0, abi.iptr(kdims), None, 0, None))
+        counts = np.zeros(int(np.prod(bdims)), np.int32)
+        nblk = C.c_int64()
+        _check(self.lib, self.ctx, self.lib.msim_gpu_read_buckets(
+            self.ctx, env, None, None, abi.iptr(counts), counts.size, None, None, 0, C.byref(nblk)))
+        blocks = np.zeros(max(nblk.value, 1), np.int32)
+        _check(self.lib, self.ctx, self.lib.msim_gpu_read_buckets(
+            self.ctx, env, None, None, None, 0, None, abi.iptr(blocks), blocks.size, C.byref(nblk)))
+        return dict(bucket_cells=cells, bucket_dims=bdims, counts=counts, block_dims=kdims,
+                    blocks=blocks[: nblk.value])
 
     def wrenches(self, env: int = 0, pending: bool = False):
         nb = len(self.scene.envs[env].bodies)

@@ -16,15 +16,36 @@ def _last_json(out):
     return json.loads(out.strip().splitlines()[-1])
 
 
+# run bench.py's reference arm in-process, then list the shared objects it mapped
+_MAPS = """
+import runpy, sys
+sys.argv = ["bench.py", "--impl", "reference", "--steps", "1", "--warmup", "0"]
+try:
+    runpy.run_path("bench.py", run_name="__main__")
+except SystemExit:
+    pass
+libs = sorted({l.split()[-1] for l in open("/proc/self/maps") if l.rstrip().endswith(".so") or ".so." in l})
+print("MAPPED", [x for x in libs if "/root/repo" in x or "msim" in x or "oracle" in x])
+"""
+
+
 @pytest.mark.timeout(600)
-def test_reference_arm_line():
-    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--steps", "1",
-                        "--warmup", "1"], capture_output=True, text=True, timeout=600, cwd=ROOT)
+def test_reference_arm_line_and_no_product_loaded():
+    """The reference arm times the reference's own code and never loads the product."""
+    from oracle import oracle_py
+
+    r = subprocess.run([sys.executable, "-c", _MAPS], capture_output=True, text=True, timeout=600, cwd=ROOT)
     assert r.returncode == 0, r.stderr[-2000:]
-    d = _last_json(r.stdout)
+    lines = r.stdout.strip().splitlines()
+    d = json.loads(lines[-2])
     assert d["impl"] == "reference" and BASE_KEYS <= set(d)
-    assert d["cpu_baseline"]["kind"] == "port" and d["cpu_baseline"]["cores"] >= 1
+    kind = "reference" if oracle_py.ref_available() else "port"
+    assert d["cpu_baseline"]["kind"] == kind and d["cpu_baseline"]["cores"] >= 1
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["value"] == d["value"] > 0
+    mapped = lines[-1]
+    assert "libmsim_gpu" not in mapped and "paper_2302_04659_b200" not in mapped, mapped
+    if kind == "reference":
+        assert "libmsim_ref.so" in mapped
 
 
 @pytest.mark.gpu

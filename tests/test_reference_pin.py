@@ -164,16 +164,21 @@ def test_oracle_sdf_matches_reference_all_shape_types():
 
 
 @needs_ref
-def test_reference_config_d_builder_matches_scenes():
-    """The bench reference arm builds config D with the reference's own seeder
-    (ref_config_d_env); it must be the same world as scenes.config_d_env."""
-    from paper_2302_04659_b200.scenes import config_d
+@pytest.mark.parametrize("cfg,envs", [("A", [0]), ("B", [0, 1]), ("C", [0]), ("D", [0, 1, 2, 3])])
+def test_reference_harness_builders_match_scenes(cfg, envs):
+    """bench.py --impl reference builds its worlds in the reference harness with
+    the reference's own seeder (oracle/ref_scenes.py, no product import); they
+    must be the same worlds as the product's scenes (bit-identical)."""
+    from oracle import ref_scenes
+    from paper_2302_04659_b200 import scenes
 
+    make = {"A": lambda n: scenes.config_a(), "B": lambda n: scenes.config_b(n_envs=n),
+            "C": lambda n: scenes.config_c(n_envs=n), "D": lambda n: scenes.config_d(n)}[cfg]
+    sc = make(len(envs))
     lib = oracle_py.load_ref()
-    sc = config_d(4)
     dp = C.POINTER(C.c_double)
-    for e in range(4):
-        h = lib.ref_config_d_env(e)
+    for e in envs:
+        h = ref_scenes.build_world(cfg, e)
         n = lib.oracle_particle_count(h)
         x, v = np.zeros((n, 3)), np.zeros((n, 3))
         lib.oracle_read_particles(h, x.ctypes.data_as(dp), v.ctypes.data_as(dp), None, None, None)
@@ -183,7 +188,13 @@ def test_reference_config_d_builder_matches_scenes():
         lib.oracle_destroy(h)
         assert np.array_equal(x, sc.envs[e].x) and np.array_equal(v, sc.envs[e].v)
         for b, spec in zip(B, sc.envs[e].bodies):
-            assert tuple(b.t) == tuple(spec.t) and tuple(b.v) == tuple(spec.v) and b.mode == spec.mode
+            assert tuple(b.t) == tuple(spec.t) and tuple(b.v) == tuple(spec.v) and tuple(b.w) == tuple(spec.w)
+            assert b.mode == spec.mode and b.mass == spec.mass and tuple(b.inertia) == tuple(spec.inertia)
+        cs = [oracle_py.abi.convert(s.to_c(), oracle_py.abi.Shape) for s in sc.envs[e].shapes]
+        rs = ref_scenes._spec(cfg, e)[9]
+        assert len(cs) == len(rs)
+        for a, b in zip(cs, rs):
+            assert bytes(a) == bytes(b)
 
 
 @needs_ref
