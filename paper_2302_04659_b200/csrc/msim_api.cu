@@ -484,12 +484,13 @@ void upload_bodies(msim_gpu_ctx* c) {
       }
   c->wrench_h.clear();
   c->pending_h.clear();
-  CK(cudaMemcpyAsync(c->wrench_d.p, wr.data(), sizeof(double) * wr.size(), cudaMemcpyHostToDevice, s));
   CK(cudaMemcpyAsync(c->pending_d.p, pd.data(), sizeof(double) * pd.size(), cudaMemcpyHostToDevice, s));
   c->bodies_on_device = true;
   SimParams P = params(c);
-  launch_rigid(P, 0, -1, s);
+  launch_rigid(P, 0, -1, s);  // world transforms of every shape (zeroes the accumulating wrenches ...)
   CK(cudaGetLastError());
+  // ... which are then restored: only the re-configured envs start from zero
+  CK(cudaMemcpyAsync(c->wrench_d.p, wr.data(), sizeof(double) * wr.size(), cudaMemcpyHostToDevice, s));
   // keep host storage alive until the copies land
   CK(cudaStreamSynchronize(s));
 }
