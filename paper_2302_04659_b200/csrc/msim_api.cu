@@ -120,7 +120,7 @@ struct msim_gpu_ctx {
   // binning + grid
   int bset = 0;  // which of the two bucket-structure sets the next particle launch reads
   DevBuf bucket_start_d[2], active_buckets_d[2], n_active_d[2], perm_d[2];
-  DevBuf key_d, rank_d, bucket_count_d,
+  DevBuf key_d, rank_d, bucket_count_d, move_count_d,
       base_dbg_d;
   DevBuf gPM_d, gF_d, gV_d, nb_flag_d, nb_scan_d, nb_list_d, n_nb_d, scan_tmp_d;
   std::vector<char> env_grid_dirty;
@@ -251,6 +251,7 @@ SimParams params(msim_gpu_ctx* c) {
   P.key = c->key_d.as<int>();
   P.rank = c->rank_d.as<int>();
   P.bucket_count = c->bucket_count_d.as<int>();
+  P.move_count = c->move_count_d.as<int>();
   const int rs = c->bset, ws = 1 - c->bset;
   P.bucket_start = c->bucket_start_d[rs].as<int>();
   P.active_buckets = c->active_buckets_d[rs].as<int>();
@@ -346,6 +347,8 @@ void set_bucket_shape(msim_gpu_ctx* c, int f) {
   c->n_keys = c->n_env * c->buckets_per_env + 1;
   c->qf = f;
   CK(c->bucket_count_d.ensure(sizeof(int) * c->n_keys));
+  CK(c->move_count_d.ensure(sizeof(int) * c->n_keys));
+  CK(cudaMemset(c->move_count_d.p, 0, sizeof(int) * c->n_keys));
   for (int k = 0; k < 2; ++k) {
     CK(c->bucket_start_d[k].ensure(sizeof(int) * (c->n_keys + 1)));
     CK(c->active_buckets_d[k].ensure(sizeof(int) * c->n_keys));

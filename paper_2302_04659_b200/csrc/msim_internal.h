@@ -236,6 +236,7 @@ struct SimParams {
   int* key;
   int* rank;
   int* bucket_count;             // n_keys
+  int* move_count;               // n_keys: particles entering a bucket from another one (rank counter)
   int* bucket_start;             // n_keys + 1
   int* active_buckets;           // list
   int* n_active_buckets;

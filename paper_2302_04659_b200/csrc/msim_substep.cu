@@ -161,6 +161,9 @@ struct Smem {
   // publishes into maxb[r & 1] before its post-staging barrier while slot
   // (r + 1) & 1 is zeroed between that barrier and the post-scatter one
   unsigned maxb[2][3];
+  // per warp slot of a round: ballot of the particles staying in this bucket
+  // (order-preserving ranks), double-buffered by round parity like maxb
+  unsigned wball[2][Geo<F>::CAP / 32];
   ItemCtx ic;              // the current bucket's uniform context (read back instead of held in registers)
   int next_item;
 };
@@ -229,7 +232,7 @@ __device__ __forceinline__ void item_rounds(const SimParams& P, Smem<NCH, F>& S,
   const unsigned FULL = 0xffffffffu;
   volatile ItemCtx& IC = S.ic;
   {
-
+    int stay_base = 0;  // particles of this bucket that stay in it, so far (CTA-uniform)
     for (int r0 = IC.s, rpar = 0; r0 < IC.e; r0 += CAP, rpar ^= 1) {
       const int rn = min(CAP, IC.e - r0);
       const int trips = (rn + kT - 1) / kT;
@@ -539,15 +542,23 @@ __device__ __forceinline__ void item_rounds(const SimParams& P, Smem<NCH, F>& S,
             if (now_lost) key_new = P.n_keys - 1;
             P.key[j] = key_new;
           }
-          {  // next bucket key: warp-aggregated count
-            const unsigned am = __ballot_sync(FULL, valid);
-            if (valid) {
+          {  // next bucket key. Particles staying in this bucket keep their order: their
+             // ranks are prefix counts in slot order, set after the round's barrier. The
+             // (rare) movers take atomic ranks counted back from the end of their new bucket.
+            const bool stay = valid && key_new == IC.key;
+            const unsigned sb = __ballot_sync(FULL, stay);
+            if (lane == 0) S.wball[rpar][t >> 5] = sb;
+            const unsigned am = __ballot_sync(FULL, valid && !stay);
+            if (valid && !stay) {
               const unsigned peers = __match_any_sync(am, key_new);
               const int leader = __ffs(peers) - 1;
               int basecnt = 0;
-              if (lane == leader) basecnt = atomicAdd(&P.bucket_count[key_new], __popc(peers));
+              if (lane == leader) {
+                basecnt = atomicAdd(&P.move_count[key_new], __popc(peers));
+                atomicAdd(&P.bucket_count[key_new], __popc(peers));
+              }
               basecnt = __shfl_sync(peers, basecnt, leader);
-              P.rank[j] = basecnt + __popc(peers & ((1u << lane) - 1u));
+              P.rank[j] = -1 - (basecnt + __popc(peers & ((1u << lane) - 1u)));
             }
           }
           if (IC.do_g2p) {  // per-env max speed (bucket env-uniform): warp max -> one atomic
@@ -558,20 +569,36 @@ __device__ __forceinline__ void item_rounds(const SimParams& P, Smem<NCH, F>& S,
           }
         }
       }
-      if (!IC.do_p2g) continue;
-      // fixed-point scales of this round: |node sum| <= rn * max bound < 2^30 / scale
+      if (IC.do_p2g) {
+        // fixed-point scales of this round: |node sum| <= rn * max bound < 2^30 / scale
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        mx_m = fmaxf(mx_m, __shfl_xor_sync(FULL, mx_m, o));
-        mx_p = fmaxf(mx_p, __shfl_xor_sync(FULL, mx_p, o));
-        mx_f = fmaxf(mx_f, __shfl_xor_sync(FULL, mx_f, o));
-      }
-      if (lane == 0) {
-        atomicMax(&S.maxb[rpar][0], __float_as_uint(mx_m));
-        atomicMax(&S.maxb[rpar][1], __float_as_uint(mx_p));
-        atomicMax(&S.maxb[rpar][2], __float_as_uint(mx_f));
+        for (int o = 16; o > 0; o >>= 1) {
+          mx_m = fmaxf(mx_m, __shfl_xor_sync(FULL, mx_m, o));
+          mx_p = fmaxf(mx_p, __shfl_xor_sync(FULL, mx_p, o));
+          mx_f = fmaxf(mx_f, __shfl_xor_sync(FULL, mx_f, o));
+        }
+        if (lane == 0) {
+          atomicMax(&S.maxb[rpar][0], __float_as_uint(mx_m));
+          atomicMax(&S.maxb[rpar][1], __float_as_uint(mx_p));
+          atomicMax(&S.maxb[rpar][2], __float_as_uint(mx_f));
+        }
       }
       __syncthreads();
+      if (!redo) {  // order-preserving ranks of this round's stayers (slot order)
+        const unsigned lt = (1u << lane) - 1u;
+        int acc = 0;
+#pragma unroll
+        for (int w = 0; w < CAP / 32; ++w) {
+          const unsigned b = w * 32 < rn ? S.wball[rpar][w] : 0u;
+          for (int trip = 0; trip < trips; ++trip) {
+            const int t = trip * kT + tid;
+            if ((t >> 5) == w && ((b >> lane) & 1u)) P.rank[r0 + t] = stay_base + acc + __popc(b & lt);
+          }
+          acc += __popc(b);
+        }
+        stay_base += acc;
+      }
+      if (!IC.do_p2g) continue;
 
       // ---------------- per-thread scatter of one staged particle into the fixed-point tile
       {
@@ -656,26 +683,37 @@ __device__ __forceinline__ void item_rounds(const SimParams& P, Smem<NCH, F>& S,
         sc[0] = sc[1] = sc[2] = sc_p;
         if (NCH == 7) sc[4 % NCH] = sc[5 % NCH] = sc[6 % NCH] = sc_f;
         __syncthreads();
-        // ---------------- flush the round's node tile (vector REDs) + touched node blocks
+        // ---------------- flush the round's node tile (vector REDs)
         float qs[NCH];
 #pragma unroll
         for (int q = 0; q < NCH; ++q) qs[q] = sc[q] > 0.f ? 1.0f / sc[q] : 0.f;
-        for (int t = tid; t < PN; t += kT) {
+        // a node holds mass only if it lies in some staged particle's stencil, hence
+        // inside the grid: no bounds test; global index = tile base + local offset
+        const long long gbase = IC.benv * P.nodes_per_env +
+                                ((long long)(IC.oz - 1) * P.dims[1] + (IC.oy - 1)) * P.dims[0] + (IC.ox - 1);
+        const long long sxy = (long long)P.dims[0] * P.dims[1];
+        auto flush_node = [&](int t, long long gi) {
           const int im = S.itile[3][t];
-          if (im != 0) {  // (the 4 padding words per z-layer are never written)
-            const int lz = t / kTZS, rem = t - lz * kTZS, ly = rem / PX, lx = rem - ly * PX;
-            const int gx = IC.ox - 1 + lx, gy = IC.oy - 1 + ly, gz = IC.oz - 1 + lz;
-            if (gx >= 0 && gy >= 0 && gz >= 0 && gx < P.dims[0] && gy < P.dims[1] && gz < P.dims[2]) {
-              const long long gi = IC.benv * P.nodes_per_env + ((long long)gz * P.dims[1] + gy) * P.dims[0] + gx;
-              red_add_v4(&P.gPM[gi], qs[0] * (float)S.itile[0][t], qs[1] * (float)S.itile[1][t],
-                         qs[2] * (float)S.itile[2][t], qs[3] * (float)im);
-              if (NCH == 7)
-                red_add_v4(&P.gF[gi], qs[4] * (float)S.itile[4][t], qs[5] * (float)S.itile[5][t],
-                           qs[6] * (float)S.itile[6][t], 0.0f);
-            }
+          if (im != 0) {
+            red_add_v4(&P.gPM[gi], qs[0] * (float)S.itile[0][t], qs[1] * (float)S.itile[1][t],
+                       qs[2] * (float)S.itile[2][t], qs[3] * (float)im);
+            if (NCH == 7)
+              red_add_v4(&P.gF[gi], qs[4] * (float)S.itile[4][t], qs[5] * (float)S.itile[5][t],
+                         qs[6] * (float)S.itile[6][t], 0.0f);
           }
 #pragma unroll
           for (int q = 0; q < NCH; ++q) S.itile[q][t] = 0;
+        };
+        if constexpr (kT % (PX * PY) == 0) {  // whole z-layers per pass (F = 1: 2 layers of 8 x 8)
+          constexpr int LPP = kT / (PX * PY);
+          const int lxy = tid % (PX * PY), lx = lxy % PX, ly = lxy / PX;
+          const long long goff = (long long)ly * P.dims[0] + lx;
+          for (int lz = tid / (PX * PY); lz < PZ; lz += LPP) flush_node(lz * kTZS + lxy, gbase + lz * sxy + goff);
+        } else {
+          for (int t = tid; t < PN; t += kT) {
+            const int lz = t / kTZS, rem = t - lz * kTZS, ly = rem / PX, lx = rem - ly * PX;
+            if (lx < PX && ly < PY) flush_node(t, gbase + lz * sxy + (long long)ly * P.dims[0] + lx);
+          }
         }
         // no barrier here: the next round touches itile only after its
         // post-staging barrier (and maxb[rpar] is not written again before
@@ -683,6 +721,7 @@ __device__ __forceinline__ void item_rounds(const SimParams& P, Smem<NCH, F>& S,
       }
     }
 
+    if (!redo && tid == 0 && stay_base) atomicAdd(&P.bucket_count[IC.key], stay_base);
     if (IC.penalty && !redo) {
       const int b0 = P.body_off[IC.benv], nb = min(P.body_off[IC.benv + 1] - b0, kMaxBodiesPerEnv);
       for (int t = tid; t < nb * 6; t += kT) {
@@ -835,10 +874,15 @@ __global__ void __launch_bounds__(256) k_rebin(SimParams P) {
   P.rank[i] = basecnt + __popc(peers & ((1u << lane) - 1u));
 }
 
+// Particle i (slot of the launch that keyed it) -> its slot in the next launch:
+// stayers (rank >= 0) from the bucket's start in their old order, movers
+// (rank = -1 - r) from its end.
 __global__ void k_perm(SimParams P) {
   const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (i >= P.n) return;
-  P.perm_w[P.bucket_start_w[P.key[i]] + P.rank[i]] = (int)i;
+  const int k = P.key[i], r = P.rank[i];
+  if (r == -1) P.move_count[k] = 0;  // exactly one mover per bucket has rank -1: reset the counter
+  P.perm_w[(r >= 0 ? P.bucket_start_w[k] : P.bucket_start_w[k + 1]) + r] = (int)i;
 }
 
 // Zero the nodes touched by the last P2G (phase API: the reference clears
