@@ -247,7 +247,7 @@ def run_ours(args):
         torch.cuda.set_device(0)
 
     from paper_2302_04659_b200 import GpuWorld, abi
-    from paper_2302_04659_b200.dist import StepStats, allreduce_stats, shard, weak_first_env
+    from paper_2302_04659_b200.dist import LibStats, StepStats, allreduce_stats, rank_envs
     from paper_2302_04659_b200.scenes import SAND, SOFT_CLAY, WATER, config_a, config_b, config_c, config_d, config_e
 
     lib = abi.load()
@@ -255,12 +255,8 @@ def run_ours(args):
     cfg = args.config
     scaling = "weak"
     if cfg in ("B", "C", "D"):
-        if args.weak:
-            lo, hi = weak_first_env(args.envs, rank), weak_first_env(args.envs, rank) + args.envs
-        else:
-            lo, hi = shard(args.envs, rank, world)
-            scaling = "strong"
-        n_envs = hi - lo
+        lo, n_envs = rank_envs(args.envs, rank, world, weak=args.weak)
+        scaling = "weak" if args.weak else "strong"
         if cfg == "D":
             scene = config_d(n_envs=n_envs, first_env=lo)
             workload = WORKLOADS["D"]
@@ -303,8 +299,19 @@ def run_ours(args):
             dist.all_reduce(t, op=dist.ReduceOp.SUM)
         return float(t.item())
 
+    # the per-env-step statistics exchange: the library's device reduction + NCCL
+    # all-reduce on its stream (msim_gpu_step_stats); torch's all-reduce if NCCL
+    # cannot be resolved
+    os.environ.setdefault("NCCL_DEBUG", "WARN")  # keep NCCL's version banner off stdout (one JSON line)
+    try:
+        libstats = LibStats(lib, ctx, rank, world)
+    except RuntimeError as e:
+        libstats = None
+        print(f"[bench] library NCCL stats unavailable ({e}); torch all-reduce", file=sys.stderr)
     for _ in range(args.warmup):
         gw.env_step()
+        if libstats:
+            libstats.step()
     torch.cuda.synchronize()
 
     # ---- timed region: K env steps, device events on the library stream
@@ -320,9 +327,12 @@ def run_ours(args):
     for _ in range(args.steps):
         rep = gw.env_step()
         # per-env-step statistics exchange (the only collective)
-        st = StepStats(n_part * S, n_envs, rep.cfl_cycles, rep.lost_particles, rep.max_penetration,
-                       rep.max_force_balance_error)
-        st = allreduce_stats(st, device=dev) if world > 1 else st
+        if libstats:
+            st = libstats.step()
+        else:
+            st = StepStats(n_part * S, n_envs, rep.cfl_cycles, rep.lost_particles, rep.max_penetration,
+                           rep.max_force_balance_error)
+            st = allreduce_stats(st, device=dev) if world > 1 else st
         stats.particle_substeps += st.particle_substeps
         stats.env_steps += st.env_steps
     ev1.record(stream)
@@ -430,7 +440,9 @@ def run_ours(args):
                     "h2d_bytes_per_step": nb * C.sizeof(abi.Body), "d2h_bytes_per_step": nb * 48 + C.sizeof(rep)},
             "cpu_baseline": cpu,
             "setup_s": setup_s,
-            "stats": {"particle_substeps": stats.particle_substeps, "env_steps": stats.env_steps},
+            "stats": {"particle_substeps": stats.particle_substeps, "env_steps": stats.env_steps,
+                      "exchange": "msim_gpu_step_stats (device reduction + NCCL all-reduce on the library stream)"
+                      if libstats else "torch.distributed all_reduce"},
         }
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -279,6 +279,22 @@ int msim_gpu_sync_all_bodies(msim_gpu_ctx* ctx, const msim_body* bodies, int n_t
 /* force xyz, torque xyz per body, all envs concatenated (n_total*6 doubles). */
 int msim_gpu_read_all_wrenches(msim_gpu_ctx* ctx, int pending, double* wrench6);
 
+/* ---- multi-GPU statistics ----------------------------------
+ * One process per GPU, each context owning a contiguous range of independent
+ * envs; the only exchange is the per-env-step statistics, reduced over the
+ * context's envs on the device and all-reduced with NCCL on the context's
+ * stream (stream-ordered after the env step, capturable). NCCL is resolved
+ * at run time from the process (no link dependency).
+ *   msim_gpu_nccl_unique_id: rank 0 makes the id, the caller broadcasts it;
+ *   msim_gpu_comm_init: every rank joins (rank, world, id);
+ *   msim_gpu_step_stats: statistics of the LAST env step of this context
+ *     (allreduce = 0) or of all ranks (allreduce = 1):
+ *     sums[4] = particle-substeps, env steps, CFL cycles, lost particles;
+ *     maxs[2] = max penetration, max force-balance error. */
+int msim_gpu_nccl_unique_id(uint8_t* id128);
+int msim_gpu_comm_init(msim_gpu_ctx* ctx, int rank, int world, const uint8_t* id128);
+int msim_gpu_step_stats(msim_gpu_ctx* ctx, int allreduce, double* sums, double* maxs);
+
 /* ---- instrumentation ---------------------------------------------------- */
 void* msim_gpu_stream(msim_gpu_ctx* ctx);          /* the context's cudaStream_t */
 int64_t msim_gpu_launches(const msim_gpu_ctx* ctx);  /* kernels launched so far */

@@ -130,7 +130,7 @@ EXPORTED = [
     "msim_gpu_read_bodies", "msim_gpu_read_report", "msim_gpu_lost_count",
     "msim_gpu_constitutive", "msim_rng_create", "msim_rng_destroy", "msim_rng_uniform",
     "msim_rng_fill_uniform", "msim_gpu_body_count", "msim_gpu_sync_all_bodies",
-    "msim_gpu_read_all_wrenches", "msim_gpu_stream", "msim_gpu_launches", "msim_gpu_set_kernel_timing",
+    "msim_gpu_read_all_wrenches", "msim_gpu_nccl_unique_id", "msim_gpu_comm_init", "msim_gpu_step_stats", "msim_gpu_stream", "msim_gpu_launches", "msim_gpu_set_kernel_timing",
     "msim_gpu_kernel_count", "msim_gpu_kernel_stats",
     "msim_seed_box_count", "msim_seed_box",
     "msim_gpu_metric_fill", "msim_gpu_render_heightmap", "msim_gpu_metric_write_iou", "msim_gpu_chamfer",
@@ -173,6 +173,9 @@ _SIGS = {
     "msim_gpu_read_binning": (C.c_int, [_vp, C.c_int, _ip, _ip, C.c_int64, _ip, C.c_int64, _lp, _lp, C.c_int64, _lp]),
     "msim_gpu_read_buckets": (C.c_int, [_vp, C.c_int, _ip, _ip, _ip, C.c_int64, _ip, _ip, C.c_int64, _lp]),
     "msim_gpu_set_kinematic_schedule": (C.c_int, [_vp, C.c_int, _dp, _u8p]),
+    "msim_gpu_nccl_unique_id": (C.c_int, [_u8p]),
+    "msim_gpu_comm_init": (C.c_int, [_vp, C.c_int, C.c_int, _u8p]),
+    "msim_gpu_step_stats": (C.c_int, [_vp, C.c_int, _dp, _dp]),
     "msim_gpu_read_wrenches": (C.c_int, [_vp, C.c_int, C.c_int, _dp, _dp]),
     "msim_gpu_read_bodies": (C.c_int, [_vp, C.c_int, C.POINTER(Body), C.c_int]),
     "msim_gpu_read_report": (C.c_int, [_vp, C.c_int, C.POINTER(StepReport)]),

@@ -107,6 +107,11 @@ struct msim_gpu_ctx {
   // never disturbs the other envs' integrated poses or staged wrenches
   bool bodies_dirty = false;
   std::vector<std::vector<double>> wrench_h, pending_h;  // per env, 6 per body (while dirty)
+  // multi-GPU statistics (msim_dist.cu): NCCL communicator over the ranks, stats vector
+  void* comm = nullptr;
+  int comm_rank = 0, comm_world = 1;
+  DevBuf stats_d;
+  int last_substeps = 0;
   // kinematic pose schedule of the next env_step (msim_gpu_set_kinematic_schedule)
   DevBuf sched_d, sched_mask_d;
   int sched_steps = 0;
@@ -145,6 +150,7 @@ struct msim_gpu_ctx {
   ~msim_gpu_ctx() {
     for (auto& g : graphs)
       if (g.exec) cudaGraphExecDestroy(g.exec);
+    nccl_comm_destroy(comm);
   }
 };
 
@@ -1108,6 +1114,7 @@ int msim_gpu_env_step(msim_gpu_ctx* c, int n_rigid, int n_soft, msim_step_report
     }
     const int rc = step_call(c, n_rigid * n_soft, c->n_bodies > 0, n_soft, nullptr);
     c->sched_steps = 0;  // a schedule drives exactly one env step
+    c->last_substeps = n_rigid * n_soft;
     c->time += n_rigid * n_soft * c->desc.dt;
     if (report) {  // all envs' report words in one transfer (not one round trip per env)
       const int ne = c->n_env;
@@ -1134,6 +1141,45 @@ int msim_gpu_env_step(msim_gpu_ctx* c, int n_rigid, int n_soft, msim_step_report
       *report = agg;
     }
     return rc;
+  });
+}
+
+int msim_gpu_nccl_unique_id(uint8_t* id128) {
+  const char* e = nccl_unique_id(id128);
+  if (e) {
+    g_create_error = e;
+    return MSIM_ERR_DEVICE;
+  }
+  return MSIM_OK;
+}
+
+int msim_gpu_comm_init(msim_gpu_ctx* c, int rank, int world, const uint8_t* id128) {
+  return guarded(c, [&]() -> int {
+    if (world < 1 || rank < 0 || rank >= world) return fail(c, MSIM_ERR_INVALID, "comm_init: bad rank / world size");
+    set_device(c);
+    nccl_comm_destroy(c->comm);
+    c->comm = nullptr;
+    if (const char* e = nccl_comm_init(&c->comm, rank, world, id128)) return fail(c, MSIM_ERR_DEVICE, e);
+    c->comm_rank = rank;
+    c->comm_world = world;
+    return MSIM_OK;
+  });
+}
+
+int msim_gpu_step_stats(msim_gpu_ctx* c, int allreduce, double* sums, double* maxs) {
+  return guarded(c, [&]() -> int {
+    if (allreduce && !c->comm) return fail(c, MSIM_ERR_INVALID, "step_stats: no communicator (msim_gpu_comm_init)");
+    set_device(c);
+    CK(c->stats_d.ensure(8 * sizeof(double)));
+    if (const char* e = launch_step_stats(params(c), c->last_substeps, c->stats_d.as<double>(),
+                                          allreduce ? c->comm : nullptr, c->stream))
+      return fail(c, MSIM_ERR_DEVICE, e);
+    double h[6];
+    CK(cudaMemcpyAsync(h, c->stats_d.p, sizeof h, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    if (sums) std::memcpy(sums, h, 4 * sizeof(double));
+    if (maxs) std::memcpy(maxs, h + 4, 2 * sizeof(double));
+    return MSIM_OK;
   });
 }
 

@@ -289,6 +289,11 @@ size_t scan_tmp_ints(int n);
 // ---- hot path (msim_substep.cu)
 // Bucket keys of the stored positions (after uploads / external writes).
 void launch_rebin(const SimParams& P, cudaStream_t s);
+// msim_dist.cu: NCCL resolved at run time; each returns nullptr or an error message
+const char* nccl_unique_id(unsigned char* id128);
+const char* nccl_comm_init(void** comm, int rank, int world, const unsigned char* id128);
+void nccl_comm_destroy(void* comm);
+const char* launch_step_stats(const SimParams& P, int substeps, double* stats_d, void* comm, cudaStream_t s);
 // Zero the grid nodes touched by the last P2G (manual phases) and reset flags.
 void launch_clear(const SimParams& P, cudaStream_t s);
 // Per-env actions for the phase API (all envs, dt_c = dt).

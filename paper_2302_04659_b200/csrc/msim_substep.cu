@@ -634,6 +634,10 @@ __device__ __forceinline__ void item_rounds(const SimParams& P, Smem<NCH, F>& S,
           bspline_w(q0.z, wy);
           bspline_w(q0.w, wz);
           const float ms = q0.x * sc_m;
+          // x weights pre-scaled by the mass and momentum fixed-point factors: one
+          // FMUL per node (w sc_p) and the mass term as a single FFMA into fix_rn
+          const float wxm[3] = {wx[0] * ms, wx[1] * ms, wx[2] * ms};
+          const float wxp[3] = {wx[0] * sc_p, wx[1] * sc_p, wx[2] * sc_p};
           // b = q1.xyz; A row-major: A00 q1.w A01 q2.x A02 q2.y A10 q2.z A11 q2.w A12 q3.x A20 q3.y A21 q3.z A22 q3.w
           float4 qf4 = make_float4(0.f, 0.f, 0.f, 0.f), qf5 = qf4, qf6 = qf4;
           if constexpr (NCH == 7) {
@@ -660,15 +664,14 @@ __device__ __forceinline__ void item_rounds(const SimParams& P, Smem<NCH, F>& S,
               const int nt = (cz + dk) * kTZS + (cy + dj) * PX + cx;
 #pragma unroll kScatterDiUnroll
               for (int di = 0; di < 3; ++di) {
-                const float w = wyz * (di == 0 ? wx[0] : (di == 1 ? wx[1] : wx[2]));
-                const float wp = w * sc_p;
-                atomicAdd(&S.itile[3][nt + di], fix_rn(w * ms));
+                const float wp = wyz * (di == 0 ? wxp[0] : (di == 1 ? wxp[1] : wxp[2]));
+                atomicAdd(&S.itile[3][nt + di], fix_rn(wyz * (di == 0 ? wxm[0] : (di == 1 ? wxm[1] : wxm[2]))));
                 atomicAdd(&S.itile[0][nt + di], fix_rn(wp * rx));
                 atomicAdd(&S.itile[1][nt + di], fix_rn(wp * ry));
                 atomicAdd(&S.itile[2][nt + di], fix_rn(wp * rz));
                 rx += q1.w; ry += q2.z; rz += q3.y;  // + column 0 (A00, A10, A20)
                 if (NCH == 7) {
-                  const float wf = w * sc_f;
+                  const float wf = wyz * (di == 0 ? wx[0] : (di == 1 ? wx[1] : wx[2])) * sc_f;
                   atomicAdd(&S.itile[4 % NCH][nt + di], fix_rn(wf * fxr));
                   atomicAdd(&S.itile[5 % NCH][nt + di], fix_rn(wf * fyr));
                   atomicAdd(&S.itile[6 % NCH][nt + di], fix_rn(wf * fzr));

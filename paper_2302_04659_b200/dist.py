@@ -26,6 +26,46 @@ def weak_first_env(n_per_rank: int, rank: int) -> int:
     return rank * n_per_rank
 
 
+def rank_envs(n_envs: int, rank: int, world: int, weak: bool = False) -> tuple[int, int]:
+    """(first global env id, env count) of a rank: the contiguous shard of a fixed
+    batch of n_envs (strong scaling, bench.py's default), or n_envs of its own
+    (weak). Seeds follow the global env id, so any world size steps the same
+    per-env worlds."""
+    if weak:
+        return weak_first_env(n_envs, rank), n_envs
+    lo, hi = shard(n_envs, rank, world)
+    return lo, hi - lo
+
+
+class LibStats:
+    """The library's own statistics exchange (msim_gpu_comm_init / msim_gpu_step_stats):
+    device-side reduction + NCCL all-reduce on the context stream. The NCCL id is
+    made by rank 0 and broadcast over the torch process group (host plumbing)."""
+
+    def __init__(self, lib, ctx, rank: int, world: int):
+        import ctypes as C
+
+        import numpy as np
+
+        self.lib, self.ctx, self.C, self.np = lib, ctx, C, np
+        uid = np.zeros(128, dtype=np.uint8)
+        if rank == 0 and lib.msim_gpu_nccl_unique_id(uid.ctypes.data_as(C.POINTER(C.c_uint8))) != 0:
+            raise RuntimeError(lib.msim_gpu_create_error().decode())
+        if world > 1:
+            box = [uid.tobytes()]
+            dist.broadcast_object_list(box, src=0)
+            uid = np.frombuffer(box[0], dtype=np.uint8).copy()
+        if lib.msim_gpu_comm_init(ctx, rank, world, uid.ctypes.data_as(C.POINTER(C.c_uint8))) != 0:
+            raise RuntimeError(lib.msim_gpu_last_error(ctx).decode())
+
+    def step(self) -> StepStats:
+        sums, maxs = self.np.zeros(4), self.np.zeros(2)
+        dp = self.C.POINTER(self.C.c_double)
+        if self.lib.msim_gpu_step_stats(self.ctx, 1, sums.ctypes.data_as(dp), maxs.ctypes.data_as(dp)) != 0:
+            raise RuntimeError(self.lib.msim_gpu_last_error(self.ctx).decode())
+        return StepStats(*sums.tolist(), *maxs.tolist())
+
+
 @dataclass
 class StepStats:
     particle_substeps: float = 0.0

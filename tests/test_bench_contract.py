@@ -61,3 +61,17 @@ def test_gpu_arm_line():
     assert d["e2e"]["h2d_bytes_per_step"] > 0 and d["e2e"]["d2h_bytes_per_step"] > 0
     assert {"sm_mhz", "sm_max_mhz", "reasons"} <= set(d["clocks"])
     assert d["kernels"]["k_particles"]["launches"] > 0
+
+
+@pytest.mark.timeout(600)
+def test_launcher_relaunches_one_process_per_gpu():
+    """bench.py --gpus 2 relaunches itself under torch.distributed.run (the
+    driver's N > 1 launch); on the reference arm rank 0 alone prints the line
+    and rank 1 exits 0 without work."""
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--gpus", "2",
+                        "--steps", "1", "--warmup", "0"], capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["impl"] == "reference" and d["n_gpus"] == 2
