@@ -305,7 +305,7 @@ def run_ours(args):
     os.environ.setdefault("NCCL_DEBUG", "WARN")  # keep NCCL's version banner off stdout (one JSON line)
     try:
         libstats = LibStats(lib, ctx, rank, world)
-    except RuntimeError as e:
+    except (RuntimeError, AttributeError) as e:
         libstats = None
         print(f"[bench] library NCCL stats unavailable ({e}); torch all-reduce", file=sys.stderr)
     for _ in range(args.warmup):

@@ -211,6 +211,17 @@ int msim_gpu_set_rigid_gravity(msim_gpu_ctx* ctx, const double* g3);
 int msim_gpu_set_gravity(msim_gpu_ctx* ctx, const double* g3);
 int msim_gpu_set_lost_fraction_threshold(msim_gpu_ctx* ctx, double threshold);
 
+/* Deterministic mode (the reference's contract that results do not depend on
+ * scheduling, mpm.hpp:7-8): with on = 1, repeated runs from the
+ * same inputs give bit-identical particles, grid, wrenches and reports. Every
+ * order-dependent float sum becomes an integer sum (int64 fixed point for the
+ * grid at per-env exponents fixed per launch, and for the wrenches), and the
+ * particle order is kept canonical (stayers in order, movers sorted). Covers
+ * env_step / soft_substep in particle coupling mode; costs extra grid traffic.
+ * A contribution that outgrows the launch's fixed-point range (~2^15 x the
+ * previous launch's largest) reports MSIM_ERR_DIVERGED. */
+int msim_gpu_set_deterministic(msim_gpu_ctx* ctx, int on);
+
 /* ---- stepping ----------------------------------------------------------- */
 /* n_substeps x soft_substep with the configured penalty hook, all envs.
  * cycles_out (may be NULL) receives the per-env cycle count of the LAST substep. */

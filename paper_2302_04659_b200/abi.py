@@ -121,7 +121,7 @@ class FillResult(C.Structure):  # msim_fill_result = FillResult (scenario.hpp:55
 EXPORTED = [
     "msim_gpu_create", "msim_gpu_destroy", "msim_gpu_last_error", "msim_gpu_create_error",
     "msim_gpu_version", "msim_gpu_set_particles", "msim_gpu_write_particles",
-    "msim_gpu_set_bodies", "msim_gpu_set_kinematic_schedule", "msim_gpu_set_coupling", "msim_gpu_sync_bodies", "msim_gpu_set_dt",
+    "msim_gpu_set_bodies", "msim_gpu_set_kinematic_schedule", "msim_gpu_set_deterministic", "msim_gpu_set_coupling", "msim_gpu_sync_bodies", "msim_gpu_set_dt",
     "msim_gpu_set_rigid_gravity", "msim_gpu_set_gravity", "msim_gpu_set_lost_fraction_threshold",
     "msim_gpu_soft_substep", "msim_gpu_p2g", "msim_gpu_grid_update", "msim_gpu_g2p",
     "msim_gpu_env_step", "msim_gpu_particle_count", "msim_gpu_read_particles",
@@ -174,6 +174,7 @@ _SIGS = {
     "msim_gpu_read_buckets": (C.c_int, [_vp, C.c_int, _ip, _ip, _ip, C.c_int64, _ip, _ip, C.c_int64, _lp]),
     "msim_gpu_set_kinematic_schedule": (C.c_int, [_vp, C.c_int, _dp, _u8p]),
     "msim_gpu_nccl_unique_id": (C.c_int, [_u8p]),
+    "msim_gpu_set_deterministic": (C.c_int, [_vp, C.c_int]),
     "msim_gpu_comm_init": (C.c_int, [_vp, C.c_int, C.c_int, _u8p]),
     "msim_gpu_step_stats": (C.c_int, [_vp, C.c_int, _dp, _dp]),
     "msim_gpu_read_wrenches": (C.c_int, [_vp, C.c_int, C.c_int, _dp, _dp]),
@@ -223,8 +224,11 @@ def load(path: str | None = None) -> C.CDLL:
             f"{path} not found: build the CUDA library first (python -c 'import __graft_entry__ as g; g.build()')"
         )
     lib = C.CDLL(path)
+    override = "MSIM_GPU_LIB" in os.environ  # an older profiling build may lack newer entry points
     for name, (res, args) in _SIGS.items():
-        fn = getattr(lib, name)
+        fn = getattr(lib, name, None) if override else getattr(lib, name)
+        if fn is None:
+            continue
         fn.restype = res
         fn.argtypes = args
     _lib = lib

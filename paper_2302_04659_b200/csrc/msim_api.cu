@@ -107,6 +107,9 @@ struct msim_gpu_ctx {
   // never disturbs the other envs' integrated poses or staged wrenches
   bool bodies_dirty = false;
   std::vector<std::vector<double>> wrench_h, pending_h;  // per env, 6 per body (while dirty)
+  // deterministic mode (msim_gpu_set_deterministic)
+  int det = 0;
+  DevBuf gPMd_d, w64_d, a64_d, r64_d, det_bnd_d, det_mexp_d;
   // multi-GPU statistics (msim_dist.cu): NCCL communicator over the ranks, stats vector
   void* comm = nullptr;
   int comm_rank = 0, comm_world = 1;
@@ -254,6 +257,13 @@ SimParams params(msim_gpu_ctx* c) {
   P.err_code = c->err_code_d.as<int>();
   P.err_pid = c->err_pid_d.as<int>();
   P.mean_mass = c->mean_mass_d.as<double>();
+  P.det = c->det;
+  P.gPMd = c->det ? c->gPMd_d.as<longlong4>() : nullptr;
+  P.w64 = c->w64_d.as<long long>();
+  P.a64 = c->a64_d.as<long long>();
+  P.r64 = c->r64_d.as<long long>();
+  P.det_bnd = c->det_bnd_d.as<unsigned>();
+  P.det_mexp = c->det_mexp_d.as<int>();
   P.key = c->key_d.as<int>();
   P.rank = c->rank_d.as<int>();
   P.bucket_count = c->bucket_count_d.as<int>();
@@ -388,6 +398,8 @@ int collect_errors(msim_gpu_ctx* c) {
         return fail(c, MSIM_ERR_DIVERGED, "lost particle fraction exceeds threshold" + where);
       case kErrCfl:
         return fail(c, MSIM_ERR_DIVERGED, "CFL violation persists after max substep halvings" + where);
+      case kErrDetRange:
+        return fail(c, MSIM_ERR_DIVERGED, "deterministic fixed-point range exceeded" + where);
       case kErrNan:
         return fail(c, MSIM_ERR_DIVERGED, "NaN/Inf in particle " + std::to_string(local) + where);
       default:
@@ -478,6 +490,8 @@ void upload_bodies(msim_gpu_ctx* c) {
   CK(c->vol_pool_d.ensure(sizeof(float) * std::max<size_t>(pool.size(), 1)));
   CK(c->wrench_d.ensure(sizeof(double) * 6 * std::max<size_t>(bd.size(), 1)));
   CK(c->pending_d.ensure(sizeof(double) * 6 * std::max<size_t>(bd.size(), 1)));
+  CK(c->w64_d.ensure(sizeof(long long) * 6 * std::max<size_t>(bd.size(), 1)));
+  CK(cudaMemsetAsync(c->w64_d.p, 0, sizeof(long long) * 6 * std::max<size_t>(bd.size(), 1), c->stream));
   if (!bd.empty()) CK(cudaMemcpyAsync(c->bodies_d.p, bd.data(), sizeof(BodyDev) * bd.size(), cudaMemcpyHostToDevice, s));
   if (!sh.empty()) CK(cudaMemcpyAsync(c->shapes_host_d.p, sh.data(), sizeof(ShapeHost) * sh.size(), cudaMemcpyHostToDevice, s));
   if (!pool.empty()) CK(cudaMemcpyAsync(c->vol_pool_d.p, pool.data(), sizeof(float) * pool.size(), cudaMemcpyHostToDevice, s));
@@ -723,6 +737,10 @@ int msim_gpu_create(const msim_soft_desc* desc, const msim_material* materials, 
     per_env(c->err_pid_d, sizeof(int));
     per_env(c->balance_d, sizeof(double));
     per_env(c->mean_mass_d, sizeof(double));
+    per_env(c->a64_d, 3 * sizeof(long long));
+    per_env(c->r64_d, 3 * sizeof(long long));
+    per_env(c->det_bnd_d, sizeof(unsigned));
+    per_env(c->det_mexp_d, sizeof(int));
     CK(cudaMemset(c->err_pid_d.p, 0x7f, sizeof(int) * n_env));
     CK(c->env_off_d.ensure(sizeof(long long) * (n_env + 1)));
     CK(cudaMemset(c->env_off_d.p, 0, sizeof(long long) * (n_env + 1)));
@@ -826,6 +844,14 @@ int msim_gpu_set_particles(msim_gpu_ctx* c, int64_t n, const int64_t* env_offset
       c->mean_mass_h[e] = ne > 0 ? msum / (double)ne : 0.0;  // World::init (coupling.hpp:97-99)
     }
     CK(cudaMemcpyAsync(c->mean_mass_d.p, c->mean_mass_h.data(), sizeof(double) * c->n_env, cudaMemcpyHostToDevice, s));
+    {  // deterministic mode: node mass sums <= the env's mass < 2^58 units
+      std::vector<int> mexp(c->n_env);
+      for (int e = 0; e < c->n_env; ++e) {
+        const double M = c->mean_mass_h[e] * (double)(env_offsets[e + 1] - env_offsets[e]);
+        mexp[e] = M > 0.0 ? 58 - (int)std::ceil(std::log2(M)) : 58;
+      }
+      CK(cudaMemcpy(c->det_mexp_d.p, mexp.data(), sizeof(int) * c->n_env, cudaMemcpyHostToDevice));
+    }
     if (n > 0) {
       // stage doubles on the device in chunks, convert to fp32 SoA
       const long long chunk = 1 << 20;
@@ -956,6 +982,27 @@ int msim_gpu_set_bodies(msim_gpu_ctx* c, int env, const msim_body* bodies, int n
   });
 }
 
+int msim_gpu_set_deterministic(msim_gpu_ctx* c, int on) {
+  return guarded(c, [&]() -> int {
+    set_device(c);
+    on = on ? 1 : 0;
+    if (on == c->det) return MSIM_OK;
+    if (on) {
+      const size_t nodes = (size_t)c->nodes_per_env * c->n_env;
+      CK(c->gPMd_d.ensure(sizeof(longlong4) * std::max<size_t>(nodes, 1)));
+      CK(cudaMemsetAsync(c->gPMd_d.p, 0, sizeof(longlong4) * std::max<size_t>(nodes, 1), c->stream));
+      CK(cudaMemsetAsync(c->det_bnd_d.p, 0, sizeof(unsigned) * c->n_env, c->stream));
+      CK(cudaMemsetAsync(c->a64_d.p, 0, 3 * sizeof(long long) * c->n_env, c->stream));
+      CK(cudaMemsetAsync(c->r64_d.p, 0, 3 * sizeof(long long) * c->n_env, c->stream));
+      CK(cudaMemsetAsync(c->w64_d.p, 0, 6 * sizeof(long long) * std::max(c->n_bodies, 1), c->stream));
+      CK(cudaStreamSynchronize(c->stream));
+    }
+    c->det = on;
+    c->perm_valid = false;  // re-bin: the deterministic particle order starts from the upload order
+    return MSIM_OK;
+  });
+}
+
 int msim_gpu_set_kinematic_schedule(msim_gpu_ctx* c, int n_steps, const double* poses, const uint8_t* mask) {
   return guarded(c, [&]() -> int {
     set_device(c);
@@ -1047,8 +1094,15 @@ int msim_gpu_set_record_binning(msim_gpu_ctx* c, int on) {
   });
 }
 
+static int det_mode_check(msim_gpu_ctx* c) {
+  if (c->det && split_mode(c))
+    return fail(c, MSIM_ERR_INVALID, "deterministic mode covers particle coupling (no grid coupling / split channels)");
+  return MSIM_OK;
+}
+
 int msim_gpu_soft_substep(msim_gpu_ctx* c, int n_substeps, int32_t* cycles_out) {
   return guarded(c, [&]() -> int {
+    if (const int rc = det_mode_check(c)) return rc;
     set_device(c);
     reset_errors(c);
     return step_call(c, n_substeps, false, 1, cycles_out);
@@ -1059,6 +1113,7 @@ int msim_gpu_soft_substep(msim_gpu_ctx* c, int n_substeps, int32_t* cycles_out) 
 // per phase with every env active, dt_c = dt, momentum and force kept apart.
 static int manual_phase(msim_gpu_ctx* c, int which) {
   return guarded(c, [&]() -> int {
+    if (c->det) return fail(c, MSIM_ERR_INVALID, "deterministic mode covers env_step / soft_substep (not the phase API)");
     set_device(c);
     reset_errors(c);
     if (c->n == 0) return MSIM_OK;
@@ -1103,6 +1158,7 @@ int msim_gpu_g2p(msim_gpu_ctx* c) { return manual_phase(c, 2); }
 int msim_gpu_env_step(msim_gpu_ctx* c, int n_rigid, int n_soft, msim_step_report* report) {
   return guarded(c, [&]() -> int {
     if (n_rigid < 1 || n_soft < 1) return fail(c, MSIM_ERR_INVALID, "World: n_rigid and n_soft must be >= 1");
+    if (const int rc = det_mode_check(c)) return rc;
     set_device(c);
     cudaStream_t s = c->stream;
     reset_errors(c);

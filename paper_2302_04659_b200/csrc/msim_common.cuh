@@ -192,6 +192,8 @@ __device__ inline void rigid_env(const SimParams& P, int env, int integrate) {
     }
     double* wr = P.wrench + 6 * bi;
     for (int k = 0; k < 6; ++k) wr[k] = 0.0;
+    if (P.det)
+      for (int k = 0; k < 6; ++k) P.w64[6 * bi + k] = 0;
   }
   const int s0 = P.shape_off[env], s1 = P.shape_off[env + 1];
   for (int si = s0; si < s1; ++si) {
@@ -266,7 +268,8 @@ __device__ inline void rigid_env(const SimParams& P, int env, int integrate) {
 
 // Particle leaving the domain this cycle: its penalty reaction still counts
 // (the hook runs before p2g's loss detection, coupling.hpp:266-274).
-static __device__ MSIM_COLD void penalty_reaction_only(const SimParams& P, int env, f3 x, f3 v) {
+template <bool DET>
+__device__ MSIM_COLD void penalty_reaction_only(const SimParams& P, int env, f3 x, f3 v) {
   const int s0 = P.shape_off[env], s1 = P.shape_off[env + 1];
   const int b0 = P.body_off[env];
   for (int s = s0; s < s1; ++s) {
@@ -276,17 +279,28 @@ static __device__ MSIM_COLD void penalty_reaction_only(const SimParams& P, int e
     if (!msim_dev::penalty_force(sh, P.vol_pool, x, v, P.r_c_particle, P.c_d, f, pen)) continue;
     f3 com = {sh.com[0], sh.com[1], sh.com[2]};
     f3 tq = msim_dev::cross(x - com, f3{-f.x, -f.y, -f.z});
-    double* wr = P.wrench + 6 * (b0 + sh.body);
-    atomicAdd(wr + 0, -(double)f.x);
-    atomicAdd(wr + 1, -(double)f.y);
-    atomicAdd(wr + 2, -(double)f.z);
-    atomicAdd(wr + 3, (double)tq.x);
-    atomicAdd(wr + 4, (double)tq.y);
-    atomicAdd(wr + 5, (double)tq.z);
-    for (int k = 0; k < 3; ++k) {
-      double fk = k == 0 ? f.x : (k == 1 ? f.y : f.z);
-      atomicAdd(P.applied + 3 * env + k, fk);
-      atomicAdd(P.react + 3 * env + k, -fk);
+    if constexpr (DET) {  // integer sums (deterministic mode)
+      const double r6[6] = {-(double)f.x, -(double)f.y, -(double)f.z, (double)tq.x, (double)tq.y, (double)tq.z};
+      unsigned long long* w = reinterpret_cast<unsigned long long*>(P.w64 + 6 * (b0 + sh.body));
+      for (int k = 0; k < 6; ++k) atomicAdd(w + k, (unsigned long long)__double2ll_rn(ldexp(r6[k], kDetWrenchExp)));
+      for (int k = 0; k < 3; ++k) {
+        const long long rk = __double2ll_rn(ldexp(r6[k], kDetWrenchExp));
+        atomicAdd(reinterpret_cast<unsigned long long*>(P.r64 + 3 * env + k), (unsigned long long)rk);
+        atomicAdd(reinterpret_cast<unsigned long long*>(P.a64 + 3 * env + k), (unsigned long long)(-rk));
+      }
+    } else {
+      double* wr = P.wrench + 6 * (b0 + sh.body);
+      atomicAdd(wr + 0, -(double)f.x);
+      atomicAdd(wr + 1, -(double)f.y);
+      atomicAdd(wr + 2, -(double)f.z);
+      atomicAdd(wr + 3, (double)tq.x);
+      atomicAdd(wr + 4, (double)tq.y);
+      atomicAdd(wr + 5, (double)tq.z);
+      for (int k = 0; k < 3; ++k) {
+        double fk = k == 0 ? f.x : (k == 1 ? f.y : f.z);
+        atomicAdd(P.applied + 3 * env + k, fk);
+        atomicAdd(P.react + 3 * env + k, -fk);
+      }
     }
     float_bits_max(&P.max_pen_bits[env], pen);
   }

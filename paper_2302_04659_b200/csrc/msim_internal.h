@@ -46,7 +46,17 @@ struct EnvRun {
                        // substep, re-done on the device when the CFL plan disagrees
   int redo;            // this env's P2G must be redone with dt_c (speculation missed)
   int rigid_idx;       // rigid step of the current env_step (kinematic schedule row)
+  int det_sm, det_sp;  // deterministic mode: fixed-point exponents of this launch's grid mass / momentum
 };
+
+// Deterministic mode (msim_gpu_set_deterministic): every order-dependent float
+// sum becomes an integer sum. Grid nodes accumulate int64 fixed point at a
+// per-env exponent fixed for the launch; wrench / force-balance sums int64 at
+// 2^kDetWrenchExp per N (N m). Particle order: movers sorted by their previous
+// slot after k_perm (stayers keep their order by construction).
+constexpr int kDetWrenchExp = 36;
+constexpr int kDetMomentumExp = 40;  // |largest round bound| ~ 2^-40 of the int64 range per contribution
+constexpr int kErrDetRange = 33;     // deterministic fixed-point range exceeded (a contribution grew ~2^15x in one step)
 
 // Internal error codes latched per environment (first one wins); mapped to
 // MSIM_ERR_INVALID / MSIM_ERR_DIVERGED with the reference's messages.
@@ -257,6 +267,14 @@ struct SimParams {
   int* n_nb;
 
   int* scan_tmp;
+  // deterministic mode (null otherwise)
+  int det;
+  longlong4* gPMd;               // per node: int64 momentum (or p + dt f) xyz, mass
+  long long* w64;                // per body x 6: wrench accumulators at 2^kDetWrenchExp
+  long long* a64;                // per env x 3: applied force this cycle
+  long long* r64;                // per env x 3: reactions this cycle
+  unsigned* det_bnd;             // per env: max momentum-channel round bound of the last launch (float bits)
+  const int* det_mexp;           // per env: mass exponent (from the env's total mass)
   double* balance_max;           // per env: max force-balance error this step
   double lost_threshold;
 };

@@ -328,6 +328,7 @@ __global__ void k_clear_env_grid(SimParams P, int env) {
     P.gPM[gi] = z;
     if (P.gF) P.gF[gi] = z;
     P.gV[gi] = z;
+    if (P.det) P.gPMd[gi] = make_longlong4(0, 0, 0, 0);
   }
   if (t < P.blocks_per_env) P.nb_flag[env * P.blocks_per_env + t] = 0;
 }

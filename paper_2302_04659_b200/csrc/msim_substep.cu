@@ -191,6 +191,13 @@ constexpr SpreadTable make_spread() {
 }
 __constant__ SpreadTable kSpread = make_spread();
 
+// Deterministic mode: integer fixed-point accumulation (commutative, so the
+// result does not depend on the order CTAs / warps add in).
+__device__ __forceinline__ void red_add_i64(long long* a, long long v) {
+  asm volatile("red.global.add.u64 [%0], %1;" ::"l"(a), "l"(v) : "memory");
+}
+__device__ __forceinline__ long long det_fix(double v, int e) { return __double2ll_rn(ldexp(v, e)); }
+
 // Round-to-nearest float -> int for |x| < 2^22 with one FFMA-able add: the
 // integer lands in the low mantissa bits of x + 1.5 * 2^23 (avoids F2I).
 __device__ __forceinline__ int fix_rn(float x) { return __float_as_int(x + 12582912.0f) - 0x4B400000; }
@@ -202,7 +209,7 @@ __device__ __forceinline__ void red_add_v4(float4* a, float x, float y, float z,
 
 // Global-memory scatter of one particle (fallback when its stencil leaves the
 // bucket's P2G tile, e.g. a particle faster than the CFL bound assumed).
-template <int NCH>
+template <int NCH, bool DET>
 __device__ MSIM_COLD void scatter_global(const SimParams& P, int env, const int* b, const float* w9, float m, f3 bp,
                                const float* Ap, f3 bf, const float* Af, bool mark) {
   for (int dk = 0; dk < 3; ++dk)
@@ -213,7 +220,16 @@ __device__ MSIM_COLD void scatter_global(const SimParams& P, int env, const int*
                        bp.z + Ap[6] * di + Ap[7] * dj + Ap[8] * dk};
         const int gx = b[0] + di, gy = b[1] + dj, gz = b[2] + dk;
         const long long gi = env * P.nodes_per_env + ((long long)gz * P.dims[1] + gy) * P.dims[0] + gx;
-        red_add_v4(&P.gPM[gi], w * pq.x, w * pq.y, w * pq.z, w * m);
+        if constexpr (DET) {
+          const int sm = P.run[env].det_sm, sp = P.run[env].det_sp;
+          long long* g = &P.gPMd[gi].x;
+          red_add_i64(g + 0, det_fix((double)(w * pq.x), sp));
+          red_add_i64(g + 1, det_fix((double)(w * pq.y), sp));
+          red_add_i64(g + 2, det_fix((double)(w * pq.z), sp));
+          red_add_i64(g + 3, det_fix((double)(w * m), sm));
+        } else {
+          red_add_v4(&P.gPM[gi], w * pq.x, w * pq.y, w * pq.z, w * m);
+        }
         if (NCH == 7) {
           const f3 fq = {bf.x + Af[0] * di + Af[1] * dj + Af[2] * dk, bf.y + Af[3] * di + Af[4] * dj + Af[5] * dk,
                          bf.z + Af[6] * di + Af[7] * dj + Af[8] * dk};
@@ -225,7 +241,7 @@ __device__ MSIM_COLD void scatter_global(const SimParams& P, int env, const int*
 
 // The rounds of one bucket (<= kCap particles each): per-particle phase, then
 // the fixed-point scatter and flush. Bucket-uniform values come from S.ic.
-template <int NCH, int F, bool AM>
+template <int NCH, int F, bool AM, bool DET>
 __device__ __forceinline__ void item_rounds(const SimParams& P, Smem<NCH, F>& S, bool redo) {
   MSIM_GEO_ALIASES(F)
   const int tid = threadIdx.x, lane = tid & 31;
@@ -399,7 +415,7 @@ __device__ __forceinline__ void item_rounds(const SimParams& P, Smem<NCH, F>& S,
           } else if (p2g_here) {
             // leaves the domain now: reaction-only IC.penalty, freeze, count (mpm.hpp:239-245)
             if (!redo) {
-              if (P.hooks && !P.grid_mode && P.shape_off[penv + 1] > P.shape_off[penv]) penalty_reaction_only(P, penv, x, v);
+              if (P.hooks && !P.grid_mode && P.shape_off[penv + 1] > P.shape_off[penv]) penalty_reaction_only<DET>(P, penv, x, v);
               atomicAdd((unsigned long long*)&P.lost_count[penv], 1ull);
             }
             meta |= 1u << kLostBit;
@@ -443,11 +459,23 @@ __device__ __forceinline__ void item_rounds(const SimParams& P, Smem<NCH, F>& S,
 #pragma unroll
               for (int o = 16; o > 0; o >>= 1) pb = max(pb, __shfl_xor_sync(FULL, pb, o));
               if (lane == 0) {
-                double* ws = S.wsum + 6 * min(sh.body, kMaxBodiesPerEnv - 1);
+                if constexpr (DET) {  // warp sums are deterministic; integer totals
+                  long long* w = P.w64 + 6 * (P.body_off[IC.benv] + sh.body);
 #pragma unroll
-                for (int k = 0; k < 6; ++k) atomicAdd(ws + k, (double)r6[k]);
+                  for (int k = 0; k < 6; ++k) red_add_i64(w + k, det_fix((double)r6[k], kDetWrenchExp));
 #pragma unroll
-                for (int k = 0; k < 3; ++k) atomicAdd(S.wsum + 6 * kMaxBodiesPerEnv + k, -(double)r6[k]);
+                  for (int k = 0; k < 3; ++k) {
+                    const long long rk = det_fix((double)r6[k], kDetWrenchExp);
+                    red_add_i64(P.r64 + 3 * IC.benv + k, rk);
+                    red_add_i64(P.a64 + 3 * IC.benv + k, -rk);
+                  }
+                } else {
+                  double* ws = S.wsum + 6 * min(sh.body, kMaxBodiesPerEnv - 1);
+#pragma unroll
+                  for (int k = 0; k < 6; ++k) atomicAdd(ws + k, (double)r6[k]);
+#pragma unroll
+                  for (int k = 0; k < 3; ++k) atomicAdd(S.wsum + 6 * kMaxBodiesPerEnv + k, -(double)r6[k]);
+                }
                 atomicMax(&S.penmax, pb);
               }
             }
@@ -524,7 +552,7 @@ __device__ __forceinline__ void item_rounds(const SimParams& P, Smem<NCH, F>& S,
               mx_f = fmaxf(mx_f, fmaxf(fabsf(bf.x) + 2.f * f0, fmaxf(fabsf(bf.y) + 2.f * f1, fabsf(bf.z) + 2.f * f2)));
             }
           } else {
-            scatter_global<NCH>(P, penv, b2, w9, m, bb, A, bf, Af, !redo);
+            scatter_global<NCH, DET>(P, penv, b2, w9, m, bb, A, bf, Af, !redo);
           }
         }
         if (t < CAP) S.cellof[t] = staged ? cell : -1;
@@ -611,9 +639,25 @@ __device__ __forceinline__ void item_rounds(const SimParams& P, Smem<NCH, F>& S,
         // round r - 1's post-scatter barrier; its next writers come after this
         // round's post-scatter barrier
         if (tid < 3) S.maxb[rpar ^ 1][tid] = 0u;
-        const float sc_m = bm > 0.f ? kFix / bm : 0.f;
-        const float sc_p = bpm > 0.f ? kFix / bpm : 0.f;
+        float sc_m = bm > 0.f ? kFix / bm : 0.f;
+        float sc_p = bpm > 0.f ? kFix / bpm : 0.f;
         const float sc_f = bfm > 0.f ? kFix / bfm : 0.f;
+        int dsh_m = 0, dsh_p = 0;  // DET: shift from the round's scale 2^e to the launch's 2^S
+        if constexpr (DET) {
+          // power-of-two round scales: the round's integer sums convert exactly
+          const int em = sc_m > 0.f ? ilogbf(sc_m) : 0, ep = sc_p > 0.f ? ilogbf(sc_p) : 0;
+          sc_m = sc_m > 0.f ? ldexpf(1.0f, em) : 0.f;
+          sc_p = sc_p > 0.f ? ldexpf(1.0f, ep) : 0.f;
+          const EnvRun& er = P.run[IC.benv];
+          dsh_m = er.det_sm - em;
+          dsh_p = er.det_sp - ep;
+          if (!redo && tid == 0) {
+            atomicMax(&P.det_bnd[IC.benv], __float_as_uint(bpm));
+            // the round's largest possible node sum at the launch's scale must stay < 2^61
+            if (ldexpf(bm * (float)rn, er.det_sm) >= 2.3e18f || ldexpf(bpm * (float)rn, er.det_sp) >= 2.3e18f)
+              set_error(P, IC.benv, kErrDetRange, 0x7fffffff);
+          }
+        }
         // Golden-ratio spread: consecutive lanes take staged slots ~0.618 rn apart
         // (odd, coprime with rn: a bijection on [0, rn)), i.e. particles spread over
         // the whole bucket, so a warp's 27-node stencils rarely share a node (staged
@@ -697,7 +741,16 @@ __device__ __forceinline__ void item_rounds(const SimParams& P, Smem<NCH, F>& S,
         const long long sxy = (long long)P.dims[0] * P.dims[1];
         auto flush_node = [&](int t, long long gi) {
           const int im = S.itile[3][t];
-          if (im != 0) {
+          if (DET && im != 0) {  // exact integer conversion to the launch's fixed point
+            auto sh = [](int v, int d) {
+              return d >= 0 ? (long long)v << d : (d > -63 ? (long long)v >> -d : (v < 0 ? -1ll : 0ll));
+            };
+            long long* g = &P.gPMd[gi].x;
+            red_add_i64(g + 0, sh(S.itile[0][t], dsh_p));
+            red_add_i64(g + 1, sh(S.itile[1][t], dsh_p));
+            red_add_i64(g + 2, sh(S.itile[2][t], dsh_p));
+            red_add_i64(g + 3, sh(im, dsh_m));
+          } else if (im != 0) {
             red_add_v4(&P.gPM[gi], qs[0] * (float)S.itile[0][t], qs[1] * (float)S.itile[1][t],
                        qs[2] * (float)S.itile[2][t], qs[3] * (float)im);
             if (NCH == 7)
@@ -725,7 +778,9 @@ __device__ __forceinline__ void item_rounds(const SimParams& P, Smem<NCH, F>& S,
     }
 
     if (!redo && tid == 0 && stay_base) atomicAdd(&P.bucket_count[IC.key], stay_base);
-    if (IC.penalty && !redo) {
+    if (DET && IC.penalty && !redo) {
+      if (tid == 0 && S.penmax) atomicMax(&P.max_pen_bits[IC.benv], S.penmax);
+    } else if (IC.penalty && !redo) {
       const int b0 = P.body_off[IC.benv], nb = min(P.body_off[IC.benv + 1] - b0, kMaxBodiesPerEnv);
       for (int t = tid; t < nb * 6; t += kT) {
         const double val = S.wsum[t];
@@ -745,7 +800,7 @@ __device__ __forceinline__ void item_rounds(const SimParams& P, Smem<NCH, F>& S,
   }
 }
 
-template <int NCH, int F, bool AM>
+template <int NCH, int F, bool AM, bool DET>
 __global__ void __launch_bounds__(kT, kCtasPerSm) k_particles(SimParams P) {
   MSIM_GEO_ALIASES(F)
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -823,7 +878,7 @@ __global__ void __launch_bounds__(kT, kCtasPerSm) k_particles(SimParams P) {
       IC.lostb = lostb; IC.do_g2p = do_g2p; IC.do_p2g = do_p2g; IC.penalty = penalty;
     }
     __syncthreads();
-    item_rounds<NCH, F, AM>(P, S, redo);
+    item_rounds<NCH, F, AM, DET>(P, S, redo);
     __syncthreads();
     if (!redo && tid < Gm::NBT) {  // the bucket's touched node blocks (once per bucket)
       if (S.bflag[tid]) {
@@ -872,9 +927,13 @@ __global__ void __launch_bounds__(256) k_rebin(SimParams P) {
   const unsigned peers = __match_any_sync(am, key);
   const int leader = __ffs(peers) - 1;
   int basecnt = 0;
-  if (lane == leader) basecnt = atomicAdd(&P.bucket_count[key], __popc(peers));
+  if (lane == leader) {
+    basecnt = atomicAdd(P.det ? &P.move_count[key] : &P.bucket_count[key], __popc(peers));
+    if (P.det) atomicAdd(&P.bucket_count[key], __popc(peers));
+  }
   basecnt = __shfl_sync(peers, basecnt, leader);
-  P.rank[i] = basecnt + __popc(peers & ((1u << lane) - 1u));
+  const int r = basecnt + __popc(peers & ((1u << lane) - 1u));
+  P.rank[i] = P.det ? -1 - r : r;  // deterministic mode: all "movers", put in index order after k_perm
 }
 
 // Particle i (slot of the launch that keyed it) -> its slot in the next launch:
@@ -884,8 +943,41 @@ __global__ void k_perm(SimParams P) {
   const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (i >= P.n) return;
   const int k = P.key[i], r = P.rank[i];
-  if (r == -1) P.move_count[k] = 0;  // exactly one mover per bucket has rank -1: reset the counter
+  if (r == -1 && !P.det) P.move_count[k] = 0;  // exactly one mover per bucket has rank -1: reset the counter
   P.perm_w[(r >= 0 ? P.bucket_start_w[k] : P.bucket_start_w[k + 1]) + r] = (int)i;
+}
+
+// Deterministic mode: the movers at the end of each bucket (atomic ranks) are
+// put in the order of their previous slots, so the next launch's particle
+// order -- hence every fixed-point scale and every sum -- is reproducible.
+// One CTA per bucket; each mover's position = #movers with a smaller slot.
+__global__ void __launch_bounds__(128) k_det_sort_movers(SimParams P) {
+  __shared__ int tail[1024];
+  for (int k = blockIdx.x; k < P.n_keys; k += gridDim.x) {
+    const int cnt = P.move_count[k];
+    if (cnt == 0) continue;
+    __syncthreads();
+    int* seg = P.perm_w + P.bucket_start_w[k + 1] - cnt;
+    if (cnt <= 1024) {
+      for (int t = threadIdx.x; t < cnt; t += blockDim.x) tail[t] = seg[t];
+      __syncthreads();
+      for (int t = threadIdx.x; t < cnt; t += blockDim.x) {
+        const int v = tail[t];
+        int pos = 0;
+        for (int u = 0; u < cnt; ++u) pos += tail[u] < v;
+        seg[pos] = v;
+      }
+    } else if (threadIdx.x == 0) {  // a very crowded bucket: insertion sort in place
+      for (int a = 1; a < cnt; ++a) {
+        const int v = seg[a];
+        int b = a - 1;
+        while (b >= 0 && seg[b] > v) seg[b + 1] = seg[b], --b;
+        seg[b + 1] = v;
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) P.move_count[k] = 0;
+  }
 }
 
 // Zero the nodes touched by the last P2G (phase API: the reference clears
@@ -905,6 +997,7 @@ __global__ void k_clear(SimParams P) {
     P.gPM[gi] = z;
     P.gF[gi] = z;
     P.gV[gi] = z;
+    if (P.det) P.gPMd[gi] = make_longlong4(0, 0, 0, 0);
   }
 }
 
@@ -922,7 +1015,14 @@ __global__ void __launch_bounds__(256) k_grid(SimParams P) {
               gz = kBZ * (lb / (P.bdims[0] * P.bdims[1])) + lane / (kBX * kBY);
     const bool inside = gx < P.dims[0] && gy < P.dims[1] && gz < P.dims[2];
     const long long gi = env * P.nodes_per_env + ((long long)gz * P.dims[1] + gy) * P.dims[0] + gx;
-    const float4 pm = inside ? P.gPM[gi] : make_float4(0.f, 0.f, 0.f, 0.f);
+    float4 pm = inside ? P.gPM[gi] : make_float4(0.f, 0.f, 0.f, 0.f);
+    if (P.det && inside) {  // int64 fixed point of this launch (4 channels)
+      const longlong4 q = P.gPMd[gi];
+      const int sm = P.run[env].det_sm, sp = P.run[env].det_sp;
+      pm = make_float4((float)ldexp((double)q.x, -sp), (float)ldexp((double)q.y, -sp), (float)ldexp((double)q.z, -sp),
+                       (float)ldexp((double)q.w, -sm));
+      if (P.clear_on_read) P.gPMd[gi] = make_longlong4(0, 0, 0, 0);
+    }
     const float4 ff = (inside && P.split) ? P.gF[gi] : make_float4(0.f, 0.f, 0.f, 0.f);
     const bool live = inside && pm.w > 0.0f;
     const float dt = P.run[env].dt_c;
@@ -1004,6 +1104,17 @@ __global__ void __launch_bounds__(256) k_grid(SimParams P) {
 // ---------------------------------------------------------------------------
 // Per-env bookkeeping.
 
+// Deterministic mode: this launch's grid fixed-point exponents of an env: mass
+// from the env's total mass (node sums < 2^61), momentum from the largest round
+// bound of the previous launch (a contribution of that size ~ 2^kDetMomentumExp).
+__device__ void det_exponents(const SimParams& P, int env, EnvRun& r) {
+  if (!P.det) return;
+  r.det_sm = P.det_mexp[env];
+  const float b = __uint_as_float(P.det_bnd[env]);
+  r.det_sp = b > 0.f ? kDetMomentumExp - ilogbf(b) : kDetMomentumExp;
+  P.det_bnd[env] = 0u;
+}
+
 __device__ void plan_cycles(const SimParams& P, int env, EnvRun& r) {  // mpm.hpp:399-409
   const double vmax = (double)__uint_as_float(P.vmax_bits[env]);
   int halvings = 0;
@@ -1054,6 +1165,7 @@ __global__ void k_call_begin(SimParams P, int n_sub, int first_action) {
   r.rigid_idx = 0;
   if (n_sub > 0 && P.integrate_rigid) rigid_env(P, env, 1);  // rigid step 0: integrate + sync
   if (n_sub > 0) plan_cycles(P, env, r);
+  det_exponents(P, env, r);
   r.dt_g2p = 0.0f;
   r.dt_p2g = r.dt_c;  // the first P2G knows its dt exactly
   P.vmax_bits[env] = 0u;
@@ -1090,6 +1202,7 @@ __global__ void k_iter_begin(SimParams P) {
       rigid_env(P, env, 1);
     }
   }
+  det_exponents(P, env, r);
   P.vmax_bits[env] = 0u;
 }
 
@@ -1098,6 +1211,15 @@ __global__ void k_iter_end(SimParams P) {
   if (env >= P.n_env) return;
   EnvRun& r = P.run[env];
   if (r.action == kActIdle) return;
+  if (P.det) {  // integer sums of this cycle -> the double accumulators (exact up to 2^-36)
+    const int b0 = P.body_off[env], b1 = P.body_off[env + 1];
+    for (int k = 6 * b0; k < 6 * b1; ++k) P.wrench[k] = ldexp((double)P.w64[k], -kDetWrenchExp);
+    for (int k = 0; k < 3; ++k) {
+      P.applied[3 * env + k] = ldexp((double)P.a64[3 * env + k], -kDetWrenchExp);
+      P.react[3 * env + k] = ldexp((double)P.r64[3 * env + k], -kDetWrenchExp);
+      P.a64[3 * env + k] = P.r64[3 * env + k] = 0;
+    }
+  }
   double ex = P.applied[3 * env] + P.react[3 * env];
   double ey = P.applied[3 * env + 1] + P.react[3 * env + 1];
   double ez = P.applied[3 * env + 2] + P.react[3 * env + 2];
@@ -1146,7 +1268,9 @@ __global__ void k_redo_clear(SimParams P) {
     const int gx = kBX * (lb % P.bdims[0]) + l % kBX, gy = kBY * ((lb / P.bdims[0]) % P.bdims[1]) + (l / kBX) % kBY,
               gz = kBZ * (lb / (P.bdims[0] * P.bdims[1])) + l / (kBX * kBY);
     if (gx >= P.dims[0] || gy >= P.dims[1] || gz >= P.dims[2]) continue;
-    P.gPM[env * P.nodes_per_env + ((long long)gz * P.dims[1] + gy) * P.dims[0] + gx] = z;
+    const long long gi = env * P.nodes_per_env + ((long long)gz * P.dims[1] + gy) * P.dims[0] + gx;
+    P.gPM[gi] = z;
+    if (P.det) P.gPMd[gi] = make_longlong4(0, 0, 0, 0);
   }
 }
 
@@ -1177,18 +1301,23 @@ struct Timed {
 };
 
 // persistent grid: as many CTAs as fit on the device at once (occupancy query)
-template <int NCH, int F, bool AM>
+template <int NCH, int F, bool AM, bool DET = false>
 void launch_k_particles(const SimParams& P, cudaStream_t s) {
   static int per_sm = 0;
   if (!per_sm) {
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_particles<NCH, F, AM>, kT, sizeof(Smem<NCH, F>));
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_particles<NCH, F, AM, DET>, kT, sizeof(Smem<NCH, F>));
     if (per_sm <= 0) per_sm = 1;
   }
-  k_particles<NCH, F, AM><<<sm_count() * per_sm, kT, sizeof(Smem<NCH, F>), s>>>(P);
+  k_particles<NCH, F, AM, DET><<<sm_count() * per_sm, kT, sizeof(Smem<NCH, F>), s>>>(P);
 }
 
 template <bool AM>
 void particle_kernel_m(const SimParams& P, cudaStream_t s) {
+  if (P.det) {  // deterministic mode: 4 channels only (msim_gpu_set_deterministic)
+    if (P.qf == 2) launch_k_particles<4, 2, AM, true>(P, s);
+    else launch_k_particles<4, 1, AM, true>(P, s);
+    return;
+  }
   if (P.qf == 2) {
     if (P.split) launch_k_particles<7, 2, AM>(P, s);
     else launch_k_particles<4, 2, AM>(P, s);
@@ -1206,10 +1335,14 @@ void particle_kernel(const SimParams& P, cudaStream_t s) {
 }  // namespace
 
 void configure_kernels() {
-#define MSIM_SET_SMEM(NCH, F, AM) \
-  cudaFuncSetAttribute(k_particles<NCH, F, AM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(Smem<NCH, F>))
-  MSIM_SET_SMEM(4, 1, false); MSIM_SET_SMEM(7, 1, false); MSIM_SET_SMEM(4, 2, false); MSIM_SET_SMEM(7, 2, false);
-  MSIM_SET_SMEM(4, 1, true); MSIM_SET_SMEM(7, 1, true); MSIM_SET_SMEM(4, 2, true); MSIM_SET_SMEM(7, 2, true);
+#define MSIM_SET_SMEM(NCH, F, AM, DET)                                                              \
+  cudaFuncSetAttribute(k_particles<NCH, F, AM, DET>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                       (int)sizeof(Smem<NCH, F>))
+  MSIM_SET_SMEM(4, 1, false, false); MSIM_SET_SMEM(7, 1, false, false); MSIM_SET_SMEM(4, 2, false, false);
+  MSIM_SET_SMEM(7, 2, false, false); MSIM_SET_SMEM(4, 1, true, false); MSIM_SET_SMEM(7, 1, true, false);
+  MSIM_SET_SMEM(4, 2, true, false); MSIM_SET_SMEM(7, 2, true, false);
+  MSIM_SET_SMEM(4, 1, false, true); MSIM_SET_SMEM(4, 2, false, true); MSIM_SET_SMEM(4, 1, true, true);
+  MSIM_SET_SMEM(4, 2, true, true);
 #undef MSIM_SET_SMEM
 }
 
@@ -1227,6 +1360,7 @@ void launch_rebin(const SimParams& P, cudaStream_t s) {
   Timed tm(P, kKBucketScan, s, 4);
   scan_exclusive(Q.bucket_count, Q.bucket_start_w, Q.n_keys, Q.active_buckets_w, Q.n_active_buckets_w, Q.scan_tmp, s);
   if (Q.n > 0) k_perm<<<nblk(Q.n), 256, 0, s>>>(Q);
+  if (Q.det) k_det_sort_movers<<<sm_count() * 8, 128, 0, s>>>(Q);
 }
 
 void launch_clear(const SimParams& P, cudaStream_t s) {
@@ -1256,6 +1390,7 @@ void launch_particles(const SimParams& P, cudaStream_t s) {
     // launch still reads this launch's perm / bucket offsets
     scan_exclusive(P.bucket_count, P.bucket_start_w, P.n_keys, P.active_buckets_w, P.n_active_buckets_w, P.scan_tmp, s);
     if (P.n > 0) k_perm<<<nblk(P.n), 256, 0, s>>>(P);
+    if (P.det) k_det_sort_movers<<<sm_count() * 8, 128, 0, s>>>(P);
   }
   Timed tm(P, kKBlockScan, s, 3);
   scan_exclusive(P.nb_flag, P.nb_scan, P.n_blocks, P.nb_list, P.n_nb, P.scan_tmp, s);

@@ -40,7 +40,7 @@ class GpuWorld:
     """All environments of a Scene on one device."""
 
     def __init__(self, scene: Scene, device: int = 0, split_channels: bool = False,
-                 record_binning: bool = False, bucket_factor: int = 0):
+                 record_binning: bool = False, bucket_factor: int = 0, deterministic: bool = False):
         self.lib = lib = abi.load()
         self.scene = scene
         self.n_env = len(scene.envs)
@@ -56,6 +56,8 @@ class GpuWorld:
             _check(lib, ctx, lib.msim_gpu_set_record_binning(ctx, 1))
         if bucket_factor:
             _check(lib, ctx, lib.msim_gpu_set_bucket_factor(ctx, bucket_factor))
+        if deterministic:
+            _check(lib, ctx, lib.msim_gpu_set_deterministic(ctx, 1))
         self.counts = [e.n for e in scene.envs]
         self.offsets = np.zeros(self.n_env + 1, dtype=np.int64)
         self.offsets[1:] = np.cumsum(self.counts)
