@@ -176,9 +176,10 @@ __device__ inline void set_kinematic_pose(BodyDev& b, const double* p, double dt
 // wrench; scripted: constant twist; scheduled kinematic: the schedule's pose
 // of this rigid step), then sync_rigid_to_soft: zero the accumulating
 // wrenches and rebuild the per-shape world transforms.
-__device__ inline void rigid_env(const SimParams& P, int env, int integrate) {
+// lane / nlanes: the threads sharing the env (one warp: bodies, then shapes, in parallel).
+__device__ inline void rigid_env(const SimParams& P, int env, int integrate, int lane = 0, int nlanes = 1) {
   const int b0 = P.body_off[env], b1 = P.body_off[env + 1];
-  for (int bi = b0; bi < b1; ++bi) {
+  for (int bi = b0 + lane; bi < b1; bi += nlanes) {
     BodyDev& b = P.bodies[bi];
     if (integrate) {
       if (b.mode == MSIM_BODY_DYNAMIC)
@@ -195,8 +196,9 @@ __device__ inline void rigid_env(const SimParams& P, int env, int integrate) {
     if (P.det)
       for (int k = 0; k < 6; ++k) P.w64[6 * bi + k] = 0;
   }
+  if (nlanes > 1) __syncwarp();  // shapes read their (integrated) bodies
   const int s0 = P.shape_off[env], s1 = P.shape_off[env + 1];
-  for (int si = s0; si < s1; ++si) {
+  for (int si = s0 + lane; si < s1; si += nlanes) {
     const ShapeHost& sh = P.shape_src[si];
     const BodyDev& b = P.bodies[b0 + sh.body];
     dq bq = {b.q[0], b.q[1], b.q[2], b.q[3]};

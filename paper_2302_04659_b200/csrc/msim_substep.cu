@@ -800,13 +800,13 @@ __device__ __forceinline__ void item_rounds(const SimParams& P, Smem<NCH, F>& S,
   }
 }
 
+// One CTA's share of a particle launch (cta of ncta).
 template <int NCH, int F, bool AM, bool DET>
-__global__ void __launch_bounds__(kT, kCtasPerSm) k_particles(SimParams P) {
+__device__ __forceinline__ void particles_cta(const SimParams& P, unsigned char* smem_raw, const bool redo, const int cta,
+                                              const int ncta) {
   MSIM_GEO_ALIASES(F)
-  extern __shared__ __align__(16) unsigned char smem_raw[];
   Smem<NCH, F>& S = *reinterpret_cast<Smem<NCH, F>*>(smem_raw);
   const int tid = threadIdx.x;
-  const bool redo = P.redo_pass != 0;
   if (redo && !*P.any_redo) return;
   const int nitems = *P.n_active_buckets;
 
@@ -817,14 +817,14 @@ __global__ void __launch_bounds__(kT, kCtasPerSm) k_particles(SimParams P) {
   // Buckets are handed out dynamically after a first static one per CTA (one
   // atomic per further bucket): their sizes vary, and a static round-robin
   // leaves a tail of CTAs with more work (-12 % per launch at D).
-  for (int item = blockIdx.x; item < nitems;) {
+  for (int item = cta; item < nitems;) {
     const int key = P.active_buckets[item];
     const bool lostb = key == P.n_keys - 1;
     const int benv = lostb ? 0 : key / P.buckets_per_env;
     if (redo && (lostb || !P.run[benv].redo)) {  // CTA-uniform
       __syncthreads();
       if (tid == 0)
-        S.next_item = (int)gridDim.x + (kDynamicItems ? atomicAdd(P.item_counter + redo, 1) : item);
+        S.next_item = ncta + (kDynamicItems ? atomicAdd(P.item_counter + redo, 1) : item);
       __syncthreads();
       item = S.next_item;
       continue;
@@ -888,20 +888,26 @@ __global__ void __launch_bounds__(kT, kCtasPerSm) k_particles(SimParams P) {
         P.nb_flag[IC.benv * P.blocks_per_env + (kz * P.bdims[1] + ky) * P.bdims[0] + kx] = 1;
       }
     }
-    if (tid == 0) S.next_item = (int)gridDim.x + (kDynamicItems ? atomicAdd(P.item_counter + redo, 1) : item);
+    if (tid == 0) S.next_item = ncta + (kDynamicItems ? atomicAdd(P.item_counter + redo, 1) : item);
     __syncthreads();
     item = S.next_item;
   }
   // the last fetching CTA out resets the hand-out counter for the next launch
   // (no memset node; CTAs without a first bucket never fetched)
-  if (kDynamicItems && tid == 0 && (int)blockIdx.x < nitems) {
+  if (kDynamicItems && tid == 0 && cta < nitems) {
     __threadfence();
-    if (atomicAdd(P.item_counter + 2 + redo, 1) == min((int)gridDim.x, nitems) - 1) {
+    if (atomicAdd(P.item_counter + 2 + redo, 1) == min(ncta, nitems) - 1) {
       P.item_counter[redo] = 0;
       P.item_counter[2 + redo] = 0;
       __threadfence();
     }
   }
+}
+
+template <int NCH, int F, bool AM, bool DET>
+__global__ void __launch_bounds__(kT, kCtasPerSm) k_particles(SimParams P) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  particles_cta<NCH, F, AM, DET>(P, smem_raw, P.redo_pass != 0, (int)blockIdx.x, (int)gridDim.x);
 }
 
 // Bucket keys of stored positions (after uploads): no loss flagging here, a
@@ -939,12 +945,14 @@ __global__ void __launch_bounds__(256) k_rebin(SimParams P) {
 // Particle i (slot of the launch that keyed it) -> its slot in the next launch:
 // stayers (rank >= 0) from the bucket's start in their old order, movers
 // (rank = -1 - r) from its end.
-__global__ void k_perm(SimParams P) {
-  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (i >= P.n) return;
+__device__ __forceinline__ void perm_at(const SimParams& P, long long i) {
   const int k = P.key[i], r = P.rank[i];
   if (r == -1 && !P.det) P.move_count[k] = 0;  // exactly one mover per bucket has rank -1: reset the counter
   P.perm_w[(r >= 0 ? P.bucket_start_w[k] : P.bucket_start_w[k + 1]) + r] = (int)i;
+}
+__global__ void k_perm(SimParams P) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i < P.n) perm_at(P, i);
 }
 
 // Deterministic mode: the movers at the end of each bucket (atomic ranks) are
@@ -1003,12 +1011,13 @@ __global__ void k_clear(SimParams P) {
 
 // Grid update (mpm.hpp:315-342) with the grid-mode penalty hook
 // (coupling.hpp:186-214); one warp per touched node block (32 nodes).
-__global__ void __launch_bounds__(256) k_grid(SimParams P) {
+// gtid / gthreads: this thread's index / the thread count of the launch (one warp per item)
+__device__ __forceinline__ void grid_items(const SimParams& P, const int gtid, const int gthreads) {
   static_assert(kBX * kBY * kBZ == 32, "one warp per node block");
   const int nlist = *P.n_nb;
   const int lane = threadIdx.x & 31;
   const unsigned FULL = 0xffffffffu;
-  for (int item = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; item < nlist; item += (gridDim.x * blockDim.x) >> 5) {
+  for (int item = gtid >> 5; item < nlist; item += gthreads >> 5) {
     const int nb = P.nb_list[item];
     const int env = nb / P.blocks_per_env, lb = nb - env * P.blocks_per_env;
     const int gx = kBX * (lb % P.bdims[0]) + lane % kBX, gy = kBY * ((lb / P.bdims[0]) % P.bdims[1]) + (lane / kBX) % kBY,
@@ -1098,6 +1107,10 @@ __global__ void __launch_bounds__(256) k_grid(SimParams P) {
   }
 }
 
+__global__ void __launch_bounds__(256) k_grid(SimParams P) {
+  grid_items(P, (int)(blockIdx.x * blockDim.x + threadIdx.x), (int)(gridDim.x * blockDim.x));
+}
+
 // ---------------------------------------------------------------------------
 // Per-env bookkeeping.
 
@@ -1144,71 +1157,93 @@ __global__ void k_set_action(SimParams P, int action, float dt) {
   if (action == kActG2P) P.vmax_bits[env] = 0u;
 }
 
+// One warp per env (lane 0: the env's state machine; all lanes: its rigid step).
+__device__ void call_begin_env(const SimParams& P, int env, int n_sub, int first_action, int lane) {
+  EnvRun& r = P.run[env];
+  int rigid = 0;
+  if (lane == 0) {
+    r.substeps_left = n_sub;
+    r.soft_in_rigid = 0;
+    r.cycle = 0;
+    r.cyc_sum = 0;
+    r.next_new_sub = 0;
+    r.next_new_rigid = 0;
+    r.redo = 0;
+    r.action = n_sub > 0 ? first_action : kActIdle;
+    if (P.err_code[env]) {
+      r.action = kActIdle;
+      r.substeps_left = 0;
+    } else {
+      r.rigid_idx = 0;
+      rigid = n_sub > 0 && P.integrate_rigid;
+    }
+  }
+  rigid = __shfl_sync(0xffffffffu, rigid, 0);
+  if (rigid) rigid_env(P, env, 1, lane, 32);  // rigid step 0: integrate + sync
+  __syncwarp();
+  if (lane == 0 && !P.err_code[env]) {
+    if (n_sub > 0) plan_cycles(P, env, r);
+    det_exponents(P, env, r);
+    r.dt_g2p = 0.0f;
+    r.dt_p2g = r.dt_c;  // the first P2G knows its dt exactly
+    P.vmax_bits[env] = 0u;
+  }
+}
+
 __global__ void k_call_begin(SimParams P, int n_sub, int first_action) {
-  const int env = blockIdx.x * blockDim.x + threadIdx.x;
-  if (env == 0) *P.any_redo = 0;
-  if (env >= P.n_env) return;
-  EnvRun& r = P.run[env];
-  r.substeps_left = n_sub;
-  r.soft_in_rigid = 0;
-  r.cycle = 0;
-  r.cyc_sum = 0;
-  r.next_new_sub = 0;
-  r.next_new_rigid = 0;
-  r.redo = 0;
-  r.action = n_sub > 0 ? first_action : kActIdle;
-  if (P.err_code[env]) {
-    r.action = kActIdle;
-    r.substeps_left = 0;
-    return;
-  }
-  r.rigid_idx = 0;
-  if (n_sub > 0 && P.integrate_rigid) rigid_env(P, env, 1);  // rigid step 0: integrate + sync
-  if (n_sub > 0) plan_cycles(P, env, r);
-  det_exponents(P, env, r);
-  r.dt_g2p = 0.0f;
-  r.dt_p2g = r.dt_c;  // the first P2G knows its dt exactly
-  P.vmax_bits[env] = 0u;
+  const int t = blockIdx.x * blockDim.x + threadIdx.x, env = t >> 5;
+  if (t == 0) *P.any_redo = 0;
+  if (env < P.n_env) call_begin_env(P, env, n_sub, first_action, t & 31);
 }
 
+// One warp per env (lane 0: the env's state machine; all lanes: its rigid step).
+__device__ void iter_begin_env(const SimParams& P, int env, int lane) {
+  EnvRun& r = P.run[env];
+  int rigid = 0, active = 0;
+  if (lane == 0) {
+    r.next_new_sub = 0;
+    r.next_new_rigid = 0;
+    r.redo = 0;
+    if (r.substeps_left <= 0 || P.err_code[env]) {
+      r.action = kActIdle;
+    } else {
+      active = 1;
+      r.dt_g2p = r.dt_c;
+      r.dt_p2g = r.dt_c;  // same substep: exact; new substep: speculated (same cycle count)
+      if (r.cycle == r.cycles - 1 && r.substeps_left == 1) {
+        r.action = kActG2P;
+      } else {
+        r.action = kActFused;
+        if (r.cycle + 1 >= r.cycles) {
+          r.next_new_sub = 1;
+          r.next_new_rigid = P.integrate_rigid && (r.soft_in_rigid + 1 == P.n_soft);
+        }
+        if (r.next_new_rigid) {
+          // end of rigid step: pending_wrenches = wrenches (coupling.hpp:288), then the
+          // next rigid step integrates with them and syncs (coupling.hpp:250-259)
+          const int b0 = P.body_off[env], b1 = P.body_off[env + 1];
+          for (int k = 6 * b0; k < 6 * b1; ++k) P.pending[k] = P.wrench[k];
+          r.rigid_idx += 1;
+          rigid = 1;
+        }
+      }
+    }
+  }
+  rigid = __shfl_sync(0xffffffffu, rigid, 0);
+  active = __shfl_sync(0xffffffffu, active, 0);
+  if (rigid) rigid_env(P, env, 1, lane, 32);
+  if (lane == 0 && active) {
+    det_exponents(P, env, r);
+    P.vmax_bits[env] = 0u;
+  }
+}
 __global__ void k_iter_begin(SimParams P) {
-  const int env = blockIdx.x * blockDim.x + threadIdx.x;
-  if (env == 0) *P.any_redo = 0;
-  if (env >= P.n_env) return;
-  EnvRun& r = P.run[env];
-  r.next_new_sub = 0;
-  r.next_new_rigid = 0;
-  r.redo = 0;
-  if (r.substeps_left <= 0 || P.err_code[env]) {
-    r.action = kActIdle;
-    return;
-  }
-  r.dt_g2p = r.dt_c;
-  r.dt_p2g = r.dt_c;  // same substep: exact; new substep: speculated (same cycle count)
-  if (r.cycle == r.cycles - 1 && r.substeps_left == 1) {
-    r.action = kActG2P;
-  } else {
-    r.action = kActFused;
-    if (r.cycle + 1 >= r.cycles) {
-      r.next_new_sub = 1;
-      r.next_new_rigid = P.integrate_rigid && (r.soft_in_rigid + 1 == P.n_soft);
-    }
-    if (r.next_new_rigid) {
-      // end of rigid step: pending_wrenches = wrenches (coupling.hpp:288), then the
-      // next rigid step integrates with them and syncs (coupling.hpp:250-259)
-      const int b0 = P.body_off[env], b1 = P.body_off[env + 1];
-      for (int k = 6 * b0; k < 6 * b1; ++k) P.pending[k] = P.wrench[k];
-      r.rigid_idx += 1;
-      rigid_env(P, env, 1);
-    }
-  }
-  det_exponents(P, env, r);
-  P.vmax_bits[env] = 0u;
+  const int t = blockIdx.x * blockDim.x + threadIdx.x, env = t >> 5;
+  if (t == 0) *P.any_redo = 0;
+  if (env < P.n_env) iter_begin_env(P, env, t & 31);
 }
 
-__global__ void k_iter_end(SimParams P) {
-  const int env = blockIdx.x * blockDim.x + threadIdx.x;
-  if (env >= P.n_env) return;
+__device__ void iter_end_env(const SimParams& P, int env) {
   EnvRun& r = P.run[env];
   if (r.action == kActIdle) return;
   if (P.det) {  // integer sums of this cycle -> the double accumulators (exact up to 2^-36)
@@ -1252,16 +1287,19 @@ __global__ void k_iter_end(SimParams P) {
   }
   if (P.err_code[env]) r.substeps_left = 0;
 }
+__global__ void k_iter_end(SimParams P) {
+  const int env = blockIdx.x * blockDim.x + threadIdx.x;
+  if (env < P.n_env) iter_end_env(P, env);
+}
 
 // Redo pass, step 1: zero the P2G accumulators of envs whose speculated dt
 // missed (their node blocks are in the node-block list of this launch).
-__global__ void k_redo_clear(SimParams P) {
+__device__ void redo_clear_range(const SimParams& P, long long gtid, long long gthreads) {
   if (!*P.any_redo) return;
   const int nlist = *P.n_nb;
   const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
   constexpr int NB = kBX * kBY * kBZ;
-  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < (long long)nlist * NB;
-       t += (long long)gridDim.x * blockDim.x) {
+  for (long long t = gtid; t < (long long)nlist * NB; t += gthreads) {
     const int nb = P.nb_list[t / NB], l = (int)(t % NB);
     const int env = nb / P.blocks_per_env, lb = nb - env * P.blocks_per_env;
     if (!P.run[env].redo) continue;
@@ -1272,6 +1310,9 @@ __global__ void k_redo_clear(SimParams P) {
     P.gPM[gi] = z;
     if (P.det) P.gPMd[gi] = make_longlong4(0, 0, 0, 0);
   }
+}
+__global__ void k_redo_clear(SimParams P) {
+  redo_clear_range(P, blockIdx.x * (long long)blockDim.x + threadIdx.x, (long long)gridDim.x * blockDim.x);
 }
 
 inline unsigned nblk(long long n, int t = 256) { return (unsigned)((n + t - 1) / t); }
@@ -1374,7 +1415,7 @@ void launch_set_action(const SimParams& P, int action, float dt, cudaStream_t s)
 
 void launch_call_begin(const SimParams& P, int n_sub, int first_action, cudaStream_t s) {
   Timed tm(P, kKPlan, s);
-  k_call_begin<<<nblk(P.n_env), 256, 0, s>>>(P, n_sub, first_action);
+  k_call_begin<<<nblk(32LL * P.n_env), 256, 0, s>>>(P, n_sub, first_action);
 }
 
 void launch_particles(const SimParams& P, cudaStream_t s) {
@@ -1409,7 +1450,7 @@ void launch_iteration_end(const SimParams& P, cudaStream_t s) {
 void launch_iteration(const SimParams& P, bool bookkeeping, bool grid_update, cudaStream_t s) {
   if (bookkeeping) {
     Timed tm(P, kKRigid, s);
-    k_iter_begin<<<nblk(P.n_env), 256, 0, s>>>(P);
+    k_iter_begin<<<nblk(32LL * P.n_env), 256, 0, s>>>(P);
   }
   launch_particles(P, s);
   {
