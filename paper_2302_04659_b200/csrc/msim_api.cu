@@ -375,6 +375,7 @@ void set_bucket_shape(msim_gpu_ctx* c, int f) {
   const long long scan_n = std::max<long long>(std::max(c->n_keys, c->n_env * c->blocks_per_env),
                                                std::min<long long>(c->nodes_per_env + 1, INT_MAX));
   CK(c->scan_tmp_d.ensure(sizeof(int) * scan_tmp_ints((int)scan_n)));
+  CK(cudaMemset(c->scan_tmp_d.p, 0, sizeof(int) * scan_tmp_ints((int)scan_n)));  // single-pass scan status
   CK(cudaDeviceSynchronize());
   c->perm_valid = false;
 }
@@ -1406,6 +1407,7 @@ int msim_gpu_read_binning(msim_gpu_ctx* c, int env, int32_t* base, int32_t* cell
     CK(nlc.ensure(sizeof(int)));
     CK(an.ensure(sizeof(long long) * nn));
     CK(tmp.ensure(sizeof(int) * scan_tmp_ints((int)std::max<long long>(nbins + 1, nn + 1))));
+    CK(cudaMemsetAsync(tmp.p, 0, sizeof(int) * scan_tmp_ints((int)std::max<long long>(nbins + 1, nn + 1)), s));
     SimParams P = params(c);
     const int* b = c->base_dbg_d.as<int>() + 3 * first;
     launch_binning_out(P, ne, b, cc.as<int>(), cs.as<int>(), cp.as<int>(), nf.as<int>(), ns.as<int>(),

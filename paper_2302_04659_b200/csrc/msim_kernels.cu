@@ -50,101 +50,6 @@ __device__ __forceinline__ int block_excl_scan(int v, int* total) {
   return r;
 }
 
-__global__ void __launch_bounds__(256) k_scan_reduce(const int* in, int n, int* tsum, int* tcnt) {
-  int base = blockIdx.x * kScanTile + threadIdx.x * 8;
-  int s = 0, c = 0;
-#pragma unroll
-  for (int k = 0; k < 8; ++k) {
-    int i = base + k;
-    int v = i < n ? in[i] : 0;
-    s += v;
-    c += v != 0;
-  }
-  __shared__ int tot;
-  int ex = block_excl_scan(s, &tot);
-  (void)ex;
-  __shared__ int totc;
-  int exc = block_excl_scan(c, &totc);
-  (void)exc;
-  if (threadIdx.x == 0) {
-    tsum[blockIdx.x] = tot;
-    tcnt[blockIdx.x] = totc;
-  }
-}
-
-__global__ void __launch_bounds__(256) k_scan_top(int* tsum, int* tcnt, int ntiles) {
-  // exclusive scan of tile sums in place, chunks of 256*8
-  __shared__ int carry_s, carry_c;
-  if (threadIdx.x == 0) carry_s = carry_c = 0;
-  __syncthreads();
-  for (int start = 0; start < ntiles; start += kScanTile) {
-    int vs[8], vc[8];
-    int ss = 0, sc = 0;
-    int b = start + threadIdx.x * 8;
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      vs[k] = b + k < ntiles ? tsum[b + k] : 0;
-      vc[k] = b + k < ntiles ? tcnt[b + k] : 0;
-      ss += vs[k];
-      sc += vc[k];
-    }
-    __shared__ int ts, tc;
-    int es = block_excl_scan(ss, &ts);
-    int ec = block_excl_scan(sc, &tc);
-    int rs = carry_s + es, rc = carry_c + ec;
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      if (b + k < ntiles) {
-        tsum[b + k] = rs;
-        tcnt[b + k] = rc;
-      }
-      rs += vs[k];
-      rc += vc[k];
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      carry_s += ts;
-      carry_c += tc;
-    }
-    __syncthreads();
-  }
-}
-
-__global__ void __launch_bounds__(256) k_scan_apply(int* in, int n, int* out, const int* tsum,
-                                                    const int* tcnt, int* list, int* n_list,
-                                                    int ntiles) {
-  int base = blockIdx.x * kScanTile + threadIdx.x * 8;
-  int v[8];
-  int s = 0, c = 0;
-#pragma unroll
-  for (int k = 0; k < 8; ++k) {
-    int i = base + k;
-    v[k] = i < n ? in[i] : 0;
-    s += v[k];
-    c += v[k] != 0;
-  }
-  __shared__ int tot, totc;
-  int es = block_excl_scan(s, &tot) + tsum[blockIdx.x];
-  int ec = block_excl_scan(c, &totc) + tcnt[blockIdx.x];
-#pragma unroll
-  for (int k = 0; k < 8; ++k) {
-    int i = base + k;
-    if (i < n) {
-      out[i] = es;
-      if (v[k] != 0) in[i] = 0;  // consumed: counts/flags restart from zero
-      if (list && v[k] != 0) list[ec++] = i;
-    }
-    es += v[k];
-  }
-  if (blockIdx.x == ntiles - 1 && threadIdx.x == 0) {
-    out[n] = tsum[blockIdx.x] + tot;
-    if (n_list) *n_list = tcnt[blockIdx.x] + totc;
-  }
-}
-
-// ---------------------------------------------------------------------------
-// Particle upload / download.
-
 __global__ void k_convert_in(SimParams P, long long n, const double* x, const double* v,
                              const double* F, const double* C, const double* mass,
                              const double* vol0, const int32_t* mat, const int* env_of,
@@ -384,6 +289,83 @@ inline unsigned nblk(long long n, int t = 256) { return (unsigned)((n + t - 1) /
 
 }  // namespace
 
+// Single-pass exclusive scan with compaction (the contract of the 3-kernel scan
+// above, one launch): tiles take ids in launch order from a counter, publish
+// their aggregate, look back over predecessors' published aggregates /
+// inclusive prefixes, publish their inclusive prefix, then write. Status word
+// per tile: flag (2 bits: 1 aggregate, 2 inclusive) | sum (31 bits) | count (31).
+constexpr unsigned long long kStAgg = 1ull << 62, kStIncl = 2ull << 62;
+__device__ __forceinline__ unsigned long long st_pack(unsigned long long flag, int s, int c) {
+  return flag | ((unsigned long long)(unsigned)s << 31) | (unsigned long long)(unsigned)c;
+}
+__global__ void __launch_bounds__(256) k_scan_1pass(int* in, int n, int* out, int* list, int* n_list, int ntiles,
+                                                   unsigned long long* status, unsigned* ctr) {
+  __shared__ int tile_s, pre_s, pre_c;
+  __shared__ bool last_s;
+  if (threadIdx.x == 0) tile_s = (int)atomicAdd(&ctr[0], 1u);
+  __syncthreads();
+  const int tile = tile_s;
+  const int base = tile * kScanTile + threadIdx.x * 8;
+  int v[8], sm = 0, c = 0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    v[k] = base + k < n ? in[base + k] : 0;
+    sm += v[k];
+    c += v[k] != 0;
+  }
+  __shared__ int tot_s, tot_c;
+  int es = block_excl_scan(sm, &tot_s);
+  int ec = block_excl_scan(c, &tot_c);
+  if (threadIdx.x == 0) {
+    volatile unsigned long long* st = status;
+    int ps = 0, pc = 0;
+    if (tile > 0) {
+      st[tile] = st_pack(kStAgg, tot_s, tot_c);
+      __threadfence();
+      for (int k = tile - 1; k >= 0;) {
+        const unsigned long long w = st[k];
+        const unsigned long long f = w & (3ull << 62);
+        if (f == 0) continue;  // predecessor not published yet
+        ps += (int)((w >> 31) & 0x7fffffffull);
+        pc += (int)(w & 0x7fffffffull);
+        if (f == kStIncl) break;
+        --k;
+      }
+    }
+    st[tile] = st_pack(kStIncl, ps + tot_s, pc + tot_c);
+    __threadfence();
+    pre_s = ps;
+    pre_c = pc;
+    if (tile == ntiles - 1) {
+      out[n] = ps + tot_s;
+      if (n_list) *n_list = pc + tot_c;
+    }
+  }
+  __syncthreads();
+  es += pre_s;
+  ec += pre_c;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const int i = base + k;
+    if (i < n) {
+      out[i] = es;
+      if (v[k] != 0) in[i] = 0;  // consumed: counts/flags restart from zero
+      if (list && v[k] != 0) list[ec++] = i;
+    }
+    es += v[k];
+  }
+  // the last tile to finish clears the status words and counters for the next call
+  if (threadIdx.x == 0) {
+    __threadfence();
+    last_s = atomicAdd(&ctr[1], 1u) == (unsigned)ntiles - 1u;
+  }
+  __syncthreads();
+  if (last_s) {
+    for (int t = threadIdx.x; t < ntiles; t += blockDim.x) status[t] = 0ull;
+    if (threadIdx.x == 0) ctr[0] = ctr[1] = 0u;
+  }
+}
+
 // ---------------------------------------------------------------------------
 // Launchers.
 
@@ -395,11 +377,10 @@ size_t scan_tmp_ints(int n) {
 void scan_exclusive(int* in, int* out, int n, int* list, int* n_list, int* tmp, cudaStream_t s) {
   int ntiles = (n + kScanTile - 1) / kScanTile;
   if (ntiles == 0) ntiles = 1;
-  int* tsum = tmp;
-  int* tcnt = tmp + ntiles;
-  k_scan_reduce<<<ntiles, 256, 0, s>>>(in, n, tsum, tcnt);
-  k_scan_top<<<1, 256, 0, s>>>(tsum, tcnt, ntiles);
-  k_scan_apply<<<ntiles, 256, 0, s>>>(in, n, out, tsum, tcnt, list, n_list, ntiles);
+  // one launch: decoupled look-back over the tiles (status words + counters in tmp,
+  // zero between calls: the last tile to finish resets them)
+  k_scan_1pass<<<ntiles, 256, 0, s>>>(in, n, out, list, n_list, ntiles, reinterpret_cast<unsigned long long*>(tmp),
+                                      reinterpret_cast<unsigned*>(tmp + 2 * ntiles));
 }
 
 void launch_convert_in(const SimParams& P, long long n, const double* x, const double* v,

@@ -1398,7 +1398,7 @@ void launch_rebin(const SimParams& P, cudaStream_t s) {
   Q.bucket_start_w = P.bucket_start;
   Q.active_buckets_w = P.active_buckets;
   Q.n_active_buckets_w = P.n_active_buckets;
-  Timed tm(P, kKBucketScan, s, 4);
+  Timed tm(P, kKBucketScan, s, P.det ? 3 : 2);
   scan_exclusive(Q.bucket_count, Q.bucket_start_w, Q.n_keys, Q.active_buckets_w, Q.n_active_buckets_w, Q.scan_tmp, s);
   if (Q.n > 0) k_perm<<<nblk(Q.n), 256, 0, s>>>(Q);
   if (Q.det) k_det_sort_movers<<<sm_count() * 8, 128, 0, s>>>(Q);
@@ -1426,14 +1426,14 @@ void launch_particles(const SimParams& P, cudaStream_t s) {
     particle_kernel(Q, s);
   }
   {
-    Timed tm(P, kKBucketScan, s, 4);
+    Timed tm(P, kKBucketScan, s, P.det ? 3 : 2);
     // the next launch's bucket structure goes to the write set: the redo pass of this
     // launch still reads this launch's perm / bucket offsets
     scan_exclusive(P.bucket_count, P.bucket_start_w, P.n_keys, P.active_buckets_w, P.n_active_buckets_w, P.scan_tmp, s);
     if (P.n > 0) k_perm<<<nblk(P.n), 256, 0, s>>>(P);
     if (P.det) k_det_sort_movers<<<sm_count() * 8, 128, 0, s>>>(P);
   }
-  Timed tm(P, kKBlockScan, s, 3);
+  Timed tm(P, kKBlockScan, s, 1);
   scan_exclusive(P.nb_flag, P.nb_scan, P.n_blocks, P.nb_list, P.n_nb, P.scan_tmp, s);
 }
 
