@@ -275,7 +275,7 @@ def run_ours(args):
                      "E: 4M mixed clay / Drucker-Prager sand / J-only water / fixed-corotated jelly slabs")
                     + ", 256^3 grid h=0.005, 8 moving colliders (boxes, spheres, capsules, SDF volume), "
                     "25 substeps/env step, one scene per GPU")
-    gw = GpuWorld(scene, device=local)
+    gw = GpuWorld(scene, device=local, deterministic=args.deterministic)
     ctx = gw.ctx
     setup_s = time.perf_counter() - t_setup
     n_part = scene.n_particles
@@ -426,7 +426,8 @@ def run_ours(args):
             "data": "synthetic (seeded jittered lattices, seeding.hpp algorithm)",
             "env_steps_per_s": env_steps,
             "per_gpu": {"particle_substeps_per_s": value / world, "env_steps_per_s": env_steps / world},
-            "config": {"workload": workload, "envs_total": envs_global, "envs_per_gpu_rank0": n_envs,
+            "config": {"workload": workload + (" [deterministic mode]" if args.deterministic else ""),
+                       "envs_total": envs_global, "envs_per_gpu_rank0": n_envs,
                        "particles_per_gpu_rank0": n_part, "substeps_per_env_step": S, "dt": scene.dt,
                        "parallelism": f"env-sharded x{world} ({scaling} scaling, no data-path collective)",
                        "l2": "inputs larger than L2 (particle state 2 x %.2f GB)" % (n_part * 116 / 1e9)
@@ -462,6 +463,8 @@ def main():
     ap.add_argument("--config", choices=["A", "B", "C", "D", "E"], default="D", help="workload (SURVEY.md App. B)")
     ap.add_argument("--clay-only", action="store_true",
                     help="B / C / E: the reference's von Mises clay instead of sand / water / mixed")
+    ap.add_argument("--deterministic", action="store_true",
+                    help="msim_gpu_set_deterministic: bit-reproducible runs (int64 fixed-point sums)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--traffic", type=float, default=None, help="ncu dram bytes per launch of the dominant kernel")
     args = ap.parse_args()

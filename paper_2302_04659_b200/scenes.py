@@ -388,7 +388,9 @@ def config_e(clay_only: bool = True, slab=(50, 200, 100), grid: int = 256) -> Sc
                                     **soft_contact()))
     env.bodies = bodies
     env.shapes = shapes
-    return Scene(name="E", dims=(grid, grid, grid), h=0.005, dt=1e-4, materials=materials,
+    # App. B: 5e-4, halved to 2.5e-4 because the stiff clay inverts at 5e-4 (det F <= 0 in
+    # the first env step); 2.5e-4 runs without CFL halvings (profiles/r02_experiments_D.txt)
+    return Scene(name="E", dims=(grid, grid, grid), h=0.005, dt=2.5e-4, materials=materials,
                  envs=[env], c_d=0.05)
 
 
