@@ -35,10 +35,15 @@ for cfg, n in (("D", 1024 * 16384), ("E", 4000000)):
     if not os.path.exists(p):
         continue
     t = open(p).read()
+    if "dram__bytes_read.sum" not in t or "Gbyte" not in t:
+        continue
     r = float(re.search(r"dram__bytes_read.sum ([\d.]+) Gbyte", t).group(1))
     w = float(re.search(r"dram__bytes_write.sum ([\d.]+) Gbyte", t).group(1))
     out[cfg] = {"dram_bytes_per_particle_per_fused_launch": (r + w) * 1e9 / n, "git_sha": sha, "capture": p,
                 "particles": n}
     print(cfg, "traffic B/particle per fused launch", (r + w) * 1e9 / n)
-json.dump(out, open("profiles/traffic.json", "w"), indent=1)
+old = json.load(open("profiles/traffic.json")) if os.path.exists("profiles/traffic.json") else {}
+old = {k: v for k, v in old.items() if k in ("D", "E")}
+old.update(out)
+json.dump(old, open("profiles/traffic.json", "w"), indent=1)
 PY
