@@ -68,5 +68,17 @@ int main() {
   float smin = vol.samples[0];
   for (float v : vol.samples) smin = v < smin ? v : smin;
   std::printf("fill_fraction %.6f sdf_samples %zu sdf_min %.6f\n", fill[0].fraction, vol.samples.size(), smin);
-  return err < 1e-3 ? 0 : 1;
+
+  // a robot-driven link: the floor follows a per-rigid-step pose schedule (Robot::set_kinematic_pose,
+  // rigid.hpp:142-151), uploaded once for the whole env step; deterministic mode on
+  msim_gpu::set_deterministic(st, true);
+  const int n_rigid = 5;
+  std::vector<std::vector<msim_gpu::LinkPose>> poses(n_rigid);
+  for (int r = 0; r < n_rigid; ++r) poses[r] = {msim_gpu::LinkPose{{1.0, 0.0, 0.0, 0.0}, {0.0, 0.0, 0.102 - 0.0005 * (r + 1)}}};
+  msim_gpu::set_kinematic_schedule(st, poses);
+  msim_gpu::env_step(st, n_rigid, 1);
+  msim_body b{};
+  msim_gpu_read_bodies(st.handle(), 0, &b, 1);
+  std::printf("scheduled_link_z %.6f link_vz %.6f\n", b.t[2], b.v[2]);
+  return err < 1e-3 && std::fabs(b.t[2] - (0.102 - 0.0005 * n_rigid)) < 1e-12 ? 0 : 1;
 }

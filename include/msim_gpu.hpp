@@ -180,4 +180,26 @@ inline void sync_rigid_to_soft(SoftState& st, int env, const std::vector<msim_bo
   check(msim_gpu_sync_bodies(st.handle(), env, bodies.data(), (int)bodies.size()), st.handle());
 }
 
+// Robot-driven links (coupling.hpp:252-258 -> Robot::set_kinematic_pose,
+// rigid.hpp:142-151) for the next env_step: poses[r][i] = {qw, qx, qy, qz, tx, ty, tz}
+// of body i (all envs concatenated) at rigid step r. One upload per env step.
+struct LinkPose {
+  double q[4];
+  double t[3];
+};
+inline void set_kinematic_schedule(SoftState& st, const std::vector<std::vector<LinkPose>>& poses,
+                                   const std::vector<uint8_t>* mask = nullptr) {
+  std::vector<double> flat;
+  for (const auto& row : poses)
+    for (const LinkPose& p : row) {
+      flat.insert(flat.end(), p.q, p.q + 4);
+      flat.insert(flat.end(), p.t, p.t + 3);
+    }
+  check(msim_gpu_set_kinematic_schedule(st.handle(), (int)poses.size(), flat.data(), mask ? mask->data() : nullptr),
+        st.handle());
+}
+
+// Bit-reproducible stepping (the reference's scheduling-independence, mpm.hpp:7-8).
+inline void set_deterministic(SoftState& st, bool on) { check(msim_gpu_set_deterministic(st.handle(), on ? 1 : 0), st.handle()); }
+
 }  // namespace msim_gpu

@@ -23,3 +23,6 @@ def test_cpp_drop_in_runs_on_device():
     assert float(fields[7]) < 0.0  # the floor pushes the clay up: reaction on the body points down
     assert fields[8] == "fill_fraction" and float(fields[9]) == 1.0  # every particle inside the domain box
     assert int(fields[11]) > 0 and -0.011 < float(fields[13]) < -0.008  # box SDF minimum ~ -half_z
+    # the scheduled link (set_kinematic_schedule) and deterministic mode through the C++ mirror
+    assert fields[14] == "scheduled_link_z" and abs(float(fields[15]) - (0.102 - 0.0005 * 5)) < 1e-6
+    assert fields[16] == "link_vz" and float(fields[17]) < 0.0  # finite-difference twist of the descending link
