@@ -35,13 +35,13 @@ for cfg, n in (("D", 1024 * 16384), ("E", 4000000)):
     if not os.path.exists(p):
         continue
     t = open(p).read()
-    if "dram__bytes_read.sum" not in t or "Gbyte" not in t:
-        continue
-    r = float(re.search(r"dram__bytes_read.sum ([\d.]+) Gbyte", t).group(1))
-    w = float(re.search(r"dram__bytes_write.sum ([\d.]+) Gbyte", t).group(1))
-    out[cfg] = {"dram_bytes_per_particle_per_fused_launch": (r + w) * 1e9 / n, "git_sha": sha, "capture": p,
+    def val(name):
+        m = re.search(name + r" ([\d.]+) (G|M)byte", t)
+        return float(m.group(1)) * (1e9 if m.group(2) == "G" else 1e6)
+    r, w = val("dram__bytes_read.sum"), val("dram__bytes_write.sum")
+    out[cfg] = {"dram_bytes_per_particle_per_fused_launch": (r + w) / n, "git_sha": sha, "capture": p,
                 "particles": n}
-    print(cfg, "traffic B/particle per fused launch", (r + w) * 1e9 / n)
+    print(cfg, "traffic B/particle per fused launch", (r + w) / n)
 old = json.load(open("profiles/traffic.json")) if os.path.exists("profiles/traffic.json") else {}
 old = {k: v for k, v in old.items() if k in ("D", "E")}
 old.update(out)
