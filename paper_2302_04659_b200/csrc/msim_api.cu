@@ -19,6 +19,16 @@
 
 #include "msim_internal.h"
 
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX v3: named ranges for nsys / ncu --nvtx
+
+namespace {
+// NVTX range of one ABI call (no-op without a tool attached).
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
+}  // namespace
+
 using namespace msim_impl;
 using msim_dev::MatParams;
 using msim_dev::ShapeDev;
@@ -553,6 +563,7 @@ void swap_buffers(msim_gpu_ctx* c) {
 // Launch sequence: call_begin -> P2G -> grid, then one fused launch per cycle.
 // The host syncs once at the end (more only when some env halved its step).
 int step_call(msim_gpu_ctx* c, int n_sub, bool integrate_rigid, int n_soft, int32_t* cycles_out) {
+  NvtxRange range(integrate_rigid ? "msim.env_step" : "msim.soft_substep");
   cudaStream_t s = c->stream;
   if (c->n == 0 || n_sub <= 0) return MSIM_OK;
   prepare(c, true);
@@ -631,7 +642,10 @@ int step_call(msim_gpu_ctx* c, int n_sub, bool integrate_rigid, int n_soft, int3
     }
     CK(cudaGetLastError());
     CK(cudaMemcpyAsync(run.data(), c->run_d.p, sizeof(EnvRun) * c->n_env, cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
+    {
+      NvtxRange wait("msim.step_sync");
+      CK(cudaStreamSynchronize(s));
+    }
     c->timer.flush();
     more = 0;
     for (const EnvRun& r : run)
@@ -804,6 +818,7 @@ int msim_gpu_set_bucket_factor(msim_gpu_ctx* c, int factor) {
 int msim_gpu_set_particles(msim_gpu_ctx* c, int64_t n, const int64_t* env_offsets, const double* x,
                            const double* v, const double* F, const double* C, const double* mass,
                            const double* vol0, const int32_t* material) {
+  NvtxRange range("msim.set_particles");
   return guarded(c, [&]() -> int {
     if (n < 0 || n >= INT_MAX / 2) return fail(c, MSIM_ERR_INVALID, "set_particles: particle count out of range");
     if (!env_offsets || env_offsets[0] != 0 || env_offsets[c->n_env] != n)
@@ -1005,6 +1020,7 @@ int msim_gpu_set_deterministic(msim_gpu_ctx* c, int on) {
 }
 
 int msim_gpu_set_kinematic_schedule(msim_gpu_ctx* c, int n_steps, const double* poses, const uint8_t* mask) {
+  NvtxRange range("msim.set_kinematic_schedule");
   return guarded(c, [&]() -> int {
     set_device(c);
     if (n_steps < 1 || !poses) return fail(c, MSIM_ERR_INVALID, "set_kinematic_schedule: need >= 1 rigid step of poses");
@@ -1224,6 +1240,7 @@ int msim_gpu_comm_init(msim_gpu_ctx* c, int rank, int world, const uint8_t* id12
 }
 
 int msim_gpu_step_stats(msim_gpu_ctx* c, int allreduce, double* sums, double* maxs) {
+  NvtxRange range("msim.step_stats");
   return guarded(c, [&]() -> int {
     if (allreduce && !c->comm) return fail(c, MSIM_ERR_INVALID, "step_stats: no communicator (msim_gpu_comm_init)");
     set_device(c);

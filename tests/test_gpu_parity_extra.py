@@ -9,18 +9,23 @@ import numpy as np
 import pytest
 
 from gpu_helpers import rel
-from oracle.oracle_py import OracleWorld
+from oracle import oracle_py
+from oracle.oracle_py import OracleWorld, RefWorld
 from paper_2302_04659_b200 import GpuWorld, SimulationDiverged, abi
 from paper_2302_04659_b200.scenes import (SOFT_CLAY, STIFF_CLAY, V0_SOFT, BodySpec, Scene, ShapeSpec, block_env,
                                           box_sdf_volume, lattice_span, quat_from_axis_angle, soft_contact)
 
 pytestmark = pytest.mark.gpu
 
+# every scenario against the restatement and, where built, the reference's own code (oracle/_ref)
+CHECKERS = [pytest.param(OracleWorld, id="oracle")] + (
+    [pytest.param(RefWorld, id="reference")] if oracle_py.ref_available() else [])
 
-def compare(scene, steps=1, gw=None, envs=None, wrench=True, tol_x=1e-4, tol_v=1e-4):
+
+def compare(scene, steps=1, gw=None, envs=None, wrench=True, tol_x=1e-4, tol_v=1e-4, checker=OracleWorld):
     gw = gw or GpuWorld(scene)
     envs = range(len(scene.envs)) if envs is None else envs
-    ows = {e: OracleWorld(scene, env=e) for e in envs}
+    ows = {e: checker(scene, env=e) for e in envs}
     for _ in range(steps):
         gw.env_step()
         for o in ows.values():
@@ -50,7 +55,8 @@ def small_block(seed, lo=(0.10, 0.10, 0.10), n=(10, 10, 6), v=None, mat=SOFT_CLA
     return env
 
 
-def test_cfl_halving_and_redo_batched():
+@pytest.mark.parametrize("checker", CHECKERS)
+def test_cfl_halving_and_redo_batched(checker):
     """Env 0 crosses the CFL threshold during the step (cycles 1 -> 2: the fused
     P2G speculated dt must be re-done); env 1 halves every substep; env 2 never."""
     envs = [small_block(11), small_block(13, v=(9.0, 0, 0)), small_block(15)]
@@ -58,12 +64,13 @@ def test_cfl_halving_and_redo_batched():
     envs[0].x[:, 2] += 0.30
     envs[1].x[:, 0] -= 0.05
     scene = Scene(name="cfl", dims=(64, 64, 64), h=0.01, dt=5e-4, envs=envs, n_rigid=25)
-    gw, ows, _ = compare(scene)
+    gw, ows, _ = compare(scene, checker=checker)
     cyc = [gw.report(e).cfl_cycles for e in range(3)]
     assert cyc[1] == 50 and cyc[2] == 25 and 25 < cyc[0] < 50, cyc
 
 
-def test_grid_coupling_mode():
+@pytest.mark.parametrize("checker", CHECKERS)
+def test_grid_coupling_mode(checker):
     """penalty_grid (coupling.hpp:186-214): node forces scaled by m_i / mean particle mass."""
     env = small_block(21, lo=(0.10, 0.10, 0.041), n=(10, 10, 7))
     env.v = np.tile([0.02, 0.0, -0.1], (env.n, 1))
@@ -72,10 +79,11 @@ def test_grid_coupling_mode():
     env.shapes = [ShapeSpec(abi.SHAPE_PLANE, 0, params=(0, 0, 1, 0))]
     scene = Scene(name="grid", dims=(32, 32, 32), h=0.01, dt=2e-4, envs=[env], n_rigid=4,
                   coupling_mode=abi.COUPLING_GRID)
-    gw, ows, _ = compare(scene, steps=2)
+    gw, ows, _ = compare(scene, steps=2, checker=checker)
 
 
-def test_all_collider_types_scripted():
+@pytest.mark.parametrize("checker", CHECKERS)
+def test_all_collider_types_scripted(checker):
     """Plane (tilted), sphere, box, capsule and an SDF volume (software trilinear,
     sdf.hpp:46-62) on scripted bodies moving/rotating into a clay slab."""
     env = small_block(31, lo=(0.12, 0.12, 0.03), n=(30, 30, 8))
@@ -99,19 +107,21 @@ def test_all_collider_types_scripted():
     ]
     env.bodies, env.shapes = bodies, shapes
     scene = Scene(name="shapes", dims=(40, 40, 40), h=0.01, dt=5e-4, envs=[env], c_d=0.05)
-    gw, ows, _ = compare(scene, steps=2)
+    gw, ows, _ = compare(scene, steps=2, checker=checker)
     fg, _ = gw.wrenches(0, pending=True)
     assert np.count_nonzero(np.linalg.norm(fg, axis=1)) >= 3  # several colliders in contact
 
 
-def test_slip_boundaries_and_stiff_material():
+@pytest.mark.parametrize("checker", CHECKERS)
+def test_slip_boundaries_and_stiff_material(checker):
     env = small_block(41, lo=(0.10, 0.10, 0.025), n=(12, 12, 6), v=(0.3, -0.2, -0.5), mat=STIFF_CLAY, mid=1)
     scene = Scene(name="slip", dims=(32, 32, 32), h=0.01, dt=2e-4, envs=[env], materials=[SOFT_CLAY, STIFF_CLAY],
                   boundary=(1, 1, 1, 1, 1, 1))
-    compare(scene, steps=2)
+    compare(scene, steps=2, checker=checker)
 
 
-def test_nsoft2_dynamic_body_wrench_quirk():
+@pytest.mark.parametrize("checker", CHECKERS)
+def test_nsoft2_dynamic_body_wrench_quirk(checker):
     """n_soft = 2: wrenches summed over both substeps, applied once with
     dt_rigid = n_soft dt at the next rigid step (coupling.hpp:248-251, :288)."""
     env = small_block(51, lo=(0.10, 0.10, 0.06), n=(10, 10, 7))
@@ -119,20 +129,21 @@ def test_nsoft2_dynamic_body_wrench_quirk():
     env.bodies = [ball]
     env.shapes = [ShapeSpec(abi.SHAPE_SPHERE, 0, params=(0.015,))]
     scene = Scene(name="nsoft2", dims=(32, 32, 32), h=0.01, dt=2e-4, envs=[env], n_rigid=5, n_soft=2)
-    gw, ows, _ = compare(scene, steps=6)
+    gw, ows, _ = compare(scene, steps=6, checker=checker)
     bg, bo = gw.bodies(0)[0], ows[0].bodies()[0]
     assert np.allclose(np.array(bg.t), np.array(bo.t), atol=1e-7)
     assert abs(bg.v[2] - bo.v[2]) <= 1e-3 * abs(bo.v[2])
 
 
-def test_particles_leaving_domain_are_frozen():
+@pytest.mark.parametrize("checker", CHECKERS)
+def test_particles_leaving_domain_are_frozen(checker):
     """Lost particles: frozen with v = 0 and counted once (mpm.hpp:239-245)."""
     env = small_block(61, lo=(0.03, 0.10, 0.10), n=(8, 8, 8), v=(-0.5, 0, 0))
     env.x[:7, 0] = -0.05  # outside the grid: flagged by the first P2G
     env.x[7:9, 2] = 0.5
     scene = Scene(name="lost", dims=(32, 32, 32), h=0.01, dt=5e-4, envs=[env], gravity=(0, 0, 0),
                   lost_fraction_threshold=1.0, n_rigid=25)
-    gw, ows, _ = compare(scene, steps=2)
+    gw, ows, _ = compare(scene, steps=2, checker=checker)
     assert gw.lost_count(0) == ows[0].lost_count() > 0
 
 
