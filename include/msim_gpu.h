@@ -154,8 +154,12 @@ typedef struct msim_coupling {
   double c_d;                      /* 10 */
 } msim_coupling;
 
-/* StepReport (coupling.hpp:41-50), rigid/soft fields; summed/maxed over
- * environments for batched contexts (per-env values via msim_gpu_read_report). */
+/* StepReport (coupling.hpp:41-50), rigid/soft fields. For a batched context
+ * msim_gpu_env_step aggregates over the environments: cfl_cycles = the MAX over
+ * envs of each env's cycle count (the reference's per-World count, summed over
+ * its substeps), max_penetration / max_force_balance_error = max over envs,
+ * lost_particles = sum over envs. Per-env values: msim_gpu_read_report; the
+ * sum over envs of cfl_cycles: msim_gpu_step_stats. */
 typedef struct msim_step_report {
   int32_t rigid_steps;
   int32_t soft_substeps;
