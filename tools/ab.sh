@@ -1,0 +1,8 @@
+#!/bin/bash
+# usage: ab.sh envs steps variant...   (base = in-tree lib); two alternating passes
+envs=$1; steps=$2; shift 2
+for pass in 1 2; do
+for v in base "$@"; do
+  if [ $v = base ]; then lib=paper_2302_04659_b200/libmsim_gpu.so; else lib=paper_2302_04659_b200/build/$v/libmsim_gpu.so; fi
+  MSIM_GPU_LIB=$lib python bench.py --steps $steps --warmup 3 --envs $envs --no-cpu-baseline 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.readlines()[-1]); print('$v', round(d['kernels']['k_particles']['avg_ms'],4), 'ms/launch', round(d['value']/1e9,3), 'G', d['clocks']['sm_mhz'])"
+done; done
