@@ -92,6 +92,7 @@ struct msim_gpu_ctx {
   int n_keys = 0;
   int qf = 0;          // particle bucket = qf^3 node blocks (set_bucket_shape)
   int qf_request = 0;  // 0: chosen from the particle density at set_particles
+  int split_r = 1;     // particle-kernel items per bucket (set_particles: small scenes > 1)
   int qdims[3] = {0, 0, 0};
   int buckets_per_env = 0;
 
@@ -225,6 +226,7 @@ SimParams params(msim_gpu_ctx* c) {
   P.any_model = 0;
   for (const auto& m : c->mats_h) P.any_model |= m.model != MSIM_MODEL_HENCKY_VON_MISES;
   P.split = split_mode(c) ? 1 : 0;
+  P.split_r = c->det ? 1 : c->split_r;  // deterministic mode keeps stable in-kernel ranks
   P.grid_mode = c->coupling.mode == MSIM_COUPLING_GRID;
   P.r_c_particle = (float)(c->coupling.r_c_factor * d.h);
   P.r_c_grid = (float)std::max(c->coupling.r_c_factor * d.h, 0.65 * d.h);
@@ -841,6 +843,15 @@ int msim_gpu_set_particles(msim_gpu_ctx* c, int64_t n, const int64_t* env_offset
         f = ppc < 6.0 ? 2 : 1;  // < ~190 particles in a 32-cell bucket: use 8x8x4-cell buckets
       }
       set_bucket_shape(c, f);
+    }
+    {  // a scene too small to give every resident particle-kernel CTA a round of its
+       // own: a bucket's rounds are spread over split_r CTAs (interleaved)
+      int sms = 148;
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
+      const double slots = (double)sms * kParticleCtasPerSm * kParticleRound;
+      int r = n > 0 ? (int)std::ceil(slots / (double)n) : 1;
+      if (const char* ev = std::getenv("MSIM_SPLIT_R")) r = std::atoi(ev);  // tuning override
+      c->split_r = std::max(1, std::min(r, 8));
     }
     c->n = n;
     c->cur = 0;

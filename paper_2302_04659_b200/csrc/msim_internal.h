@@ -57,6 +57,9 @@ struct EnvRun {
 constexpr int kDetWrenchExp = 36;
 constexpr int kDetMomentumExp = 40;  // |largest round bound| ~ 2^-40 of the int64 range per contribution
 constexpr int kErrDetRange = 33;     // deterministic fixed-point range exceeded (a contribution grew ~2^15x in one step)
+// Resident particle-kernel rounds on the device (default build: 5 CTAs / SM x 128
+// particles), for the small-scene split heuristic (msim_gpu_set_particles).
+constexpr int kParticleCtasPerSm = 5, kParticleRound = 128;
 
 // Internal error codes latched per environment (first one wins); mapped to
 // MSIM_ERR_INVALID / MSIM_ERR_DIVERGED with the reference's messages.
@@ -197,6 +200,7 @@ struct SimParams {
   int n_blocks;              // n_env*blocks_per_env (node-block flags)
   int any_model;             // some material is not the reference's von Mises clay (jp + dispatch)
   int split;                 // keep momentum and force separately
+  int split_r;               // rounds of a bucket split over this many CTAs (small scenes; >= 1)
   int grid_mode;             // coupling mode grid
   float r_c_particle, r_c_grid, c_d;
   double dt_full;            // SoftState::dt

@@ -141,6 +141,7 @@ struct ItemCtx {
   int key, benv, s, e, act, ox, oy, oz, s0, s1;
   float dt, dtp;
   int lostb, do_g2p, do_p2g, penalty;
+  int rstep;           // slot stride between this item's rounds (CAP x split_r)
   unsigned smask;      // env shapes (bit k = shape s0 + k, k < 32) that can reach the bucket box
   float blo[3], bhi[3];  // the bucket's particles' box widened by 2 h (positions after G2P)
 };
@@ -249,7 +250,7 @@ __device__ __forceinline__ void item_rounds(const SimParams& P, Smem<NCH, F>& S,
   volatile ItemCtx& IC = S.ic;
   {
     int stay_base = 0;  // particles of this bucket that stay in it, so far (CTA-uniform)
-    for (int r0 = IC.s, rpar = 0; r0 < IC.e; r0 += CAP, rpar ^= 1) {
+    for (int r0 = IC.s, rpar = 0; r0 < IC.e; r0 += IC.rstep, rpar ^= 1) {
       const int rn = min(CAP, IC.e - r0);
       const int trips = (rn + kT - 1) / kT;
       float mx_m = 0.f, mx_p = 0.f, mx_f = 0.f;
@@ -260,7 +261,7 @@ __device__ __forceinline__ void item_rounds(const SimParams& P, Smem<NCH, F>& S,
         const int j = r0 + t;
         const int i = valid ? P.perm[j] : 0;
 #ifndef MSIM_NO_L2_PREFETCH  // L2 prefetch of this thread's next particle, one trip ahead (-1 %)
-        const int i_pf = j + kT < IC.e ? P.perm[j + kT] : -1;
+        const int i_pf = j + IC.rstep < IC.e ? P.perm[j + IC.rstep] : -1;
 #endif
         unsigned meta = valid ? lds(&P.cur.meta[i]) : (1u << kLostBit);
         const int penv = (meta >> 8) & kEnvMask;
@@ -573,7 +574,8 @@ __device__ __forceinline__ void item_rounds(const SimParams& P, Smem<NCH, F>& S,
           {  // next bucket key. Particles staying in this bucket keep their order: their
              // ranks are prefix counts in slot order, set after the round's barrier. The
              // (rare) movers take atomic ranks counted back from the end of their new bucket.
-            const bool stay = valid && key_new == IC.key;
+            // (split buckets: every particle takes an atomic rank, see particles_cta)
+            const bool stay = valid && key_new == IC.key && (P.split_r == 1 || IC.lostb);
             const unsigned sb = __ballot_sync(FULL, stay);
             if (lane == 0) S.wball[rpar][t >> 5] = sb;
             const unsigned am = __ballot_sync(FULL, valid && !stay);
@@ -808,7 +810,13 @@ __device__ __forceinline__ void particles_cta(const SimParams& P, unsigned char*
   Smem<NCH, F>& S = *reinterpret_cast<Smem<NCH, F>*>(smem_raw);
   const int tid = threadIdx.x;
   if (redo && !*P.any_redo) return;
-  const int nitems = *P.n_active_buckets;
+  // Small scenes (split_r > 1): item = (bucket, part), part p taking the bucket's
+  // rounds p, p + split_r, ... Stayers then cannot be ranked in order across
+  // CTAs: every particle takes an atomic rank from its bucket's end (the
+  // deterministic mode's mover sort restores the slot order). The lost bucket is
+  // not split (its particles stay in order).
+  const int R = P.split_r;
+  const int nitems = *P.n_active_buckets * R;
 
   for (int t = tid; t < NCH * PN; t += kT) (&S.itile[0][0])[t] = 0;
   for (int t = tid; t < Gm::NBT; t += kT) S.bflag[t] = 0;
@@ -818,10 +826,12 @@ __device__ __forceinline__ void particles_cta(const SimParams& P, unsigned char*
   // atomic per further bucket): their sizes vary, and a static round-robin
   // leaves a tail of CTAs with more work (-12 % per launch at D).
   for (int item = cta; item < nitems;) {
-    const int key = P.active_buckets[item];
+    const int bi = R > 1 ? item / R : item, part = item - bi * R;
+    const int key = P.active_buckets[bi];
     const bool lostb = key == P.n_keys - 1;
     const int benv = lostb ? 0 : key / P.buckets_per_env;
-    if (redo && (lostb || !P.run[benv].redo)) {  // CTA-uniform
+    const int s = P.bucket_start[key] + part * CAP, e = P.bucket_start[key + 1];
+    if ((redo && (lostb || !P.run[benv].redo)) || s >= e || (lostb && part > 0)) {  // CTA-uniform
       __syncthreads();
       if (tid == 0)
         S.next_item = ncta + (kDynamicItems ? atomicAdd(P.item_counter + redo, 1) : item);
@@ -829,7 +839,6 @@ __device__ __forceinline__ void particles_cta(const SimParams& P, unsigned char*
       item = S.next_item;
       continue;
     }
-    const int s = P.bucket_start[key], e = P.bucket_start[key + 1];
     const int act = lostb ? kActIdle : P.run[benv].action;
     const bool do_g2p = act == kActFused || act == kActG2P;
     const bool do_p2g = act == kActP2G || act == kActFused;
@@ -872,7 +881,7 @@ __device__ __forceinline__ void particles_cta(const SimParams& P, unsigned char*
     if (tid < 6) (&S.maxb[0][0])[tid] = 0u;
     if (tid == 0) {
       S.penmax = 0u;
-      IC.key = key; IC.benv = benv; IC.s = s; IC.e = e; IC.act = act;
+      IC.key = key; IC.benv = benv; IC.s = s; IC.e = e; IC.act = act; IC.rstep = (lostb ? 1 : R) * CAP;
       IC.ox = ox; IC.oy = oy; IC.oz = oz; IC.s0 = s0; IC.s1 = s1;
       IC.dt = dt; IC.dtp = dtp;
       IC.lostb = lostb; IC.do_g2p = do_g2p; IC.do_p2g = do_p2g; IC.penalty = penalty;
@@ -1287,22 +1296,36 @@ __device__ void iter_end_env(const SimParams& P, int env) {
   }
   if (P.err_code[env]) r.substeps_left = 0;
 }
-__global__ void k_iter_end(SimParams P) {
-  const int env = blockIdx.x * blockDim.x + threadIdx.x;
-  if (env < P.n_env) iter_end_env(P, env);
-}
-
-// Redo pass, step 1: zero the P2G accumulators of envs whose speculated dt
-// missed (their node blocks are in the node-block list of this launch).
-__device__ void redo_clear_range(const SimParams& P, long long gtid, long long gthreads) {
-  if (!*P.any_redo) return;
+// One CTA per env: thread 0 runs the env's state machine; when the speculated
+// dt of the fused P2G missed (redo), the CTA zeroes the env's P2G accumulators
+// right away (its node blocks: a contiguous range of the ascending node-block
+// list) for the redo pass.
+constexpr int kIterEndThreads = 128;
+__global__ void __launch_bounds__(kIterEndThreads) k_iter_end(SimParams P) {
+  const int env = blockIdx.x, lane = threadIdx.x;
+  __shared__ int redo;
+  if (lane == 0) {
+    iter_end_env(P, env);
+    redo = P.run[env].redo;
+  }
+  __syncthreads();
+  if (!redo) return;
   const int nlist = *P.n_nb;
+  auto lower = [&](int key) {  // first list entry >= key
+    int lo = 0, hi = nlist;
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (P.nb_list[mid] < key) lo = mid + 1;
+      else hi = mid;
+    }
+    return lo;
+  };
+  const int a = lower(env * P.blocks_per_env), b = lower((env + 1) * P.blocks_per_env);
   const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
   constexpr int NB = kBX * kBY * kBZ;
-  for (long long t = gtid; t < (long long)nlist * NB; t += gthreads) {
-    const int nb = P.nb_list[t / NB], l = (int)(t % NB);
-    const int env = nb / P.blocks_per_env, lb = nb - env * P.blocks_per_env;
-    if (!P.run[env].redo) continue;
+  for (long long q = (long long)a * NB + lane; q < (long long)b * NB; q += kIterEndThreads) {
+    const int nb = P.nb_list[q / NB], l = (int)(q % NB);
+    const int lb = nb - env * P.blocks_per_env;
     const int gx = kBX * (lb % P.bdims[0]) + l % kBX, gy = kBY * ((lb / P.bdims[0]) % P.bdims[1]) + (l / kBX) % kBY,
               gz = kBZ * (lb / (P.bdims[0] * P.bdims[1])) + l / (kBX * kBY);
     if (gx >= P.dims[0] || gy >= P.dims[1] || gz >= P.dims[2]) continue;
@@ -1310,9 +1333,6 @@ __device__ void redo_clear_range(const SimParams& P, long long gtid, long long g
     P.gPM[gi] = z;
     if (P.det) P.gPMd[gi] = make_longlong4(0, 0, 0, 0);
   }
-}
-__global__ void k_redo_clear(SimParams P) {
-  redo_clear_range(P, blockIdx.x * (long long)blockDim.x + threadIdx.x, (long long)gridDim.x * blockDim.x);
 }
 
 inline unsigned nblk(long long n, int t = 256) { return (unsigned)((n + t - 1) / t); }
@@ -1444,7 +1464,7 @@ void launch_grid(const SimParams& P, cudaStream_t s) {
 
 void launch_iteration_end(const SimParams& P, cudaStream_t s) {
   Timed tm(P, kKEnd, s);
-  k_iter_end<<<nblk(P.n_env), 256, 0, s>>>(P);
+  k_iter_end<<<P.n_env, kIterEndThreads, 0, s>>>(P);
 }
 
 void launch_iteration(const SimParams& P, bool bookkeeping, bool grid_update, cudaStream_t s) {
@@ -1453,15 +1473,11 @@ void launch_iteration(const SimParams& P, bool bookkeeping, bool grid_update, cu
     k_iter_begin<<<nblk(32LL * P.n_env), 256, 0, s>>>(P);
   }
   launch_particles(P, s);
-  {
-    Timed tm(P, kKEnd, s);
-    k_iter_end<<<nblk(P.n_env), 256, 0, s>>>(P);
-  }
+  launch_iteration_end(P, s);  // also zeroes the accumulators of envs that redo
   if (bookkeeping && !P.split) {
     // speculated-dt misses (CFL halving changed between substeps): redo those envs' P2G.
-    // Both kernels exit immediately when no env needs it.
-    Timed tm(P, kKRedo, s, 2);
-    k_redo_clear<<<sm_count() * 2, 256, 0, s>>>(P);
+    // Exits immediately when no env needs it.
+    Timed tm(P, kKRedo, s, 1);
     SimParams Q = P;
     Q.redo_pass = 1;
     particle_kernel(Q, s);

@@ -47,8 +47,13 @@ def _compare_env(gw, e, ref, rg, rr, label):
     return ex, ev
 
 
+@pytest.mark.parametrize("split", ["auto", "1"])
 @pytest.mark.parametrize("name", ["A", "B", "C"])
-def test_single_scene_one_env_step_matches_reference(name):
+def test_single_scene_one_env_step_matches_reference(name, split, monkeypatch):
+    """split: the particle kernel's bucket split for small scenes (auto: a bucket's
+    rounds over several CTAs with atomic ranks; 1: one CTA per bucket, stable ranks)."""
+    if split != "auto":
+        monkeypatch.setenv("MSIM_SPLIT_R", split)
     scene = {"A": config_a, "B": config_b, "C": config_c}[name]()
     gw, ref = GpuWorld(scene), RefWorld(scene)
     rg, rr = gw.env_step(), ref.env_step()
