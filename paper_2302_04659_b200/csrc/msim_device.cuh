@@ -19,6 +19,12 @@
 
 namespace msim_dev {
 
+// Programmatic dependent launch (msim_internal.h launch_pdl): wait for the
+// predecessor grid (complete, writes visible); allow the successor grid to be
+// scheduled. Both are no-ops in a kernel launched without the attribute.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 // ---------------------------------------------------------------------------
 // Small fp32 vector / matrix helpers (row-major 3x3 in registers).
 

@@ -57,6 +57,34 @@ struct EnvRun {
 constexpr int kDetWrenchExp = 36;
 constexpr int kDetMomentumExp = 40;  // |largest round bound| ~ 2^-40 of the int64 range per contribution
 constexpr int kErrDetRange = 33;     // deterministic fixed-point range exceeded (a contribution grew ~2^15x in one step)
+// Programmatic dependent launch (sm_90+) of the per-cycle kernels: each is
+// scheduled while its predecessor drains (the launch latency overlaps) and
+// waits in pdl_wait() (griddepcontrol.wait: predecessor complete, its writes
+// visible) before touching global memory. Kernels launched this way start with
+// pdl_wait(); pdl_trigger() lets their own successor be scheduled. Stream
+// capture records the programmatic edges in the CUDA graph. MSIM_NO_PDL=1
+// launches them plainly (the device calls are then no-ops).
+bool pdl_enabled();
+template <typename... Params, typename... Args>
+inline void launch_pdl(void (*kern)(Params...), unsigned grid, unsigned block, size_t smem, cudaStream_t s,
+                       Args... args) {
+  if (!pdl_enabled()) {
+    kern<<<grid, block, smem, s>>>(args...);
+    return;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kern, args...);
+}
+
 // Resident particle-kernel rounds on the device (default build: 5 CTAs / SM x 128
 // particles), for the small-scene split heuristic (msim_gpu_set_particles).
 constexpr int kParticleCtasPerSm = 5, kParticleRound = 128;

@@ -300,6 +300,8 @@ __device__ __forceinline__ unsigned long long st_pack(unsigned long long flag, i
 }
 __global__ void __launch_bounds__(256) k_scan_1pass(int* in, int n, int* out, int* list, int* n_list, int ntiles,
                                                    unsigned long long* status, unsigned* ctr) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ int tile_s, pre_s, pre_c;
   __shared__ bool last_s;
   if (threadIdx.x == 0) tile_s = (int)atomicAdd(&ctr[0], 1u);
@@ -379,8 +381,8 @@ void scan_exclusive(int* in, int* out, int n, int* list, int* n_list, int* tmp, 
   if (ntiles == 0) ntiles = 1;
   // one launch: decoupled look-back over the tiles (status words + counters in tmp,
   // zero between calls: the last tile to finish resets them)
-  k_scan_1pass<<<ntiles, 256, 0, s>>>(in, n, out, list, n_list, ntiles, reinterpret_cast<unsigned long long*>(tmp),
-                                      reinterpret_cast<unsigned*>(tmp + 2 * ntiles));
+  launch_pdl(k_scan_1pass, ntiles, 256, 0, s, in, n, out, list, n_list, ntiles,
+             reinterpret_cast<unsigned long long*>(tmp), reinterpret_cast<unsigned*>(tmp + 2 * ntiles));
 }
 
 void launch_convert_in(const SimParams& P, long long n, const double* x, const double* v,

@@ -42,6 +42,7 @@
 #include <cuda_runtime.h>
 
 #include <cfloat>
+#include <cstdlib>
 
 #include "msim_common.cuh"
 
@@ -915,6 +916,8 @@ __device__ __forceinline__ void particles_cta(const SimParams& P, unsigned char*
 
 template <int NCH, int F, bool AM, bool DET>
 __global__ void __launch_bounds__(kT, kCtasPerSm) k_particles(SimParams P) {
+  pdl_wait();
+  pdl_trigger();
   extern __shared__ __align__(16) unsigned char smem_raw[];
   particles_cta<NCH, F, AM, DET>(P, smem_raw, P.redo_pass != 0, (int)blockIdx.x, (int)gridDim.x);
 }
@@ -922,6 +925,8 @@ __global__ void __launch_bounds__(kT, kCtasPerSm) k_particles(SimParams P) {
 // Bucket keys of stored positions (after uploads): no loss flagging here, a
 // particle outside the domain is flagged by the next P2G (mpm.hpp:226-245).
 __global__ void __launch_bounds__(256) k_rebin(SimParams P) {
+  pdl_wait();
+  pdl_trigger();
   const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   const bool valid = i < P.n;
   int key = P.n_keys - 1;
@@ -960,6 +965,8 @@ __device__ __forceinline__ void perm_at(const SimParams& P, long long i) {
   P.perm_w[(r >= 0 ? P.bucket_start_w[k] : P.bucket_start_w[k + 1]) + r] = (int)i;
 }
 __global__ void k_perm(SimParams P) {
+  pdl_wait();
+  pdl_trigger();
   const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (i < P.n) perm_at(P, i);
 }
@@ -969,6 +976,8 @@ __global__ void k_perm(SimParams P) {
 // order -- hence every fixed-point scale and every sum -- is reproducible.
 // One CTA per bucket; each mover's position = #movers with a smaller slot.
 __global__ void __launch_bounds__(128) k_det_sort_movers(SimParams P) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ int tail[1024];
   for (int k = blockIdx.x; k < P.n_keys; k += gridDim.x) {
     const int cnt = P.move_count[k];
@@ -1117,6 +1126,8 @@ __device__ __forceinline__ void grid_items(const SimParams& P, const int gtid, c
 }
 
 __global__ void __launch_bounds__(256) k_grid(SimParams P) {
+  pdl_wait();
+  pdl_trigger();
   grid_items(P, (int)(blockIdx.x * blockDim.x + threadIdx.x), (int)(gridDim.x * blockDim.x));
 }
 
@@ -1200,6 +1211,8 @@ __device__ void call_begin_env(const SimParams& P, int env, int n_sub, int first
 }
 
 __global__ void k_call_begin(SimParams P, int n_sub, int first_action) {
+  pdl_wait();
+  pdl_trigger();
   const int t = blockIdx.x * blockDim.x + threadIdx.x, env = t >> 5;
   if (t == 0) *P.any_redo = 0;
   if (env < P.n_env) call_begin_env(P, env, n_sub, first_action, t & 31);
@@ -1247,6 +1260,8 @@ __device__ void iter_begin_env(const SimParams& P, int env, int lane) {
   }
 }
 __global__ void k_iter_begin(SimParams P) {
+  pdl_wait();
+  pdl_trigger();
   const int t = blockIdx.x * blockDim.x + threadIdx.x, env = t >> 5;
   if (t == 0) *P.any_redo = 0;
   if (env < P.n_env) iter_begin_env(P, env, t & 31);
@@ -1302,6 +1317,8 @@ __device__ void iter_end_env(const SimParams& P, int env) {
 // list) for the redo pass.
 constexpr int kIterEndThreads = 128;
 __global__ void __launch_bounds__(kIterEndThreads) k_iter_end(SimParams P) {
+  pdl_wait();
+  pdl_trigger();
   const int env = blockIdx.x, lane = threadIdx.x;
   __shared__ int redo;
   if (lane == 0) {
@@ -1369,7 +1386,7 @@ void launch_k_particles(const SimParams& P, cudaStream_t s) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_particles<NCH, F, AM, DET>, kT, sizeof(Smem<NCH, F>));
     if (per_sm <= 0) per_sm = 1;
   }
-  k_particles<NCH, F, AM, DET><<<sm_count() * per_sm, kT, sizeof(Smem<NCH, F>), s>>>(P);
+  launch_pdl(k_particles<NCH, F, AM, DET>, sm_count() * per_sm, kT, sizeof(Smem<NCH, F>), s, P);
 }
 
 template <bool AM>
@@ -1395,6 +1412,14 @@ void particle_kernel(const SimParams& P, cudaStream_t s) {
 
 }  // namespace
 
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("MSIM_NO_PDL");
+    return !(e && *e && *e != '0');
+  }();
+  return on;
+}
+
 void configure_kernels() {
 #define MSIM_SET_SMEM(NCH, F, AM, DET)                                                              \
   cudaFuncSetAttribute(k_particles<NCH, F, AM, DET>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
@@ -1410,7 +1435,7 @@ void configure_kernels() {
 void launch_rebin(const SimParams& P, cudaStream_t s) {
   {
     Timed tm(P, kKBin, s);
-    if (P.n > 0) k_rebin<<<nblk(P.n), 256, 0, s>>>(P);
+    if (P.n > 0) launch_pdl(k_rebin, nblk(P.n), 256, 0, s, P);
   }
   // keys of the stored positions describe the NEXT particle launch: write the read set
   SimParams Q = P;
@@ -1420,8 +1445,8 @@ void launch_rebin(const SimParams& P, cudaStream_t s) {
   Q.n_active_buckets_w = P.n_active_buckets;
   Timed tm(P, kKBucketScan, s, P.det ? 3 : 2);
   scan_exclusive(Q.bucket_count, Q.bucket_start_w, Q.n_keys, Q.active_buckets_w, Q.n_active_buckets_w, Q.scan_tmp, s);
-  if (Q.n > 0) k_perm<<<nblk(Q.n), 256, 0, s>>>(Q);
-  if (Q.det) k_det_sort_movers<<<sm_count() * 8, 128, 0, s>>>(Q);
+  if (Q.n > 0) launch_pdl(k_perm, nblk(Q.n), 256, 0, s, Q);
+  if (Q.det) launch_pdl(k_det_sort_movers, sm_count() * 8, 128, 0, s, Q);
 }
 
 void launch_clear(const SimParams& P, cudaStream_t s) {
@@ -1435,7 +1460,7 @@ void launch_set_action(const SimParams& P, int action, float dt, cudaStream_t s)
 
 void launch_call_begin(const SimParams& P, int n_sub, int first_action, cudaStream_t s) {
   Timed tm(P, kKPlan, s);
-  k_call_begin<<<nblk(32LL * P.n_env), 256, 0, s>>>(P, n_sub, first_action);
+  launch_pdl(k_call_begin, nblk(32LL * P.n_env), 256, 0, s, P, n_sub, first_action);
 }
 
 void launch_particles(const SimParams& P, cudaStream_t s) {
@@ -1450,8 +1475,8 @@ void launch_particles(const SimParams& P, cudaStream_t s) {
     // the next launch's bucket structure goes to the write set: the redo pass of this
     // launch still reads this launch's perm / bucket offsets
     scan_exclusive(P.bucket_count, P.bucket_start_w, P.n_keys, P.active_buckets_w, P.n_active_buckets_w, P.scan_tmp, s);
-    if (P.n > 0) k_perm<<<nblk(P.n), 256, 0, s>>>(P);
-    if (P.det) k_det_sort_movers<<<sm_count() * 8, 128, 0, s>>>(P);
+    if (P.n > 0) launch_pdl(k_perm, nblk(P.n), 256, 0, s, P);
+    if (P.det) launch_pdl(k_det_sort_movers, sm_count() * 8, 128, 0, s, P);
   }
   Timed tm(P, kKBlockScan, s, 1);
   scan_exclusive(P.nb_flag, P.nb_scan, P.n_blocks, P.nb_list, P.n_nb, P.scan_tmp, s);
@@ -1459,18 +1484,18 @@ void launch_particles(const SimParams& P, cudaStream_t s) {
 
 void launch_grid(const SimParams& P, cudaStream_t s) {
   Timed tm(P, kKGrid, s);
-  k_grid<<<sm_count() * 8, 256, 0, s>>>(P);
+  launch_pdl(k_grid, sm_count() * 8, 256, 0, s, P);
 }
 
 void launch_iteration_end(const SimParams& P, cudaStream_t s) {
   Timed tm(P, kKEnd, s);
-  k_iter_end<<<P.n_env, kIterEndThreads, 0, s>>>(P);
+  launch_pdl(k_iter_end, P.n_env, kIterEndThreads, 0, s, P);
 }
 
 void launch_iteration(const SimParams& P, bool bookkeeping, bool grid_update, cudaStream_t s) {
   if (bookkeeping) {
     Timed tm(P, kKRigid, s);
-    k_iter_begin<<<nblk(32LL * P.n_env), 256, 0, s>>>(P);
+    launch_pdl(k_iter_begin, nblk(32LL * P.n_env), 256, 0, s, P);
   }
   launch_particles(P, s);
   launch_iteration_end(P, s);  // also zeroes the accumulators of envs that redo
