@@ -93,6 +93,7 @@ struct msim_gpu_ctx {
   int qf = 0;          // particle bucket = qf^3 node blocks (set_bucket_shape)
   int qf_request = 0;  // 0: chosen from the particle density at set_particles
   int split_r = 1;     // particle-kernel items per bucket (set_particles: small scenes > 1)
+  size_t scan_tmp_half = 0;  // ints per scan status area (scan_tmp_d holds two)
   int qdims[3] = {0, 0, 0};
   int buckets_per_env = 0;
 
@@ -298,6 +299,7 @@ SimParams params(msim_gpu_ctx* c) {
   P.nb_list = c->nb_list_d.as<int>();
   P.n_nb = c->n_nb_d.as<int>();
   P.scan_tmp = c->scan_tmp_d.as<int>();
+  P.scan_tmp2 = P.scan_tmp + c->scan_tmp_half;
   P.balance_max = c->balance_d.as<double>();
   P.lost_threshold = d.lost_fraction_threshold;
   return P;
@@ -386,8 +388,10 @@ void set_bucket_shape(msim_gpu_ctx* c, int f) {
   CK(cudaMemset(c->bucket_count_d.p, 0, sizeof(int) * c->n_keys));
   const long long scan_n = std::max<long long>(std::max(c->n_keys, c->n_env * c->blocks_per_env),
                                                std::min<long long>(c->nodes_per_env + 1, INT_MAX));
-  CK(c->scan_tmp_d.ensure(sizeof(int) * scan_tmp_ints((int)scan_n)));
-  CK(cudaMemset(c->scan_tmp_d.p, 0, sizeof(int) * scan_tmp_ints((int)scan_n)));  // single-pass scan status
+  // two status areas: the node-block scan runs concurrently with the bucket scan
+  c->scan_tmp_half = scan_tmp_ints((int)scan_n);
+  CK(c->scan_tmp_d.ensure(sizeof(int) * 2 * c->scan_tmp_half));
+  CK(cudaMemset(c->scan_tmp_d.p, 0, sizeof(int) * 2 * c->scan_tmp_half));  // single-pass scan status
   CK(cudaDeviceSynchronize());
   c->perm_valid = false;
 }

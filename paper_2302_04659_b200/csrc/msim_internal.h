@@ -299,6 +299,7 @@ struct SimParams {
   int* n_nb;
 
   int* scan_tmp;
+  int* scan_tmp2;  // second scan status area (the node-block scan, concurrent with the bucket scan)
   // deterministic mode (null otherwise)
   int det;
   longlong4* gPMd;               // per node: int64 momentum (or p + dt f) xyz, mass
@@ -332,8 +333,11 @@ void launch_clear_env_grid(const SimParams& P, int env, cudaStream_t s);
 void launch_binning_out(const SimParams& P, long long n_env_p, const int* base, int* cell_count,
                         int* cell_start, int* cell_particles, int* node_flag, int* node_scan,
                         int* node_list, int* n_list, long long* active_nodes, int* tmp, cudaStream_t s);
+// early: the scan's input is complete before its stream predecessor finishes
+// (launched with programmatic dependent launch, it runs concurrently with the
+// predecessor and waits for it only before exiting; tmp must not be shared)
 void scan_exclusive(int* in, int* out, int n, int* compact_list, int* n_compact, int* tmp,
-                    cudaStream_t s);
+                    cudaStream_t s, bool early = false);
 size_t scan_tmp_ints(int n);
 
 // ---- hot path (msim_substep.cu)

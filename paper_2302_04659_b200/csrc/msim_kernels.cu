@@ -298,9 +298,10 @@ constexpr unsigned long long kStAgg = 1ull << 62, kStIncl = 2ull << 62;
 __device__ __forceinline__ unsigned long long st_pack(unsigned long long flag, int s, int c) {
   return flag | ((unsigned long long)(unsigned)s << 31) | (unsigned long long)(unsigned)c;
 }
+template <bool EARLY>
 __global__ void __launch_bounds__(256) k_scan_1pass(int* in, int n, int* out, int* list, int* n_list, int ntiles,
                                                    unsigned long long* status, unsigned* ctr) {
-  pdl_wait();
+  if (!EARLY) pdl_wait();
   pdl_trigger();
   __shared__ int tile_s, pre_s, pre_c;
   __shared__ bool last_s;
@@ -366,6 +367,7 @@ __global__ void __launch_bounds__(256) k_scan_1pass(int* in, int n, int* out, in
     for (int t = threadIdx.x; t < ntiles; t += blockDim.x) status[t] = 0ull;
     if (threadIdx.x == 0) ctr[0] = ctr[1] = 0u;
   }
+  if (EARLY) pdl_wait();  // complete only after the predecessor (keeps the stream order)
 }
 
 // ---------------------------------------------------------------------------
@@ -376,12 +378,12 @@ size_t scan_tmp_ints(int n) {
   return 2 * (size_t)ntiles + 64;
 }
 
-void scan_exclusive(int* in, int* out, int n, int* list, int* n_list, int* tmp, cudaStream_t s) {
+void scan_exclusive(int* in, int* out, int n, int* list, int* n_list, int* tmp, cudaStream_t s, bool early) {
   int ntiles = (n + kScanTile - 1) / kScanTile;
   if (ntiles == 0) ntiles = 1;
   // one launch: decoupled look-back over the tiles (status words + counters in tmp,
   // zero between calls: the last tile to finish resets them)
-  launch_pdl(k_scan_1pass, ntiles, 256, 0, s, in, n, out, list, n_list, ntiles,
+  launch_pdl(early ? k_scan_1pass<true> : k_scan_1pass<false>, ntiles, 256, 0, s, in, n, out, list, n_list, ntiles,
              reinterpret_cast<unsigned long long*>(tmp), reinterpret_cast<unsigned*>(tmp + 2 * ntiles));
 }
 

@@ -1259,12 +1259,20 @@ __device__ void iter_begin_env(const SimParams& P, int env, int lane) {
     P.vmax_bits[env] = 0u;
   }
 }
+// Scheduled (programmatic launch) once k_grid has started, i.e. after k_iter_end
+// and the particle kernel completed. In particle coupling mode outside the
+// deterministic mode k_grid reads nothing this kernel writes (only the envs'
+// dt_c and the grid), so the rigid step runs alongside k_grid and waits for it
+// only before exiting; otherwise (grid-mode penalty reads the shapes, the
+// deterministic grid reads the launch exponents) it waits first.
 __global__ void k_iter_begin(SimParams P) {
-  pdl_wait();
+  const bool early = !P.grid_mode && !P.det;
+  if (!early) pdl_wait();
   pdl_trigger();
   const int t = blockIdx.x * blockDim.x + threadIdx.x, env = t >> 5;
   if (t == 0) *P.any_redo = 0;
   if (env < P.n_env) iter_begin_env(P, env, t & 31);
+  if (early) pdl_wait();
 }
 
 __device__ void iter_end_env(const SimParams& P, int env) {
@@ -1316,8 +1324,11 @@ __device__ void iter_end_env(const SimParams& P, int env) {
 // right away (its node blocks: a contiguous range of the ascending node-block
 // list) for the redo pass.
 constexpr int kIterEndThreads = 128;
+// Scheduled (programmatic launch) once the node-block scan has started, i.e.
+// after the particle kernel completed: the state machine only reads the
+// particle kernel's outputs and runs alongside k_perm; the redo clear reads the
+// node-block list and waits first.
 __global__ void __launch_bounds__(kIterEndThreads) k_iter_end(SimParams P) {
-  pdl_wait();
   pdl_trigger();
   const int env = blockIdx.x, lane = threadIdx.x;
   __shared__ int redo;
@@ -1326,6 +1337,7 @@ __global__ void __launch_bounds__(kIterEndThreads) k_iter_end(SimParams P) {
     redo = P.run[env].redo;
   }
   __syncthreads();
+  pdl_wait();
   if (!redo) return;
   const int nlist = *P.n_nb;
   auto lower = [&](int key) {  // first list entry >= key
@@ -1470,16 +1482,20 @@ void launch_particles(const SimParams& P, cudaStream_t s) {
     Q.redo_pass = 0;
     particle_kernel(Q, s);
   }
+  // the next launch's bucket structure goes to the write set: the redo pass of this
+  // launch still reads this launch's perm / bucket offsets
   {
-    Timed tm(P, kKBucketScan, s, P.det ? 3 : 2);
-    // the next launch's bucket structure goes to the write set: the redo pass of this
-    // launch still reads this launch's perm / bucket offsets
+    Timed tm(P, kKBucketScan, s, 1);
     scan_exclusive(P.bucket_count, P.bucket_start_w, P.n_keys, P.active_buckets_w, P.n_active_buckets_w, P.scan_tmp, s);
-    if (P.n > 0) launch_pdl(k_perm, nblk(P.n), 256, 0, s, P);
-    if (P.det) launch_pdl(k_det_sort_movers, sm_count() * 8, 128, 0, s, P);
   }
-  Timed tm(P, kKBlockScan, s, 1);
-  scan_exclusive(P.nb_flag, P.nb_scan, P.n_blocks, P.nb_list, P.n_nb, P.scan_tmp, s);
+  {  // node-block list: its flags are complete with the particle kernel, so it runs
+     // alongside the bucket scan (own status area)
+    Timed tm(P, kKBlockScan, s, 1);
+    scan_exclusive(P.nb_flag, P.nb_scan, P.n_blocks, P.nb_list, P.n_nb, P.scan_tmp2, s, true);
+  }
+  Timed tm(P, kKBucketScan, s, P.det ? 2 : 1);
+  if (P.n > 0) launch_pdl(k_perm, nblk(P.n), 256, 0, s, P);
+  if (P.det) launch_pdl(k_det_sort_movers, sm_count() * 8, 128, 0, s, P);
 }
 
 void launch_grid(const SimParams& P, cudaStream_t s) {
