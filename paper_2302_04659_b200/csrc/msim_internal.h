@@ -358,7 +358,10 @@ void launch_call_begin(const SimParams& P, int n_substeps, int first_action, cud
 // node-block scan -> [iter_end] -> grid update.
 void launch_iteration(const SimParams& P, bool bookkeeping, bool grid_update, cudaStream_t s);
 // The particle kernel + re-sort only (phase API).
-void launch_particles(const SimParams& P, cudaStream_t s);
+// perm_now = false: the caller launches the next-launch slot map (launch_perm)
+// itself, later in the cycle
+void launch_particles(const SimParams& P, cudaStream_t s, bool perm_now = true);
+void launch_perm(const SimParams& P, cudaStream_t s, bool early);
 // Grid update only (phase API).
 void launch_grid(const SimParams& P, cudaStream_t s);
 // Per-env end-of-launch bookkeeping only (phase API p2g: lost check, balance).

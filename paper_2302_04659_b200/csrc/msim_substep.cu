@@ -964,11 +964,15 @@ __device__ __forceinline__ void perm_at(const SimParams& P, long long i) {
   if (r == -1 && !P.det) P.move_count[k] = 0;  // exactly one mover per bucket has rank -1: reset the counter
   P.perm_w[(r >= 0 ? P.bucket_start_w[k] : P.bucket_start_w[k + 1]) + r] = (int)i;
 }
+// EARLY: launched after k_grid, whose start implies the bucket scan and the
+// particle kernel completed: runs alongside k_grid / k_iter_begin.
+template <bool EARLY>
 __global__ void k_perm(SimParams P) {
-  pdl_wait();
+  if (!EARLY) pdl_wait();
   pdl_trigger();
   const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (i < P.n) perm_at(P, i);
+  if (EARLY) pdl_wait();
 }
 
 // Deterministic mode: the movers at the end of each bucket (atomic ranks) are
@@ -1326,8 +1330,8 @@ __device__ void iter_end_env(const SimParams& P, int env) {
 constexpr int kIterEndThreads = 128;
 // Scheduled (programmatic launch) once the node-block scan has started, i.e.
 // after the particle kernel completed: the state machine only reads the
-// particle kernel's outputs and runs alongside k_perm; the redo clear reads the
-// node-block list and waits first.
+// particle kernel's outputs and runs alongside the bucket / node-block scans;
+// the redo clear reads the node-block list and waits first.
 __global__ void __launch_bounds__(kIterEndThreads) k_iter_end(SimParams P) {
   pdl_trigger();
   const int env = blockIdx.x, lane = threadIdx.x;
@@ -1457,7 +1461,7 @@ void launch_rebin(const SimParams& P, cudaStream_t s) {
   Q.n_active_buckets_w = P.n_active_buckets;
   Timed tm(P, kKBucketScan, s, P.det ? 3 : 2);
   scan_exclusive(Q.bucket_count, Q.bucket_start_w, Q.n_keys, Q.active_buckets_w, Q.n_active_buckets_w, Q.scan_tmp, s);
-  if (Q.n > 0) launch_pdl(k_perm, nblk(Q.n), 256, 0, s, Q);
+  if (Q.n > 0) launch_pdl(k_perm<false>, nblk(Q.n), 256, 0, s, Q);
   if (Q.det) launch_pdl(k_det_sort_movers, sm_count() * 8, 128, 0, s, Q);
 }
 
@@ -1475,7 +1479,13 @@ void launch_call_begin(const SimParams& P, int n_sub, int first_action, cudaStre
   launch_pdl(k_call_begin, nblk(32LL * P.n_env), 256, 0, s, P, n_sub, first_action);
 }
 
-void launch_particles(const SimParams& P, cudaStream_t s) {
+void launch_perm(const SimParams& P, cudaStream_t s, bool early) {
+  Timed tm(P, kKBucketScan, s, P.det ? 2 : 1);
+  if (P.n > 0) launch_pdl(early ? k_perm<true> : k_perm<false>, nblk(P.n), 256, 0, s, P);
+  if (P.det) launch_pdl(k_det_sort_movers, sm_count() * 8, 128, 0, s, P);
+}
+
+void launch_particles(const SimParams& P, cudaStream_t s, bool perm_now) {
   {
     Timed tm(P, kKP2G, s);
     SimParams Q = P;
@@ -1493,9 +1503,7 @@ void launch_particles(const SimParams& P, cudaStream_t s) {
     Timed tm(P, kKBlockScan, s, 1);
     scan_exclusive(P.nb_flag, P.nb_scan, P.n_blocks, P.nb_list, P.n_nb, P.scan_tmp2, s, true);
   }
-  Timed tm(P, kKBucketScan, s, P.det ? 2 : 1);
-  if (P.n > 0) launch_pdl(k_perm, nblk(P.n), 256, 0, s, P);
-  if (P.det) launch_pdl(k_det_sort_movers, sm_count() * 8, 128, 0, s, P);
+  if (perm_now) launch_perm(P, s, false);
 }
 
 void launch_grid(const SimParams& P, cudaStream_t s) {
@@ -1513,7 +1521,9 @@ void launch_iteration(const SimParams& P, bool bookkeeping, bool grid_update, cu
     Timed tm(P, kKRigid, s);
     launch_pdl(k_iter_begin, nblk(32LL * P.n_env), 256, 0, s, P);
   }
-  launch_particles(P, s);
+  // the slot map of the next launch is only needed by that launch: it goes after
+  // k_grid (and runs alongside it) when there is one
+  launch_particles(P, s, !grid_update);
   launch_iteration_end(P, s);  // also zeroes the accumulators of envs that redo
   if (bookkeeping && !P.split) {
     // speculated-dt misses (CFL halving changed between substeps): redo those envs' P2G.
@@ -1523,7 +1533,10 @@ void launch_iteration(const SimParams& P, bool bookkeeping, bool grid_update, cu
     Q.redo_pass = 1;
     particle_kernel(Q, s);
   }
-  if (grid_update) launch_grid(P, s);
+  if (grid_update) {
+    launch_grid(P, s);
+    launch_perm(P, s, true);
+  }
 }
 
 }  // namespace msim_impl
