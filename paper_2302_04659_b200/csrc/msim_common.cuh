@@ -178,18 +178,24 @@ __device__ inline void set_kinematic_pose(BodyDev& b, const double* p, double dt
 // wrenches and rebuild the per-shape world transforms.
 // lane / nlanes: the threads sharing the env (one warp: bodies, then shapes, in parallel).
 __device__ inline void rigid_env(const SimParams& P, int env, int integrate, int lane = 0, int nlanes = 1) {
+  // latency bound (one env per warp, fp64): bodies and shape descriptions are
+  // copied to registers in one batch of loads and written back in one batch of
+  // stores, instead of a chain of dependent global accesses
   const int b0 = P.body_off[env], b1 = P.body_off[env + 1];
+  const int s0 = P.shape_off[env], s1 = P.shape_off[env + 1];
+  const int ridx = P.sched_steps > 0 ? min(P.run[env].rigid_idx, P.sched_steps - 1) : 0;
   for (int bi = b0 + lane; bi < b1; bi += nlanes) {
-    BodyDev& b = P.bodies[bi];
     if (integrate) {
+      BodyDev b = P.bodies[bi];
+      double wf[6];
+      for (int k = 0; k < 6; ++k) wf[k] = P.pending[6 * bi + k];
       if (b.mode == MSIM_BODY_DYNAMIC)
-        integrate_free_body(b, P.pending + 6 * bi, P.rigid_g, P.dt_r);
+        integrate_free_body(b, wf, P.rigid_g, P.dt_r);
       else if (b.mode == MSIM_BODY_SCRIPTED)
         advance_pose(b, P.dt_r);
-      if (P.sched_steps > 0 && P.sched_mask[bi]) {
-        const int r = min(P.run[env].rigid_idx, P.sched_steps - 1);
-        set_kinematic_pose(b, P.sched + 7 * ((long long)r * P.n_bodies_total + bi), P.dt_r);
-      }
+      if (P.sched_steps > 0 && P.sched_mask[bi])
+        set_kinematic_pose(b, P.sched + 7 * ((long long)ridx * P.n_bodies_total + bi), P.dt_r);
+      P.bodies[bi] = b;
     }
     double* wr = P.wrench + 6 * bi;
     for (int k = 0; k < 6; ++k) wr[k] = 0.0;
@@ -197,10 +203,9 @@ __device__ inline void rigid_env(const SimParams& P, int env, int integrate, int
       for (int k = 0; k < 6; ++k) P.w64[6 * bi + k] = 0;
   }
   if (nlanes > 1) __syncwarp();  // shapes read their (integrated) bodies
-  const int s0 = P.shape_off[env], s1 = P.shape_off[env + 1];
   for (int si = s0 + lane; si < s1; si += nlanes) {
-    const ShapeHost& sh = P.shape_src[si];
-    const BodyDev& b = P.bodies[b0 + sh.body];
+    const ShapeHost sh = P.shape_src[si];
+    const BodyDev b = P.bodies[b0 + sh.body];
     dq bq = {b.q[0], b.q[1], b.q[2], b.q[3]};
     dq lq = {sh.lq[0], sh.lq[1], sh.lq[2], sh.lq[3]};
     dq wq = qnormcanon(qmul(bq, lq));  // compose (geometry.hpp:54-56)

@@ -1203,6 +1203,7 @@ __device__ void call_begin_env(const SimParams& P, int env, int n_sub, int first
     }
   }
   rigid = __shfl_sync(0xffffffffu, rigid, 0);
+  __syncwarp();                               // lane 0's rigid_idx = 0 visible to the body lanes
   if (rigid) rigid_env(P, env, 1, lane, 32);  // rigid step 0: integrate + sync
   __syncwarp();
   if (lane == 0 && !P.err_code[env]) {
@@ -1226,38 +1227,43 @@ __global__ void k_call_begin(SimParams P, int n_sub, int first_action) {
 __device__ void iter_begin_env(const SimParams& P, int env, int lane) {
   EnvRun& r = P.run[env];
   int rigid = 0, active = 0;
-  if (lane == 0) {
-    r.next_new_sub = 0;
-    r.next_new_rigid = 0;
-    r.redo = 0;
-    if (r.substeps_left <= 0 || P.err_code[env]) {
-      r.action = kActIdle;
-    } else {
+  if (lane == 0) {  // the env's state in registers (one batch of loads), changed fields written back
+    const EnvRun l = r;
+    const int err = P.err_code[env];
+    int action = kActIdle, nns = 0, nnr = 0;
+    if (l.substeps_left > 0 && !err) {
       active = 1;
-      r.dt_g2p = r.dt_c;
-      r.dt_p2g = r.dt_c;  // same substep: exact; new substep: speculated (same cycle count)
-      if (r.cycle == r.cycles - 1 && r.substeps_left == 1) {
-        r.action = kActG2P;
+      r.dt_g2p = l.dt_c;
+      r.dt_p2g = l.dt_c;  // same substep: exact; new substep: speculated (same cycle count)
+      if (l.cycle == l.cycles - 1 && l.substeps_left == 1) {
+        action = kActG2P;
       } else {
-        r.action = kActFused;
-        if (r.cycle + 1 >= r.cycles) {
-          r.next_new_sub = 1;
-          r.next_new_rigid = P.integrate_rigid && (r.soft_in_rigid + 1 == P.n_soft);
+        action = kActFused;
+        if (l.cycle + 1 >= l.cycles) {
+          nns = 1;
+          nnr = P.integrate_rigid && (l.soft_in_rigid + 1 == P.n_soft);
         }
-        if (r.next_new_rigid) {
-          // end of rigid step: pending_wrenches = wrenches (coupling.hpp:288), then the
-          // next rigid step integrates with them and syncs (coupling.hpp:250-259)
-          const int b0 = P.body_off[env], b1 = P.body_off[env + 1];
-          for (int k = 6 * b0; k < 6 * b1; ++k) P.pending[k] = P.wrench[k];
-          r.rigid_idx += 1;
+        if (nnr) {
+          r.rigid_idx = l.rigid_idx + 1;
           rigid = 1;
         }
       }
     }
+    r.action = action;
+    r.next_new_sub = nns;
+    r.next_new_rigid = nnr;
+    r.redo = 0;
   }
   rigid = __shfl_sync(0xffffffffu, rigid, 0);
   active = __shfl_sync(0xffffffffu, active, 0);
-  if (rigid) rigid_env(P, env, 1, lane, 32);
+  if (rigid) {
+    // end of rigid step: pending_wrenches = wrenches (coupling.hpp:288), then the
+    // next rigid step integrates with them and syncs (coupling.hpp:250-259)
+    const int b0 = P.body_off[env], b1 = P.body_off[env + 1];
+    for (int k = 6 * b0 + lane; k < 6 * b1; k += 32) P.pending[k] = P.wrench[k];
+    __syncwarp();
+    rigid_env(P, env, 1, lane, 32);
+  }
   if (lane == 0 && active) {
     det_exponents(P, env, r);
     P.vmax_bits[env] = 0u;
