@@ -13,6 +13,7 @@ python bench.py --config E --clay-only --no-cpu-baseline > $O/bench_E_clay.json 
 python bench.py --config B --no-cpu-baseline > $O/bench_B.json 2> $O/bench_B.err; echo "bench B rc=$?"
 python bench.py --config C --no-cpu-baseline > $O/bench_C.json 2> $O/bench_C.err; echo "bench C rc=$?"
 python bench.py --deterministic --no-cpu-baseline > $O/bench_D_det.json 2> $O/bench_D_det.err; echo "bench D det rc=$?"
+python bench.py --config A > $O/bench_A.json 2> $O/bench_A.err; echo "bench A rc=$?"
 python bench.py --steps 1 --warmup 1 --no-cpu-baseline > $O/bench_short.json 2>&1 && \
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches_D.csv \
     python bench.py --steps 1 --warmup 1 --no-cpu-baseline > $O/ncu_launches.log 2>&1; echo "launch list rc=$?"

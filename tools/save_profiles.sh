@@ -5,7 +5,7 @@ set -e
 T=$1
 O=gpurun_out
 SHA=$(git rev-parse --short HEAD)
-for f in D E E_clay B C D_det; do [ -f $O/bench_$f.json ] && tail -1 $O/bench_$f.json > profiles/${T}_bench_$f.json; done
+for f in D E E_clay B C D_det A; do [ -f $O/bench_$f.json ] && tail -1 $O/bench_$f.json > profiles/${T}_bench_$f.json; done
 tail -1 $O/bench_ref.json > profiles/${T}_bench_reference.json
 [ -f $O/small.json ] && cp $O/small.json profiles/${T}_small_configs.json
 [ -f $O/tasks.json ] && cp $O/tasks.json profiles/${T}_tasks_D.json
