@@ -319,29 +319,45 @@ __global__ void __launch_bounds__(256) k_scan_1pass(int* in, int n, int* out, in
   __shared__ int tot_s, tot_c;
   int es = block_excl_scan(sm, &tot_s);
   int ec = block_excl_scan(c, &tot_c);
-  if (threadIdx.x == 0) {
+  if (threadIdx.x < 32) {  // warp-wide look-back: 32 predecessors' status words per step
     volatile unsigned long long* st = status;
+    const unsigned FULL = 0xffffffffu;
+    const int lane = threadIdx.x;
+    const unsigned long long kFlag = 3ull << 62, kIncl = 2ull << 62;
     int ps = 0, pc = 0;
     if (tile > 0) {
-      st[tile] = st_pack(kStAgg, tot_s, tot_c);
-      __threadfence();
-      for (int k = tile - 1; k >= 0;) {
-        const unsigned long long w = st[k];
-        const unsigned long long f = w & (3ull << 62);
-        if (f == 0) continue;  // predecessor not published yet
-        ps += (int)((w >> 31) & 0x7fffffffull);
-        pc += (int)(w & 0x7fffffffull);
-        if (f == kStIncl) break;
-        --k;
+      if (lane == 0) {
+        st[tile] = st_pack(kStAgg, tot_s, tot_c);
+        __threadfence();
+      }
+      for (int top = tile - 1;; top -= 32) {
+        const int idx = top - lane;  // lane 0: the nearest predecessor
+        unsigned long long w = idx >= 0 ? st[idx] : kIncl;  // before tile 0: an empty inclusive prefix
+        while (__any_sync(FULL, (w & kFlag) == 0))  // some predecessor not published yet
+          if ((w & kFlag) == 0) w = st[idx];
+        const unsigned incl = __ballot_sync(FULL, (w & kFlag) == kIncl);
+        const int stop = incl ? __ffs(incl) - 1 : 31;  // lanes 0..stop contribute
+        int s = lane <= stop ? (int)((w >> 31) & 0x7fffffffull) : 0;
+        int c = lane <= stop ? (int)(w & 0x7fffffffull) : 0;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          s += __shfl_xor_sync(FULL, s, o);
+          c += __shfl_xor_sync(FULL, c, o);
+        }
+        ps += s;
+        pc += c;
+        if (incl) break;
       }
     }
-    st[tile] = st_pack(kStIncl, ps + tot_s, pc + tot_c);
-    __threadfence();
-    pre_s = ps;
-    pre_c = pc;
-    if (tile == ntiles - 1) {
-      out[n] = ps + tot_s;
-      if (n_list) *n_list = pc + tot_c;
+    if (lane == 0) {
+      st[tile] = st_pack(kStIncl, ps + tot_s, pc + tot_c);
+      __threadfence();
+      pre_s = ps;
+      pre_c = pc;
+      if (tile == ntiles - 1) {
+        out[n] = ps + tot_s;
+        if (n_list) *n_list = pc + tot_c;
+      }
     }
   }
   __syncthreads();
