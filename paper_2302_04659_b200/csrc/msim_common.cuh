@@ -177,18 +177,32 @@ __device__ inline void set_kinematic_pose(BodyDev& b, const double* p, double dt
 // of this rigid step), then sync_rigid_to_soft: zero the accumulating
 // wrenches and rebuild the per-shape world transforms.
 // lane / nlanes: the threads sharing the env (one warp: bodies, then shapes, in parallel).
-__device__ inline void rigid_env(const SimParams& P, int env, int integrate, int lane = 0, int nlanes = 1) {
-  // latency bound (one env per warp, fp64): bodies and shape descriptions are
-  // copied to registers in one batch of loads and written back in one batch of
-  // stores, instead of a chain of dependent global accesses
-  const int b0 = P.body_off[env], b1 = P.body_off[env + 1];
-  const int s0 = P.shape_off[env], s1 = P.shape_off[env + 1];
-  const int ridx = P.sched_steps > 0 ? min(P.run[env].rigid_idx, P.sched_steps - 1) : 0;
+// Latency bound (one env per warp, fp64): descriptions are read in batches
+// ahead of use, a warp passes its integrated bodies to the shape lanes through
+// shared memory (sbody: kMaxBodiesPerEnv slots per warp, or null: global), and
+// stage = true also stages the wrench (pending = wrench, coupling.hpp:288) in
+// the body lane that integrates with it. ridx: the schedule row of this rigid step.
+struct EnvRange {
+  int b0, b1, s0, s1;
+};
+__device__ __forceinline__ EnvRange env_range(const SimParams& P, int env) {
+  return {P.body_off[env], P.body_off[env + 1], P.shape_off[env], P.shape_off[env + 1]};
+}
+__device__ inline void rigid_env(const SimParams& P, int env, int integrate, int lane, int nlanes, const EnvRange& g,
+                                 int ridx, bool stage, BodyDev* sbody) {
+  const int b0 = g.b0, b1 = g.b1, s0 = g.s0, s1 = g.s1;
+  ridx = P.sched_steps > 0 ? min(ridx, P.sched_steps - 1) : 0;
+  const bool has0 = s0 + lane < s1;
+  ShapeHost sh0;  // this lane's first shape, loaded ahead of the body pass
+  if (has0) sh0 = P.shape_src[s0 + lane];
   for (int bi = b0 + lane; bi < b1; bi += nlanes) {
+    double* wr = P.wrench + 6 * bi;
     if (integrate) {
       BodyDev b = P.bodies[bi];
       double wf[6];
-      for (int k = 0; k < 6; ++k) wf[k] = P.pending[6 * bi + k];
+      for (int k = 0; k < 6; ++k) wf[k] = stage ? wr[k] : P.pending[6 * bi + k];
+      if (stage)
+        for (int k = 0; k < 6; ++k) P.pending[6 * bi + k] = wf[k];
       if (b.mode == MSIM_BODY_DYNAMIC)
         integrate_free_body(b, wf, P.rigid_g, P.dt_r);
       else if (b.mode == MSIM_BODY_SCRIPTED)
@@ -196,16 +210,18 @@ __device__ inline void rigid_env(const SimParams& P, int env, int integrate, int
       if (P.sched_steps > 0 && P.sched_mask[bi])
         set_kinematic_pose(b, P.sched + 7 * ((long long)ridx * P.n_bodies_total + bi), P.dt_r);
       P.bodies[bi] = b;
+      if (sbody && bi - b0 < kMaxBodiesPerEnv) sbody[bi - b0] = b;
+    } else if (sbody && bi - b0 < kMaxBodiesPerEnv) {
+      sbody[bi - b0] = P.bodies[bi];
     }
-    double* wr = P.wrench + 6 * bi;
     for (int k = 0; k < 6; ++k) wr[k] = 0.0;
     if (P.det)
       for (int k = 0; k < 6; ++k) P.w64[6 * bi + k] = 0;
   }
   if (nlanes > 1) __syncwarp();  // shapes read their (integrated) bodies
   for (int si = s0 + lane; si < s1; si += nlanes) {
-    const ShapeHost sh = P.shape_src[si];
-    const BodyDev b = P.bodies[b0 + sh.body];
+    const ShapeHost sh = si == s0 + lane ? sh0 : P.shape_src[si];
+    const BodyDev b = sbody && sh.body < kMaxBodiesPerEnv ? sbody[sh.body] : P.bodies[b0 + sh.body];
     dq bq = {b.q[0], b.q[1], b.q[2], b.q[3]};
     dq lq = {sh.lq[0], sh.lq[1], sh.lq[2], sh.lq[3]};
     dq wq = qnormcanon(qmul(bq, lq));  // compose (geometry.hpp:54-56)

@@ -160,7 +160,7 @@ __global__ void k_vmax(SimParams P) {
 __global__ void k_rigid_all(SimParams P, int integrate, int only_env) {
   int env = blockIdx.x * blockDim.x + threadIdx.x;
   if (env >= P.n_env || (only_env >= 0 && env != only_env)) return;
-  rigid_env(P, env, integrate);
+  rigid_env(P, env, integrate, 0, 1, env_range(P, env), P.run[env].rigid_idx, false, nullptr);
 }
 
 __global__ void k_stage(const double* wrench, double* pending, int n) {

@@ -1182,8 +1182,11 @@ __global__ void k_set_action(SimParams P, int action, float dt) {
 }
 
 // One warp per env (lane 0: the env's state machine; all lanes: its rigid step).
-__device__ void call_begin_env(const SimParams& P, int env, int n_sub, int first_action, int lane) {
+// The kernels run kRigidWarps warps per CTA; sbody: the warp's body slots.
+constexpr int kRigidWarps = 4;
+__device__ void call_begin_env(const SimParams& P, int env, int n_sub, int first_action, int lane, BodyDev* sbody) {
   EnvRun& r = P.run[env];
+  const EnvRange g = env_range(P, env);
   int rigid = 0;
   if (lane == 0) {
     r.substeps_left = n_sub;
@@ -1203,8 +1206,7 @@ __device__ void call_begin_env(const SimParams& P, int env, int n_sub, int first
     }
   }
   rigid = __shfl_sync(0xffffffffu, rigid, 0);
-  __syncwarp();                               // lane 0's rigid_idx = 0 visible to the body lanes
-  if (rigid) rigid_env(P, env, 1, lane, 32);  // rigid step 0: integrate + sync
+  if (rigid) rigid_env(P, env, 1, lane, 32, g, 0, false, sbody);  // rigid step 0: integrate + sync
   __syncwarp();
   if (lane == 0 && !P.err_code[env]) {
     if (n_sub > 0) plan_cycles(P, env, r);
@@ -1215,18 +1217,20 @@ __device__ void call_begin_env(const SimParams& P, int env, int n_sub, int first
   }
 }
 
-__global__ void k_call_begin(SimParams P, int n_sub, int first_action) {
+__global__ void __launch_bounds__(32 * kRigidWarps) k_call_begin(SimParams P, int n_sub, int first_action) {
   pdl_wait();
   pdl_trigger();
+  __shared__ BodyDev sbody[kRigidWarps][kMaxBodiesPerEnv];
   const int t = blockIdx.x * blockDim.x + threadIdx.x, env = t >> 5;
   if (t == 0) *P.any_redo = 0;
-  if (env < P.n_env) call_begin_env(P, env, n_sub, first_action, t & 31);
+  if (env < P.n_env) call_begin_env(P, env, n_sub, first_action, t & 31, sbody[threadIdx.x >> 5]);
 }
 
 // One warp per env (lane 0: the env's state machine; all lanes: its rigid step).
-__device__ void iter_begin_env(const SimParams& P, int env, int lane) {
+__device__ void iter_begin_env(const SimParams& P, int env, int lane, BodyDev* sbody) {
   EnvRun& r = P.run[env];
-  int rigid = 0, active = 0;
+  const EnvRange g = env_range(P, env);  // all lanes, in the same batch as lane 0's state
+  int rigid = 0, active = 0, ridx = 0;
   if (lane == 0) {  // the env's state in registers (one batch of loads), changed fields written back
     const EnvRun l = r;
     const int err = P.err_code[env];
@@ -1244,7 +1248,8 @@ __device__ void iter_begin_env(const SimParams& P, int env, int lane) {
           nnr = P.integrate_rigid && (l.soft_in_rigid + 1 == P.n_soft);
         }
         if (nnr) {
-          r.rigid_idx = l.rigid_idx + 1;
+          ridx = l.rigid_idx + 1;
+          r.rigid_idx = ridx;
           rigid = 1;
         }
       }
@@ -1256,14 +1261,11 @@ __device__ void iter_begin_env(const SimParams& P, int env, int lane) {
   }
   rigid = __shfl_sync(0xffffffffu, rigid, 0);
   active = __shfl_sync(0xffffffffu, active, 0);
-  if (rigid) {
-    // end of rigid step: pending_wrenches = wrenches (coupling.hpp:288), then the
-    // next rigid step integrates with them and syncs (coupling.hpp:250-259)
-    const int b0 = P.body_off[env], b1 = P.body_off[env + 1];
-    for (int k = 6 * b0 + lane; k < 6 * b1; k += 32) P.pending[k] = P.wrench[k];
-    __syncwarp();
-    rigid_env(P, env, 1, lane, 32);
-  }
+  ridx = __shfl_sync(0xffffffffu, ridx, 0);
+  // end of rigid step: pending_wrenches = wrenches (coupling.hpp:288, staged by
+  // the body lanes), then the next rigid step integrates with them and syncs
+  // (coupling.hpp:250-259)
+  if (rigid) rigid_env(P, env, 1, lane, 32, g, ridx, true, sbody);
   if (lane == 0 && active) {
     det_exponents(P, env, r);
     P.vmax_bits[env] = 0u;
@@ -1275,13 +1277,14 @@ __device__ void iter_begin_env(const SimParams& P, int env, int lane) {
 // dt_c and the grid), so the rigid step runs alongside k_grid and waits for it
 // only before exiting; otherwise (grid-mode penalty reads the shapes, the
 // deterministic grid reads the launch exponents) it waits first.
-__global__ void k_iter_begin(SimParams P) {
+__global__ void __launch_bounds__(32 * kRigidWarps) k_iter_begin(SimParams P) {
   const bool early = !P.grid_mode && !P.det;
   if (!early) pdl_wait();
   pdl_trigger();
+  __shared__ BodyDev sbody[kRigidWarps][kMaxBodiesPerEnv];
   const int t = blockIdx.x * blockDim.x + threadIdx.x, env = t >> 5;
   if (t == 0) *P.any_redo = 0;
-  if (env < P.n_env) iter_begin_env(P, env, t & 31);
+  if (env < P.n_env) iter_begin_env(P, env, t & 31, sbody[threadIdx.x >> 5]);
   if (early) pdl_wait();
 }
 
@@ -1482,7 +1485,7 @@ void launch_set_action(const SimParams& P, int action, float dt, cudaStream_t s)
 
 void launch_call_begin(const SimParams& P, int n_sub, int first_action, cudaStream_t s) {
   Timed tm(P, kKPlan, s);
-  launch_pdl(k_call_begin, nblk(32LL * P.n_env), 256, 0, s, P, n_sub, first_action);
+  launch_pdl(k_call_begin, nblk(32LL * P.n_env, 32 * kRigidWarps), 32 * kRigidWarps, 0, s, P, n_sub, first_action);
 }
 
 void launch_perm(const SimParams& P, cudaStream_t s, bool early) {
@@ -1525,7 +1528,7 @@ void launch_iteration_end(const SimParams& P, cudaStream_t s) {
 void launch_iteration(const SimParams& P, bool bookkeeping, bool grid_update, cudaStream_t s) {
   if (bookkeeping) {
     Timed tm(P, kKRigid, s);
-    launch_pdl(k_iter_begin, nblk(32LL * P.n_env), 256, 0, s, P);
+    launch_pdl(k_iter_begin, nblk(32LL * P.n_env, 32 * kRigidWarps), 32 * kRigidWarps, 0, s, P);
   }
   // the slot map of the next launch is only needed by that launch: it goes after
   // k_grid (and runs alongside it) when there is one
