@@ -82,7 +82,10 @@ inline void launch_pdl(void (*kern)(Params...), unsigned grid, unsigned block, s
   at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  cudaLaunchKernelEx(&cfg, kern, args...);
+  if (cudaLaunchKernelEx(&cfg, kern, args...) != cudaSuccess) {  // attribute refused: plain launch
+    (void)cudaGetLastError();
+    kern<<<grid, block, smem, s>>>(args...);
+  }
 }
 
 // Resident particle-kernel rounds on the device (default build: 5 CTAs / SM x 128
