@@ -81,6 +81,21 @@ def test_config_d_batch_matches_reference_per_env():
         assert rep.max_force_balance_error <= 1e-10
 
 
+def test_full_size_config_d_sampled_envs_match_reference():
+    """The benchmark's own size: all 1024 envs of D (16.8 M particles; the
+    bucket key space, the multi-tile scans and the node-block list at full
+    scale) stepped as one batch, sampled envs against their own reference
+    Worlds."""
+    scene = config_d(n_envs=1024)
+    gw = GpuWorld(scene)
+    gw.env_step()
+    for e in (0, 1, 511, 1022, 1023):
+        ref = RefWorld(scene, env=e)
+        rr = ref.env_step()
+        _compare_env(gw, e, ref, None, rr, f"D/1024 env {e}")
+        assert gw.report(e).cfl_cycles == rr.cfl_cycles
+
+
 def test_third_law_every_substep_pinch():
     """Acceptance criterion 3 on a pinch-shaped env (two fingers squeezing a block,
     acceptance.cpp:156-193): |sum of reactions + sum of applied forces| <= 1e-10 N
