@@ -1411,7 +1411,11 @@ void launch_k_particles(const SimParams& P, cudaStream_t s) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_particles<NCH, F, AM, DET>, kT, sizeof(Smem<NCH, F>));
     if (per_sm <= 0) per_sm = 1;
   }
-  launch_pdl(k_particles<NCH, F, AM, DET>, sm_count() * per_sm, kT, sizeof(Smem<NCH, F>), s, P);
+  // the redo pass (speculated dt missed: rare) exits at once when no env redoes;
+  // for small scenes one CTA per SM keeps that no-op launch cheap on the
+  // per-cycle critical path (A -1 %)
+  const int g = P.redo_pass && P.split_r > 1 ? sm_count() : sm_count() * per_sm;
+  launch_pdl(k_particles<NCH, F, AM, DET>, g, kT, sizeof(Smem<NCH, F>), s, P);
 }
 
 template <bool AM>
