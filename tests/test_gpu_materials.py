@@ -98,3 +98,26 @@ def test_config_e_reduced_mixed_materials():
     fo, _ = ow.wrenches(pending=True)
     for b in range(len(fo)):
         assert np.linalg.norm(fg[b] - fo[b]) / max(np.linalg.norm(fo[b]), 1e-6) < 1e-3, (b, fg[b], fo[b])
+
+
+@pytest.mark.parametrize("cfg,mat,n_envs,sample", [(config_b, SAND, 128, (0, 77, 127)), (config_c, WATER, 32, (0, 31))],
+                         ids=["B128_sand", "C32_water"])
+def test_bench_sized_batches_match_oracle_per_env(cfg, mat, n_envs, sample):
+    """The batched Excavate- / Pour-shaped benchmark workloads at their bench
+    size (bench.py --config B | C), stepped as one batch; sampled envs against
+    their own oracle worlds."""
+    scene = cfg(material=mat, n_envs=n_envs)
+    gw = GpuWorld(scene)
+    gw.env_step()
+    for e in sample:
+        ow = OracleWorld(scene, env=e)
+        ow.env_step()
+        pg, po = gw.particles(e), ow.particles()
+        ex = np.linalg.norm(pg["x"] - po["x"]) / np.linalg.norm(po["x"])
+        ev = rel(pg["v"], po["v"])
+        assert ex < 1e-4 and ev < 1e-4, (e, ex, ev)
+        assert np.array_equal(pg["lost"], po["lost"]), e
+        fg, _ = gw.wrenches(e, pending=True)
+        fo, _ = ow.wrenches(pending=True)
+        for b in range(len(fo)):
+            assert np.linalg.norm(fg[b] - fo[b]) / max(np.linalg.norm(fo[b]), 1e-6) < 1e-3, (e, b, fg[b], fo[b])
