@@ -959,19 +959,28 @@ __global__ void __launch_bounds__(256) k_rebin(SimParams P) {
 // Particle i (slot of the launch that keyed it) -> its slot in the next launch:
 // stayers (rank >= 0) from the bucket's start in their old order, movers
 // (rank = -1 - r) from its end.
-__device__ __forceinline__ void perm_at(const SimParams& P, long long i) {
-  const int k = P.key[i], r = P.rank[i];
+__device__ __forceinline__ void perm_kr(const SimParams& P, long long i, int k, int r) {
   if (r == -1 && !P.det) P.move_count[k] = 0;  // exactly one mover per bucket has rank -1: reset the counter
   P.perm_w[(r >= 0 ? P.bucket_start_w[k] : P.bucket_start_w[k + 1]) + r] = (int)i;
 }
-// EARLY: launched after k_grid, whose start implies the bucket scan and the
-// particle kernel completed: runs alongside k_grid / k_iter_begin.
+// Four particles per thread (16-byte key / rank loads). EARLY: launched after
+// k_grid, whose start implies the bucket scan and the particle kernel
+// completed: runs alongside k_grid / k_iter_begin.
 template <bool EARLY>
 __global__ void k_perm(SimParams P) {
   if (!EARLY) pdl_wait();
   pdl_trigger();
-  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (i < P.n) perm_at(P, i);
+  const long long i0 = 4 * (blockIdx.x * (long long)blockDim.x + threadIdx.x);
+  if (i0 + 3 < P.n) {
+    const int4 k4 = *reinterpret_cast<const int4*>(P.key + i0);
+    const int4 r4 = *reinterpret_cast<const int4*>(P.rank + i0);
+    perm_kr(P, i0, k4.x, r4.x);
+    perm_kr(P, i0 + 1, k4.y, r4.y);
+    perm_kr(P, i0 + 2, k4.z, r4.z);
+    perm_kr(P, i0 + 3, k4.w, r4.w);
+  } else {
+    for (long long i = i0; i < P.n; ++i) perm_kr(P, i, P.key[i], P.rank[i]);
+  }
   if (EARLY) pdl_wait();
 }
 
@@ -1474,7 +1483,7 @@ void launch_rebin(const SimParams& P, cudaStream_t s) {
   Q.n_active_buckets_w = P.n_active_buckets;
   Timed tm(P, kKBucketScan, s, P.det ? 3 : 2);
   scan_exclusive(Q.bucket_count, Q.bucket_start_w, Q.n_keys, Q.active_buckets_w, Q.n_active_buckets_w, Q.scan_tmp, s);
-  if (Q.n > 0) launch_pdl(k_perm<false>, nblk(Q.n), 256, 0, s, Q);
+  if (Q.n > 0) launch_pdl(k_perm<false>, nblk((Q.n + 3) / 4), 256, 0, s, Q);
   if (Q.det) launch_pdl(k_det_sort_movers, sm_count() * 8, 128, 0, s, Q);
 }
 
@@ -1494,7 +1503,7 @@ void launch_call_begin(const SimParams& P, int n_sub, int first_action, cudaStre
 
 void launch_perm(const SimParams& P, cudaStream_t s, bool early) {
   Timed tm(P, kKBucketScan, s, P.det ? 2 : 1);
-  if (P.n > 0) launch_pdl(early ? k_perm<true> : k_perm<false>, nblk(P.n), 256, 0, s, P);
+  if (P.n > 0) launch_pdl(early ? k_perm<true> : k_perm<false>, nblk((P.n + 3) / 4), 256, 0, s, P);
   if (P.det) launch_pdl(k_det_sort_movers, sm_count() * 8, 128, 0, s, P);
 }
 
