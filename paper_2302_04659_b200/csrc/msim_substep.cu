@@ -1043,6 +1043,10 @@ __global__ void k_clear(SimParams P) {
 // Grid update (mpm.hpp:315-342) with the grid-mode penalty hook
 // (coupling.hpp:186-214); one warp per touched node block (32 nodes).
 // gtid / gthreads: this thread's index / the thread count of the launch (one warp per item)
+// HOOK: grid-mode penalty (coupling.hpp:182-214); without it the kernel needs
+// a third of the registers, i.e. ~4x the warps in flight for its latency-bound
+// node-block loop.
+template <bool HOOK>
 __device__ __forceinline__ void grid_items(const SimParams& P, const int gtid, const int gthreads) {
   static_assert(kBX * kBY * kBZ == 32, "one warp per node block");
   const int nlist = *P.n_nb;
@@ -1069,7 +1073,7 @@ __device__ __forceinline__ void grid_items(const SimParams& P, const int gtid, c
     f3 vel = {0.f, 0.f, 0.f};
     f3 f = {ff.x, ff.y, ff.z};
     if (live) vel = (1.0f / pm.w) * f3{pm.x, pm.y, pm.z};  // pre-force node velocity
-    if (P.grid_mode && P.hooks) {
+    if (HOOK) {
       const int s0 = P.shape_off[env], s1 = P.shape_off[env + 1];
       const int b0 = P.body_off[env];
       const f3 xi = {(float)(P.origin[0] + P.h * gx), (float)(P.origin[1] + P.h * gy), (float)(P.origin[2] + P.h * gz)};
@@ -1133,15 +1137,16 @@ __device__ __forceinline__ void grid_items(const SimParams& P, const int gtid, c
       P.gPM[gi] = z;
       if (P.split) P.gF[gi] = z;
     } else if (P.grid_mode && live) {
-      P.gF[gi] = make_float4(f.x, f.y, f.z, 0.0f);  // the grid hook adds to grid.force
+      P.gF[gi] = make_float4(f.x, f.y, f.z, 0.0f);  // the grid hook adds to grid.force (phase API)
     }
   }
 }
 
+template <bool HOOK>
 __global__ void __launch_bounds__(256) k_grid(SimParams P) {
   pdl_wait();
   pdl_trigger();
-  grid_items(P, (int)(blockIdx.x * blockDim.x + threadIdx.x), (int)(gridDim.x * blockDim.x));
+  grid_items<HOOK>(P, (int)(blockIdx.x * blockDim.x + threadIdx.x), (int)(gridDim.x * blockDim.x));
 }
 
 // ---------------------------------------------------------------------------
@@ -1530,7 +1535,7 @@ void launch_particles(const SimParams& P, cudaStream_t s, bool perm_now) {
 
 void launch_grid(const SimParams& P, cudaStream_t s) {
   Timed tm(P, kKGrid, s);
-  launch_pdl(k_grid, sm_count() * 8, 256, 0, s, P);
+  launch_pdl(P.grid_mode && P.hooks ? k_grid<true> : k_grid<false>, sm_count() * 8, 256, 0, s, P);
 }
 
 void launch_iteration_end(const SimParams& P, cudaStream_t s) {
