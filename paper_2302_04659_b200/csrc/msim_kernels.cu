@@ -309,10 +309,18 @@ __global__ void __launch_bounds__(256) k_scan_1pass(int* in, int n, int* out, in
   __syncthreads();
   const int tile = tile_s;
   const int base = tile * kScanTile + threadIdx.x * 8;
+  // the thread's 8 items: two 16-byte loads when whole (base is a multiple of 8)
+  const bool whole = base + 8 <= n;
   int v[8], sm = 0, c = 0;
+  if (whole) {
+    const int4 a = *reinterpret_cast<const int4*>(in + base), b = *reinterpret_cast<const int4*>(in + base + 4);
+    v[0] = a.x, v[1] = a.y, v[2] = a.z, v[3] = a.w, v[4] = b.x, v[5] = b.y, v[6] = b.z, v[7] = b.w;
+  } else {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) v[k] = base + k < n ? in[base + k] : 0;
+  }
 #pragma unroll
   for (int k = 0; k < 8; ++k) {
-    v[k] = base + k < n ? in[base + k] : 0;
     sm += v[k];
     c += v[k] != 0;
   }
@@ -363,15 +371,24 @@ __global__ void __launch_bounds__(256) k_scan_1pass(int* in, int n, int* out, in
   __syncthreads();
   es += pre_s;
   ec += pre_c;
+  int o[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    o[k] = es;
+    es += v[k];
+  }
+  if (whole) {
+    *reinterpret_cast<int4*>(out + base) = make_int4(o[0], o[1], o[2], o[3]);
+    *reinterpret_cast<int4*>(out + base + 4) = make_int4(o[4], o[5], o[6], o[7]);
+  }
 #pragma unroll
   for (int k = 0; k < 8; ++k) {
     const int i = base + k;
     if (i < n) {
-      out[i] = es;
+      if (!whole) out[i] = o[k];
       if (v[k] != 0) in[i] = 0;  // consumed: counts/flags restart from zero
       if (list && v[k] != 0) list[ec++] = i;
     }
-    es += v[k];
   }
   // the last tile to finish clears the status words and counters for the next call
   if (threadIdx.x == 0) {
