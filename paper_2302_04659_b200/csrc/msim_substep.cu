@@ -22,12 +22,20 @@
 //                per-cycle re-sort).
 //   scans        bucket offsets + active list, node-block list
 //   k_iter_end   per env: substep/cycle counters, CFL plan (mpm.hpp:400-409),
-//                lost-fraction check, force-balance diagnostic
+//                lost-fraction check, force-balance diagnostic; zeroes the
+//                accumulators of an env whose P2G must be redone
 //   redo         only when a CFL halving changed the next cycle's dt: the
 //                P2G of that env is redone with the planned dt
 //   k_grid       per touched node block: (p + dt f)/m + dt g, grid-mode
 //                penalty (coupling.hpp:186-214), boundary bands
 //                (mpm.hpp:315-342); consumes (zeroes) the accumulators
+//   k_perm       the next launch's slot map (after k_grid, alongside it)
+//   k_iter_begin the next cycle's rigid step (alongside k_grid)
+//
+// Small scenes split a bucket's rounds over several CTAs (split_r). The
+// per-cycle kernels are launched with programmatic dependent launch; those
+// whose inputs are complete when they are scheduled work before waiting
+// (msim_internal.h launch_pdl).
 //
 // Because G2P(c) and P2G(c+1) share one pass, each particle-substep reads and
 // writes x, F-I, mass, V0, meta, pid once; v and C stay in registers except
