@@ -68,7 +68,7 @@ namespace {
 // 128 threads / 128 particles per round measured best with the dynamic bucket
 // hand-out (D, 1024 envs: 2.85 vs 2.98 ms per launch at 256 particles, 4.06 at 64;
 // 256 threads at 2-3 CTAs/SM +6-15 %; 64 threads / 128 at 9 CTAs/SM +12 %)
-constexpr int kT = MSIM_KT;      // threads per CTA (particle kernel), kCtasPerSm CTAs per SM
+constexpr int kT = MSIM_KT;      // threads per CTA (particle kernel), ctas_per_sm() CTAs per SM
 constexpr int kCap = MSIM_KCAP;  // particles staged per round
 // Tile geometry of a particle bucket of F^3 node blocks (QX x QY x QZ base cells).
 template <int F>
@@ -98,10 +98,23 @@ struct Geo {
 // staged P2G payload per particle: m, fx (weights recomputed in the scatter), b, A
 // (+ b_f, symmetric A_f in 7-channel mode)
 template <int NCH> constexpr int pay_floats() { return NCH == 4 ? 16 : 28; }
-#ifndef MSIM_CTAS_PER_SM
-#define MSIM_CTAS_PER_SM 5  // measured: 4 -> 1.12, 5 -> 1.05, 6 -> 1.10 ms per launch (config D, 256 envs)
+// Resident CTAs per SM (__launch_bounds__ -> register budget) and the L2
+// prefetch of the next round's particle, per instantiation. Dense buckets of the
+// reference's model in the 4-channel path (F = 1, !AM: D, A) run 6 CTAs at 80
+// registers without the prefetch (D +2.7 % against 5 CTAs at 96 with it); sparse
+// buckets / the material dispatch (E: 6 CTAs +7 %) and the 7-channel path keep
+// 5 with the prefetch (profiles/r02_experiments_D.txt).
+constexpr bool dense_clay(int NCH, int F, bool AM) { return NCH == 4 && F == 1 && !AM; }
+#ifdef MSIM_CTAS_PER_SM  // variant builds: one setting for every instantiation
+constexpr int ctas_per_sm(int, int, bool) { return MSIM_CTAS_PER_SM; }
+#else
+constexpr int ctas_per_sm(int NCH, int F, bool AM) { return dense_clay(NCH, F, AM) ? 6 : 5; }
 #endif
-constexpr int kCtasPerSm = MSIM_CTAS_PER_SM;
+#ifdef MSIM_NO_L2_PREFETCH
+constexpr bool l2_prefetch(int, int, bool) { return false; }
+#else
+constexpr bool l2_prefetch(int NCH, int F, bool AM) { return !dense_clay(NCH, F, AM); }
+#endif
 #ifdef MSIM_STATIC_ITEMS  // variant build: static round-robin bucket assignment
 constexpr bool kDynamicItems = false;
 #else
@@ -269,9 +282,8 @@ __device__ __forceinline__ void item_rounds(const SimParams& P, Smem<NCH, F>& S,
         const bool valid = t < rn;
         const int j = r0 + t;
         const int i = valid ? P.perm[j] : 0;
-#ifndef MSIM_NO_L2_PREFETCH  // L2 prefetch of this thread's next particle, one trip ahead (-1 %)
-        const int i_pf = j + IC.rstep < IC.e ? P.perm[j + IC.rstep] : -1;
-#endif
+        // L2 prefetch of this thread's next particle, one round ahead
+        const int i_pf = l2_prefetch(NCH, F, AM) && j + IC.rstep < IC.e ? P.perm[j + IC.rstep] : -1;
         unsigned meta = valid ? lds(&P.cur.meta[i]) : (1u << kLostBit);
         const int penv = (meta >> 8) & kEnvMask;
         const bool was_lost = meta >> kLostBit;
@@ -396,8 +408,7 @@ __device__ __forceinline__ void item_rounds(const SimParams& P, Smem<NCH, F>& S,
           if (AM) sts(&P.nxt.jp[j], jp);
           sts(&P.nxt.pid[j], pid);
         }
-#ifndef MSIM_NO_L2_PREFETCH
-        if (i_pf >= 0) {
+        if (l2_prefetch(NCH, F, AM) && i_pf >= 0) {
           auto pf = [](const void* a) { asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(a)); };
 #pragma unroll
           for (int a = 0; a < 3; ++a) pf(&P.cur.x[a][i_pf]);
@@ -408,7 +419,6 @@ __device__ __forceinline__ void item_rounds(const SimParams& P, Smem<NCH, F>& S,
           pf(&P.cur.meta[i_pf]);
           pf(&P.cur.pid[i_pf]);
         }
-#endif
 
         // ---------------- binning of the (new) position + P2G payload of the next cycle
         int key_new = P.n_keys - 1;
@@ -923,7 +933,7 @@ __device__ __forceinline__ void particles_cta(const SimParams& P, unsigned char*
 }
 
 template <int NCH, int F, bool AM, bool DET>
-__global__ void __launch_bounds__(kT, kCtasPerSm) k_particles(SimParams P) {
+__global__ void __launch_bounds__(kT, ctas_per_sm(NCH, F, AM)) k_particles(SimParams P) {
   pdl_wait();
   pdl_trigger();
   extern __shared__ __align__(16) unsigned char smem_raw[];
