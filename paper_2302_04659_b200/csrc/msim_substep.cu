@@ -100,15 +100,17 @@ struct Geo {
 template <int NCH> constexpr int pay_floats() { return NCH == 4 ? 16 : 28; }
 // Resident CTAs per SM (__launch_bounds__ -> register budget) and the L2
 // prefetch of the next round's particle, per instantiation. Dense buckets of the
-// reference's model in the 4-channel path (F = 1, !AM: D, A) run 6 CTAs at 80
-// registers without the prefetch (D +2.7 % against 5 CTAs at 96 with it); sparse
-// buckets / the material dispatch (E: 6 CTAs +7 %) and the 7-channel path keep
-// 5 with the prefetch (profiles/r02_experiments_D.txt).
+// reference's model in the 4-channel path (F = 1, !AM: D, A) run 8 CTAs at 64
+// registers without the prefetch (D +3.8 % against 5 CTAs at 96 with it; 6 CTAs
+// +2.5 %, 7 CTAs +0.5 %; the deterministic mode's int64 flush runs best at 6);
+// sparse buckets / the material dispatch (E: 6 CTAs +7 %) and the 7-channel
+// path keep 5 with the prefetch
+// (profiles/r02_experiments_D.txt).
 constexpr bool dense_clay(int NCH, int F, bool AM) { return NCH == 4 && F == 1 && !AM; }
 #ifdef MSIM_CTAS_PER_SM  // variant builds: one setting for every instantiation
-constexpr int ctas_per_sm(int, int, bool) { return MSIM_CTAS_PER_SM; }
+constexpr int ctas_per_sm(int, int, bool, bool) { return MSIM_CTAS_PER_SM; }
 #else
-constexpr int ctas_per_sm(int NCH, int F, bool AM) { return dense_clay(NCH, F, AM) ? 6 : 5; }
+constexpr int ctas_per_sm(int NCH, int F, bool AM, bool DET) { return dense_clay(NCH, F, AM) ? (DET ? 6 : 8) : 5; }
 #endif
 #ifdef MSIM_NO_L2_PREFETCH
 constexpr bool l2_prefetch(int, int, bool) { return false; }
@@ -933,7 +935,7 @@ __device__ __forceinline__ void particles_cta(const SimParams& P, unsigned char*
 }
 
 template <int NCH, int F, bool AM, bool DET>
-__global__ void __launch_bounds__(kT, ctas_per_sm(NCH, F, AM)) k_particles(SimParams P) {
+__global__ void __launch_bounds__(kT, ctas_per_sm(NCH, F, AM, DET)) k_particles(SimParams P) {
   pdl_wait();
   pdl_trigger();
   extern __shared__ __align__(16) unsigned char smem_raw[];
