@@ -99,23 +99,22 @@ struct Geo {
 // (+ b_f, symmetric A_f in 7-channel mode)
 template <int NCH> constexpr int pay_floats() { return NCH == 4 ? 16 : 28; }
 // Resident CTAs per SM (__launch_bounds__ -> register budget) and the L2
-// prefetch of the next round's particle, per instantiation. Dense buckets of the
-// reference's model in the 4-channel path (F = 1, !AM: D, A) run 8 CTAs at 64
-// registers without the prefetch (D +3.8 % against 5 CTAs at 96 with it; 6 CTAs
-// +2.5 %, 7 CTAs +0.5 %; the deterministic mode's int64 flush runs best at 6);
-// sparse buckets / the material dispatch (E: 6 CTAs +7 %) and the 7-channel
-// path keep 5 with the prefetch
-// (profiles/r02_experiments_D.txt).
-constexpr bool dense_clay(int NCH, int F, bool AM) { return NCH == 4 && F == 1 && !AM; }
+// prefetch of the next round's particle, per instantiation. Dense buckets
+// (F = 1) in the 4-channel path run 8 CTAs at 64 registers without the
+// prefetch: D +3.8 % against 5 CTAs at 96 with it (6 CTAs +2.5 %, 7 +0.5 %),
+// batched sand B +3 %; the deterministic twin runs best at 6 (its int64 flush).
+// Sparse 2^3-block buckets (E, C: 6 CTAs -7 %) and the 7-channel path keep 5
+// with the prefetch (profiles/r02_experiments_D.txt).
+constexpr bool dense_4ch(int NCH, int F) { return NCH == 4 && F == 1; }
 #ifdef MSIM_CTAS_PER_SM  // variant builds: one setting for every instantiation
-constexpr int ctas_per_sm(int, int, bool, bool) { return MSIM_CTAS_PER_SM; }
+constexpr int ctas_per_sm(int, int, bool) { return MSIM_CTAS_PER_SM; }
 #else
-constexpr int ctas_per_sm(int NCH, int F, bool AM, bool DET) { return dense_clay(NCH, F, AM) ? (DET ? 6 : 8) : 5; }
+constexpr int ctas_per_sm(int NCH, int F, bool DET) { return dense_4ch(NCH, F) ? (DET ? 6 : 8) : 5; }
 #endif
 #ifdef MSIM_NO_L2_PREFETCH
-constexpr bool l2_prefetch(int, int, bool) { return false; }
+constexpr bool l2_prefetch(int, int) { return false; }
 #else
-constexpr bool l2_prefetch(int NCH, int F, bool AM) { return !dense_clay(NCH, F, AM); }
+constexpr bool l2_prefetch(int NCH, int F) { return !dense_4ch(NCH, F); }
 #endif
 #ifdef MSIM_STATIC_ITEMS  // variant build: static round-robin bucket assignment
 constexpr bool kDynamicItems = false;
@@ -285,7 +284,7 @@ __device__ __forceinline__ void item_rounds(const SimParams& P, Smem<NCH, F>& S,
         const int j = r0 + t;
         const int i = valid ? P.perm[j] : 0;
         // L2 prefetch of this thread's next particle, one round ahead
-        const int i_pf = l2_prefetch(NCH, F, AM) && j + IC.rstep < IC.e ? P.perm[j + IC.rstep] : -1;
+        const int i_pf = l2_prefetch(NCH, F) && j + IC.rstep < IC.e ? P.perm[j + IC.rstep] : -1;
         unsigned meta = valid ? lds(&P.cur.meta[i]) : (1u << kLostBit);
         const int penv = (meta >> 8) & kEnvMask;
         const bool was_lost = meta >> kLostBit;
@@ -410,7 +409,7 @@ __device__ __forceinline__ void item_rounds(const SimParams& P, Smem<NCH, F>& S,
           if (AM) sts(&P.nxt.jp[j], jp);
           sts(&P.nxt.pid[j], pid);
         }
-        if (l2_prefetch(NCH, F, AM) && i_pf >= 0) {
+        if (l2_prefetch(NCH, F) && i_pf >= 0) {
           auto pf = [](const void* a) { asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(a)); };
 #pragma unroll
           for (int a = 0; a < 3; ++a) pf(&P.cur.x[a][i_pf]);
@@ -934,8 +933,11 @@ __device__ __forceinline__ void particles_cta(const SimParams& P, unsigned char*
   }
 }
 
-template <int NCH, int F, bool AM, bool DET>
-__global__ void __launch_bounds__(kT, ctas_per_sm(NCH, F, AM, DET)) k_particles(SimParams P) {
+// LAT: small scenes (split buckets, a few CTAs per SM busy): latency-bound, so
+// the 5-CTA register budget (fewer spills) instead of the dense instantiations'
+// 8 (single-scene B -3.6 % at 8)
+template <int NCH, int F, bool AM, bool DET, bool LAT = false>
+__global__ void __launch_bounds__(kT, LAT ? 5 : ctas_per_sm(NCH, F, DET)) k_particles(SimParams P) {
   pdl_wait();
   pdl_trigger();
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -1438,18 +1440,19 @@ struct Timed {
 };
 
 // persistent grid: as many CTAs as fit on the device at once (occupancy query)
-template <int NCH, int F, bool AM, bool DET = false>
+template <int NCH, int F, bool AM, bool DET = false, bool LAT = false>
 void launch_k_particles(const SimParams& P, cudaStream_t s) {
   static int per_sm = 0;
   if (!per_sm) {
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_particles<NCH, F, AM, DET>, kT, sizeof(Smem<NCH, F>));
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_particles<NCH, F, AM, DET, LAT>, kT,
+                                                  sizeof(Smem<NCH, F>));
     if (per_sm <= 0) per_sm = 1;
   }
   // the redo pass (speculated dt missed: rare) exits at once when no env redoes;
   // for small scenes one CTA per SM keeps that no-op launch cheap on the
   // per-cycle critical path (A -1 %)
   const int g = P.redo_pass && P.split_r > 1 ? sm_count() : sm_count() * per_sm;
-  launch_pdl(k_particles<NCH, F, AM, DET>, g, kT, sizeof(Smem<NCH, F>), s, P);
+  launch_pdl(k_particles<NCH, F, AM, DET, LAT>, g, kT, sizeof(Smem<NCH, F>), s, P);
 }
 
 template <bool AM>
@@ -1464,6 +1467,7 @@ void particle_kernel_m(const SimParams& P, cudaStream_t s) {
     else launch_k_particles<4, 2, AM>(P, s);
   } else {
     if (P.split) launch_k_particles<7, 1, AM>(P, s);
+    else if (P.split_r > 1) launch_k_particles<4, 1, AM, false, true>(P, s);
     else launch_k_particles<4, 1, AM>(P, s);
   }
 }
@@ -1484,14 +1488,14 @@ bool pdl_enabled() {
 }
 
 void configure_kernels() {
-#define MSIM_SET_SMEM(NCH, F, AM, DET)                                                              \
-  cudaFuncSetAttribute(k_particles<NCH, F, AM, DET>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+#define MSIM_SET_SMEM(NCH, F, AM, DET, ...)                                                                      \
+  cudaFuncSetAttribute(k_particles<NCH, F, AM, DET, ##__VA_ARGS__>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
                        (int)sizeof(Smem<NCH, F>))
   MSIM_SET_SMEM(4, 1, false, false); MSIM_SET_SMEM(7, 1, false, false); MSIM_SET_SMEM(4, 2, false, false);
   MSIM_SET_SMEM(7, 2, false, false); MSIM_SET_SMEM(4, 1, true, false); MSIM_SET_SMEM(7, 1, true, false);
   MSIM_SET_SMEM(4, 2, true, false); MSIM_SET_SMEM(7, 2, true, false);
   MSIM_SET_SMEM(4, 1, false, true); MSIM_SET_SMEM(4, 2, false, true); MSIM_SET_SMEM(4, 1, true, true);
-  MSIM_SET_SMEM(4, 2, true, true);
+  MSIM_SET_SMEM(4, 2, true, true); MSIM_SET_SMEM(4, 1, false, false, true); MSIM_SET_SMEM(4, 1, true, false, true);
 #undef MSIM_SET_SMEM
 }
 
