@@ -150,6 +150,10 @@ constexpr int kScatterDiUnroll = 1;
 #else
 constexpr int kScatterDiUnroll = 3;
 #endif
+#ifndef MSIM_TAIL_SPLIT  // parts per tail bucket (1: no tail split)
+#define MSIM_TAIL_SPLIT 4
+#endif
+constexpr int kTailSplit = MSIM_TAIL_SPLIT;
 #ifdef MSIM_G2P_ROLLED  // variant: G2P z-offset loop rolled
 constexpr int kG2pDkUnroll = 1;
 #else
@@ -164,7 +168,8 @@ struct ItemCtx {
   int key, benv, s, e, act, ox, oy, oz, s0, s1;
   float dt, dtp;
   int lostb, do_g2p, do_p2g, penalty;
-  int rstep;           // slot stride between this item's rounds (CAP x split_r)
+  int rstep;           // slot stride between this item's rounds (CAP x parts)
+  int split;           // the bucket's rounds are spread over several CTAs: atomic (unordered) ranks
   unsigned smask;      // env shapes (bit k = shape s0 + k, k < 32) that can reach the bucket box
   float blo[3], bhi[3];  // the bucket's particles' box widened by 2 h (positions after G2P)
 };
@@ -595,7 +600,7 @@ __device__ __forceinline__ void item_rounds(const SimParams& P, Smem<NCH, F>& S,
              // ranks are prefix counts in slot order, set after the round's barrier. The
              // (rare) movers take atomic ranks counted back from the end of their new bucket.
             // (split buckets: every particle takes an atomic rank, see particles_cta)
-            const bool stay = valid && key_new == IC.key && (P.split_r == 1 || IC.lostb);
+            const bool stay = valid && key_new == IC.key && !IC.split;
             const unsigned sb = __ballot_sync(FULL, stay);
             if (lane == 0) S.wball[rpar][t >> 5] = sb;
             const unsigned am = __ballot_sync(FULL, valid && !stay);
@@ -836,7 +841,15 @@ __device__ __forceinline__ void particles_cta(const SimParams& P, unsigned char*
   // deterministic mode's mover sort restores the slot order). The lost bucket is
   // not split (its particles stay in order).
   const int R = P.split_r;
-  const int nitems = *P.n_active_buckets * R;
+  const int nb = *P.n_active_buckets;
+  // Tail split (outside the deterministic mode and the small-scene split): with
+  // few buckets per CTA the last ncta buckets of the hand-out are split into
+  // kTailSplit parts each, so the launch ends evenly instead of waiting on whole
+  // last buckets; only those buckets lose their in-bucket order (atomic ranks).
+  // Batched C +2.8 %, B +1.8 %, D at 128 envs +1.1 %, E -0.8 %; off at D's 1024
+  // envs (~90 buckets per CTA: -0.5 %).
+  const int T = R == 1 && !P.det && kTailSplit > 1 && nb < 32 * ncta ? min(nb, ncta) : 0;
+  const int nitems = R > 1 ? nb * R : nb - T + T * kTailSplit;
 
   for (int t = tid; t < NCH * PN; t += kT) (&S.itile[0][0])[t] = 0;
   for (int t = tid; t < Gm::NBT; t += kT) S.bflag[t] = 0;
@@ -846,7 +859,13 @@ __device__ __forceinline__ void particles_cta(const SimParams& P, unsigned char*
   // atomic per further bucket): their sizes vary, and a static round-robin
   // leaves a tail of CTAs with more work (-12 % per launch at D).
   for (int item = cta; item < nitems;) {
-    const int bi = R > 1 ? item / R : item, part = item - bi * R;
+    int bi = item, part = 0, rr = 1;  // bucket, part, parts
+    if (R > 1) {
+      bi = item / R, part = item - bi * R, rr = R;
+    } else if (item >= nb - T) {
+      const int q = item - (nb - T);
+      bi = nb - T + q / kTailSplit, part = q - (q / kTailSplit) * kTailSplit, rr = kTailSplit;
+    }
     const int key = P.active_buckets[bi];
     const bool lostb = key == P.n_keys - 1;
     const int benv = lostb ? 0 : key / P.buckets_per_env;
@@ -901,7 +920,8 @@ __device__ __forceinline__ void particles_cta(const SimParams& P, unsigned char*
     if (tid < 6) (&S.maxb[0][0])[tid] = 0u;
     if (tid == 0) {
       S.penmax = 0u;
-      IC.key = key; IC.benv = benv; IC.s = s; IC.e = e; IC.act = act; IC.rstep = (lostb ? 1 : R) * CAP;
+      IC.key = key; IC.benv = benv; IC.s = s; IC.e = e; IC.act = act; IC.rstep = (lostb ? 1 : rr) * CAP;
+      IC.split = rr > 1 && !lostb;
       IC.ox = ox; IC.oy = oy; IC.oz = oz; IC.s0 = s0; IC.s1 = s1;
       IC.dt = dt; IC.dtp = dtp;
       IC.lostb = lostb; IC.do_g2p = do_g2p; IC.do_p2g = do_p2g; IC.penalty = penalty;
